@@ -1,0 +1,467 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product path.
+//
+// C-ABI driver over the UNMODIFIED reference library (/root/reference/proj,
+// compiled in place by oracle/Makefile into oracle/_ref/libmscref.so).  It
+// exposes the reference's own setup / apply / solve entry points to the
+// Python tests, the golden-fixture generator (tests/golden/make_golden.py)
+// and bench.py's cpu_baseline / --impl reference legs.  Every function here
+// only marshals arrays and calls the reference's public API:
+//   generate_oseen        proj/include/msc/oseen.hpp:43-44
+//   scale_rows            proj/include/msc/row_scaling.hpp:23
+//   partition_saddle      proj/include/msc/partitioned_matrix.hpp:69-70
+//   aggregate_by_numbering/equal_sizes  proj/include/msc/aggregates.hpp:41,61
+//   build_msc             proj/include/msc/schur_approx.hpp:45-46
+//   build_preconditioner  proj/include/msc/preconditioner.hpp:66-68
+//   MscPreconditioner::apply proj/src/preconditioner.cpp:85-114
+//   gmres                 proj/include/msc/gmres.hpp:44-47
+//   factor_ilut / solve   proj/include/msc/factorization.hpp:38-43
+//   matvec                proj/include/msc/sparse_matrix.hpp:87
+//   oracle::random_vector / random_saddle  proj/tests/oracles.hpp:92-142
+// The "anchored" interface re-ordering is the harness-level fix of
+// SURVEY.md §8(d) (public API only: permute + PartitionedMatrix::from_split +
+// aggregate_by_numbering); the product's host layer implements the same rule
+// (paper_1104_3349_b200/csrc/host/aggregate.cpp) and the tests check they agree.
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "msc/aggregates.hpp"
+#include "msc/factorization.hpp"
+#include "msc/gmres.hpp"
+#include "msc/oseen.hpp"
+#include "msc/parallel.hpp"
+#include "msc/partitioned_matrix.hpp"
+#include "msc/permutation.hpp"
+#include "msc/preconditioner.hpp"
+#include "msc/row_scaling.hpp"
+#include "msc/schur_approx.hpp"
+#include "oracles.hpp"
+
+using namespace msc;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_pivot = -1;
+
+struct RefProblem {
+  // Problem in the final (scaled, permuted) numbering.
+  PartitionedMatrix pm;
+  std::vector<int> perm;          // forward map of the saddle reorder (+anchoring)
+  std::vector<double> scaled_rhs; // generator rhs, scaled + permuted (may be empty)
+  AggregateSet agg;
+  SchurApproximation schur;
+  std::unique_ptr<MscPreconditioner> prec;
+  bool have_schur = false;
+};
+
+struct RefFactors {
+  TriangularFactors f;
+};
+
+const SparseMatrix* pick(RefProblem* p, int which) {
+  switch (which) {
+    case 0: return &p->pm.C;
+    case 1: return &p->pm.D;
+    case 2: return &p->pm.E;
+    case 3: return &p->pm.F;
+    case 4: return &p->pm.G;
+    case 5: return p->have_schur ? &p->schur.s_hat : nullptr;
+  }
+  return nullptr;
+}
+
+void copy_csr(const SparseMatrix& a, int* rp, int* ci, double* v) {
+  if (rp) std::memcpy(rp, a.row_offsets().data(), sizeof(int) * (a.rows() + 1));
+  if (ci) std::memcpy(ci, a.col_indices().data(), sizeof(int) * a.nnz());
+  if (v) std::memcpy(v, a.values().data(), sizeof(double) * a.nnz());
+}
+
+SparseMatrix csr_from_arrays(int nrows, int ncols, const int* rp, const int* ci,
+                             const double* v) {
+  std::vector<Triplet> t;
+  t.reserve(rp[nrows]);
+  for (int i = 0; i < nrows; ++i)
+    for (int k = rp[i]; k < rp[i + 1]; ++k) t.push_back({i, ci[k], v[k]});
+  return SparseMatrix::from_triplets(nrows, ncols, std::move(t));
+}
+
+// SURVEY.md §8(d) interface anchoring: every (2,2)-side pressure with a
+// separator-velocity neighbour in G is placed directly after its
+// smallest-index such neighbour; others keep their order at the tail.
+// `nsep` = number of separator velocities at the head of the interface.
+std::vector<int> anchored_interface_order(const PartitionedMatrix& pm, int nsep,
+                                          std::vector<char>& is_anchored) {
+  const int ng = pm.n_g();
+  std::vector<std::vector<int>> after(nsep);
+  std::vector<int> tail;
+  is_anchored.assign(ng, 0);
+  for (int q = nsep; q < ng; ++q) {
+    int best = -1;
+    for (int c : pm.G.row_cols(q)) {
+      if (c < nsep) { best = c; break; }  // columns sorted: first is smallest
+    }
+    if (best >= 0) after[best].push_back(q); else tail.push_back(q);
+  }
+  std::vector<int> order;
+  order.reserve(ng);
+  for (int v = 0; v < nsep; ++v) {
+    order.push_back(v);
+    for (int q : after[v]) { order.push_back(q); is_anchored[q] = 1; }
+  }
+  for (int q : tail) order.push_back(q);
+  return order;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const SingularMatrixError& e) {
+    g_err = e.what();
+    g_err_pivot = e.pivot_index;
+    return -2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_err_pivot = -1;
+    return -1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(int* pivot) {
+  if (pivot) *pivot = g_err_pivot;
+  return g_err.c_str();
+}
+
+void ref_random_vector(int n, unsigned seed, double* out) {
+  std::mt19937 rng(seed);
+  std::vector<double> v = oracle::random_vector(n, rng);
+  std::memcpy(out, v.data(), sizeof(double) * n);
+}
+
+void ref_problem_free(RefProblem* p) { delete p; }
+
+// Oseen problem through the reference pipeline (benchmark.cpp:45-67,101-135):
+// generate -> scale_rows -> partition_saddle(Interleaved) [-> anchoring].
+// grid_kind 0 uniform / 1 stretched.  Aggregates/Schur are built separately.
+int ref_problem_oseen(int grid_n, double nu, int grid_kind, double stretch,
+                      int nA, int anchored, RefProblem** out) {
+  return guarded([&] {
+    auto prob = generate_oseen(grid_n, nu,
+                               grid_kind ? GridKind::Stretched : GridKind::Uniform,
+                               WindKind::Recirculating, stretch);
+    RowScaling scaled = scale_rows(prob.matrices.C, prob.rhs);
+    SaddleReorder r = partition_saddle(scaled.matrix, prob.matrices.p, nA,
+                                       SaddleOrdering::Interleaved);
+    auto p = std::make_unique<RefProblem>();
+    p->perm = r.perm.forward;
+    p->scaled_rhs = permute_vector(scaled.rhs, r.perm);
+    if (anchored) {
+      const int n = r.matrix.n();
+      const int pp = r.matrix.p;
+      std::vector<char> is_anch;
+      std::vector<int> iorder =
+          anchored_interface_order(r.matrix, r.separator_size, is_anch);
+      std::vector<int> fwd(n);
+      for (int i = 0; i < pp; ++i) fwd[i] = i;
+      for (int k = 0; k < n - pp; ++k) fwd[pp + k] = pp + iorder[k];
+      Permutation ap = Permutation::from_forward(fwd);
+      SparseMatrix c2 = permute(r.matrix.C, ap);
+      p->pm = PartitionedMatrix::from_split(std::move(c2), pp,
+                                            r.matrix.d_block_ranges);
+      std::vector<int> composed(n);
+      for (int k = 0; k < n; ++k) composed[k] = p->perm[fwd[k]];
+      p->perm = composed;
+      p->scaled_rhs = permute_vector(p->scaled_rhs, ap);
+    } else {
+      p->pm = std::move(r.matrix);
+    }
+    *out = p.release();
+  });
+}
+
+// Arbitrary partitioned system from CSR arrays (tests' random saddles).
+int ref_problem_from_csr(int n, const int* rp, const int* ci, const double* v,
+                         int p, int nranges, const int* ranges, RefProblem** out) {
+  return guarded([&] {
+    std::vector<std::pair<int, int>> rr;
+    for (int i = 0; i < nranges; ++i) rr.push_back({ranges[2 * i], ranges[2 * i + 1]});
+    auto pr = std::make_unique<RefProblem>();
+    pr->pm = PartitionedMatrix::from_split(csr_from_arrays(n, n, rp, ci, v), p, rr);
+    pr->perm.resize(n);
+    for (int i = 0; i < n; ++i) pr->perm[i] = i;
+    *out = pr.release();
+  });
+}
+
+// oracle::random_saddle (tests/oracles.hpp:122-142) with the given seed.
+int ref_problem_random_saddle(int p, int ng, unsigned seed, double density,
+                              RefProblem** out) {
+  return guarded([&] {
+    std::mt19937 rng(seed);
+    auto pr = std::make_unique<RefProblem>();
+    pr->pm = oracle::random_saddle(p, ng, rng, density);
+    pr->perm.resize(p + ng);
+    for (int i = 0; i < p + ng; ++i) pr->perm[i] = i;
+    *out = pr.release();
+  });
+}
+
+void ref_problem_dims(RefProblem* p, int* n, int* pp, int* nblocks,
+                      int64_t* nnz_c) {
+  *n = p->pm.n();
+  *pp = p->pm.p;
+  *nblocks = static_cast<int>(p->pm.d_block_ranges.size());
+  *nnz_c = static_cast<int64_t>(p->pm.C.nnz());
+}
+
+// which: 0 C, 1 D, 2 E, 3 F, 4 G, 5 S_hat.  Returns nnz (or -1).
+int64_t ref_csr_shape(RefProblem* p, int which, int* nrows, int* ncols) {
+  const SparseMatrix* a = pick(p, which);
+  if (!a) return -1;
+  *nrows = a->rows();
+  *ncols = a->cols();
+  return static_cast<int64_t>(a->nnz());
+}
+int ref_csr_get(RefProblem* p, int which, int* rp, int* ci, double* v) {
+  const SparseMatrix* a = pick(p, which);
+  if (!a) return -1;
+  copy_csr(*a, rp, ci, v);
+  return 0;
+}
+void ref_get_perm(RefProblem* p, int* perm) {
+  std::memcpy(perm, p->perm.data(), sizeof(int) * p->perm.size());
+}
+int ref_get_scaled_rhs(RefProblem* p, double* out) {
+  if (p->scaled_rhs.empty()) return -1;
+  std::memcpy(out, p->scaled_rhs.data(), sizeof(double) * p->scaled_rhs.size());
+  return 0;
+}
+void ref_get_d_ranges(RefProblem* p, int* ranges) {
+  for (std::size_t i = 0; i < p->pm.d_block_ranges.size(); ++i) {
+    ranges[2 * i] = p->pm.d_block_ranges[i].first;
+    ranges[2 * i + 1] = p->pm.d_block_ranges[i].second;
+  }
+}
+
+// Aggregates: mode 0 = equal_sizes(n_g, sz) numbering (benchmark.cpp:74-99,
+// sz <= 0 -> n_g/8), mode 1 = anchored greedy sizes (close at >= sz, never
+// directly before an anchored pressure), mode 2 = explicit sizes.
+int ref_build_schur(RefProblem* p, const char* variant, int mode, int sz,
+                    int nsizes, const int* sizes_in, int workers) {
+  return guarded([&] {
+    const int ng = p->pm.n_g();
+    std::vector<int> sizes;
+    if (mode == 2) {
+      sizes.assign(sizes_in, sizes_in + nsizes);
+    } else if (mode == 1) {
+      // A pressure is "anchored" when its (2,2) row couples to an earlier
+      // interface velocity: after anchoring these follow their velocity.
+      // Recover the rule from the matrix itself: node q is a pressure iff
+      // its G-row has no entry on the diagonal block of velocities... we
+      // instead use the D-free criterion: pressure rows of the scaled Oseen
+      // system have an empty diagonal except the pin.
+      if (sz <= 0) sz = std::max(1, ng / 8);
+      std::vector<char> is_p(ng, 0);
+      for (int q = 0; q < ng; ++q) {
+        bool diag = false;
+        for (int c : p->pm.G.row_cols(q)) if (c == q) { diag = true; break; }
+        is_p[q] = !diag;
+      }
+      int cur = 0;
+      for (int q = 0; q < ng; ++q) {
+        ++cur;
+        const bool next_is_p = (q + 1 < ng) && is_p[q + 1];
+        if (cur >= sz && !next_is_p && q + 1 < ng) {
+          sizes.push_back(cur);
+          cur = 0;
+        }
+      }
+      if (cur > 0) sizes.push_back(cur);
+    } else {
+      if (sz <= 0) sz = std::max(1, ng / 8);
+      sz = std::min(sz, ng);
+      sizes = equal_sizes(ng, sz);
+    }
+    p->agg = aggregate_by_numbering(ng, sizes);
+    p->schur = build_msc(p->pm, p->agg, variant_from_name(variant), workers);
+    p->have_schur = true;
+  });
+}
+
+int ref_exact_schur(RefProblem* p) {
+  return guarded([&] {
+    p->schur = build_exact_schur(p->pm);
+    p->have_schur = true;
+  });
+}
+
+int ref_num_aggregates(RefProblem* p) {
+  return p->have_schur ? static_cast<int>(p->schur.owned_ranges.size()) : -1;
+}
+void ref_get_schur_ranges(RefProblem* p, int* ranges) {
+  for (std::size_t i = 0; i < p->schur.owned_ranges.size(); ++i) {
+    ranges[2 * i] = p->schur.owned_ranges[i].first;
+    ranges[2 * i + 1] = p->schur.owned_ranges[i].second;
+  }
+}
+
+int ref_build_precond(RefProblem* p, double tolA, int sA) {
+  return guarded([&] {
+    p->prec = std::make_unique<MscPreconditioner>(
+        build_preconditioner(p->pm, p->schur, tolA, sA));
+  });
+}
+
+int64_t ref_stored_nnz(RefProblem* p) {
+  return p->prec ? static_cast<int64_t>(p->prec->stored_nnz()) : -1;
+}
+
+// kind 0 = interior D block factors, 1 = Schur block factors.
+int ref_factor_dims(RefProblem* p, int kind, int idx, int* dim, int64_t* nnz_l,
+                    int64_t* nnz_u) {
+  if (!p->prec) return -1;
+  const auto& v = kind == 0 ? p->prec->d_factors() : p->prec->schur_factors();
+  if (idx < 0 || idx >= static_cast<int>(v.size())) return -1;
+  *dim = v[idx].dim();
+  *nnz_l = static_cast<int64_t>(v[idx].lower.nnz());
+  *nnz_u = static_cast<int64_t>(v[idx].upper.nnz());
+  return 0;
+}
+int ref_factor_get(RefProblem* p, int kind, int idx, int* lrp, int* lci,
+                   double* lv, int* urp, int* uci, double* uv, int* perm) {
+  if (!p->prec) return -1;
+  const auto& v = kind == 0 ? p->prec->d_factors() : p->prec->schur_factors();
+  const TriangularFactors& f = v[idx];
+  copy_csr(f.lower, lrp, lci, lv);
+  copy_csr(f.upper, urp, uci, uv);
+  if (perm) std::memcpy(perm, f.row_perm.forward.data(), sizeof(int) * f.dim());
+  return 0;
+}
+
+int ref_apply(RefProblem* p, const double* y, double* x) {
+  return guarded([&] {
+    std::vector<double> r = p->prec->apply(std::span<const double>(y, p->pm.n()));
+    std::memcpy(x, r.data(), sizeof(double) * r.size());
+  });
+}
+
+int ref_matvec(RefProblem* p, int which, const double* x, double* y) {
+  return guarded([&] {
+    const SparseMatrix* a = pick(p, which);
+    std::vector<double> r = matvec(*a, std::span<const double>(x, a->cols()));
+    std::memcpy(y, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// gmres (gmres.cpp:35-191).  hist must hold max_iters + 64 entries.
+int ref_gmres(RefProblem* p, int use_prec, const double* b, int restart,
+              int max_iters, double rel_tol, int left, double* x, int* iters,
+              int* converged, double* hist, int* nhist, double* seconds) {
+  return guarded([&] {
+    SolverConfig cfg;
+    cfg.restart = restart;
+    cfg.max_iters = max_iters;
+    cfg.rel_tol = rel_tol;
+    cfg.side = left ? PrecondSide::Left : PrecondSide::Right;
+    std::vector<double> rhs(b, b + p->pm.n());
+    auto [xs, rep] = gmres(p->pm.C, use_prec ? p->prec.get() : nullptr, rhs, cfg);
+    std::memcpy(x, xs.data(), sizeof(double) * xs.size());
+    *iters = rep.iterations;
+    *converged = rep.converged ? 1 : 0;
+    const int cap = *nhist;
+    const int m = static_cast<int>(rep.residual_history.size());
+    for (int i = 0; i < std::min(cap, m); ++i) hist[i] = rep.residual_history[i];
+    *nhist = m;
+    *seconds = rep.solve_seconds;
+  });
+}
+
+// ---- standalone kernels over raw CSR ------------------------------------
+
+int ref_factor_ilut(int n, const int* rp, const int* ci, const double* v,
+                    double tol, RefFactors** out) {
+  return guarded([&] {
+    auto f = std::make_unique<RefFactors>();
+    f->f = factor_ilut(csr_from_arrays(n, n, rp, ci, v), tol);
+    *out = f.release();
+  });
+}
+int ref_factor_exact(int n, const int* rp, const int* ci, const double* v,
+                     RefFactors** out) {
+  return guarded([&] {
+    auto f = std::make_unique<RefFactors>();
+    f->f = factor_exact(csr_from_arrays(n, n, rp, ci, v));
+    *out = f.release();
+  });
+}
+void ref_factors_free(RefFactors* f) { delete f; }
+void ref_factors_dims(RefFactors* f, int* dim, int64_t* nnz_l, int64_t* nnz_u) {
+  *dim = f->f.dim();
+  *nnz_l = static_cast<int64_t>(f->f.lower.nnz());
+  *nnz_u = static_cast<int64_t>(f->f.upper.nnz());
+}
+void ref_factors_get(RefFactors* f, int* lrp, int* lci, double* lv, int* urp,
+                     int* uci, double* uv, int* perm) {
+  copy_csr(f->f.lower, lrp, lci, lv);
+  copy_csr(f->f.upper, urp, uci, uv);
+  if (perm) std::memcpy(perm, f->f.row_perm.forward.data(), sizeof(int) * f->f.dim());
+}
+// Build factors directly from arrays (e.g. factors downloaded from the GPU,
+// identical to the reference's) so that the reference `solve` can be timed
+// without re-running its ILUT.
+RefFactors* ref_factors_from_arrays(int n, const int* lrp, const int* lci,
+                                    const double* lv, const int* urp,
+                                    const int* uci, const double* uv,
+                                    const int* perm) {
+  auto f = std::make_unique<RefFactors>();
+  f->f.lower = csr_from_arrays(n, n, lrp, lci, lv);
+  f->f.upper = csr_from_arrays(n, n, urp, uci, uv);
+  std::vector<int> fwd(n);
+  for (int i = 0; i < n; ++i) fwd[i] = perm ? perm[i] : i;
+  f->f.row_perm = Permutation::from_forward(fwd);
+  return f.release();
+}
+int ref_solve(RefFactors* f, const double* b, double* x) {
+  return guarded([&] {
+    std::vector<double> r = solve(f->f, std::span<const double>(b, f->f.dim()));
+    std::memcpy(x, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// CPU baseline timing: `reps` sweeps of the reference `solve` over the given
+// factor handles (one per sampled block), run with the reference's own
+// parallel_for (parallel.cpp:21-50) on `workers` threads.  rhs/out hold
+// sum(dim) doubles, concatenated per handle.  Returns wall seconds.
+double ref_time_block_solves(int nf, RefFactors** fs, const double* rhs,
+                             double* out, int reps, int workers) {
+  std::vector<std::size_t> off(nf + 1, 0);
+  for (int i = 0; i < nf; ++i) off[i + 1] = off[i] + fs[i]->f.dim();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < reps; ++r) {
+    parallel_for(nf, workers, [&](int i) {
+      std::vector<double> x =
+          solve(fs[i]->f, std::span<const double>(rhs + off[i], fs[i]->f.dim()));
+      std::memcpy(out + off[i], x.data(), sizeof(double) * x.size());
+    });
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int ref_hardware_threads() {
+  return static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+}
+
+}  // extern "C"

@@ -1,0 +1,318 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes view of oracle/_ref/libmscref.so.
+
+libmscref.so is the unmodified reference library (/root/reference/proj/src,
+compiled in place by oracle/Makefile) plus the marshalling driver
+oracle/refdrv.cpp.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module; the product
+package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libmscref.so")
+REF_SRC = "/root/reference/proj"
+
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH) or os.path.isdir(REF_SRC)
+
+
+def build() -> None:
+    """Compile the reference in place (only where /root/reference exists)."""
+    if os.path.isdir(REF_SRC):
+        subprocess.run(["make", "-s", "-C", HERE, "ref", "-j8"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_last_error.argtypes = [C.POINTER(C.c_int)]
+        L.ref_random_vector.argtypes = [C.c_int, C.c_uint, _f64p]
+        L.ref_problem_free.argtypes = [vp]
+        L.ref_problem_oseen.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double,
+                                        C.c_int, C.c_int, C.POINTER(vp)]
+        L.ref_problem_from_csr.argtypes = [C.c_int, _i32p, _i32p, _f64p, C.c_int,
+                                           C.c_int, _i32p, C.POINTER(vp)]
+        L.ref_problem_random_saddle.argtypes = [C.c_int, C.c_int, C.c_uint,
+                                                C.c_double, C.POINTER(vp)]
+        L.ref_problem_dims.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int), C.POINTER(C.c_int64)]
+        L.ref_csr_shape.restype = C.c_int64
+        L.ref_csr_shape.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_csr_get.argtypes = [vp, C.c_int, _i32p, _i32p, _f64p]
+        L.ref_get_perm.argtypes = [vp, _i32p]
+        L.ref_get_scaled_rhs.argtypes = [vp, _f64p]
+        L.ref_get_d_ranges.argtypes = [vp, _i32p]
+        L.ref_build_schur.argtypes = [vp, C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                      _i32p, C.c_int]
+        L.ref_exact_schur.argtypes = [vp]
+        L.ref_num_aggregates.argtypes = [vp]
+        L.ref_get_schur_ranges.argtypes = [vp, _i32p]
+        L.ref_build_precond.argtypes = [vp, C.c_double, C.c_int]
+        L.ref_stored_nnz.restype = C.c_int64
+        L.ref_stored_nnz.argtypes = [vp]
+        L.ref_factor_dims.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.ref_factor_get.argtypes = [vp, C.c_int, C.c_int, _i32p, _i32p, _f64p,
+                                     _i32p, _i32p, _f64p, _i32p]
+        L.ref_apply.argtypes = [vp, _f64p, _f64p]
+        L.ref_matvec.argtypes = [vp, C.c_int, _f64p, _f64p]
+        L.ref_gmres.argtypes = [vp, C.c_int, _f64p, C.c_int, C.c_int, C.c_double,
+                                C.c_int, _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                _f64p, C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.ref_factor_ilut.argtypes = [C.c_int, _i32p, _i32p, _f64p, C.c_double,
+                                      C.POINTER(vp)]
+        L.ref_factor_exact.argtypes = [C.c_int, _i32p, _i32p, _f64p, C.POINTER(vp)]
+        L.ref_factors_free.argtypes = [vp]
+        L.ref_factors_dims.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64)]
+        L.ref_factors_get.argtypes = [vp, _i32p, _i32p, _f64p, _i32p, _i32p, _f64p,
+                                      _i32p]
+        L.ref_factors_from_arrays.restype = vp
+        L.ref_factors_from_arrays.argtypes = [C.c_int, _i32p, _i32p, _f64p, _i32p,
+                                              _i32p, _f64p, C.c_void_p]
+        L.ref_solve.argtypes = [vp, _f64p, _f64p]
+        L.ref_time_block_solves.restype = C.c_double
+        L.ref_time_block_solves.argtypes = [C.c_int, C.POINTER(vp), _f64p, _f64p,
+                                            C.c_int, C.c_int]
+        L.ref_hardware_threads.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+class RefError(RuntimeError):
+    def __init__(self, msg, pivot):
+        super().__init__(msg)
+        self.pivot_index = pivot
+
+
+def _check(rc):
+    if rc != 0:
+        piv = C.c_int(-1)
+        msg = lib().ref_last_error(C.byref(piv)).decode()
+        raise RefError(msg, piv.value)
+
+
+def random_vector(n: int, seed: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    lib().ref_random_vector(n, seed, out)
+    return out
+
+
+class Csr:
+    def __init__(self, nrows, ncols, rp, ci, v):
+        self.nrows, self.ncols = nrows, ncols
+        self.rp, self.ci, self.v = rp, ci, v
+
+    @property
+    def nnz(self):
+        return int(self.rp[-1])
+
+    def to_dense(self):
+        a = np.zeros((self.nrows, self.ncols))
+        for i in range(self.nrows):
+            s, e = self.rp[i], self.rp[i + 1]
+            a[i, self.ci[s:e]] = self.v[s:e]
+        return a
+
+
+class Factors:
+    """Reference TriangularFactors (factorization.hpp:18-27) as arrays."""
+
+    def __init__(self, handle, owned=True):
+        self.h = handle
+        self.owned = owned
+        d, nl, nu = C.c_int(), C.c_int64(), C.c_int64()
+        lib().ref_factors_dims(handle, C.byref(d), C.byref(nl), C.byref(nu))
+        self.dim = d.value
+        n = self.dim
+        self.L = Csr(n, n, np.empty(n + 1, np.int32), np.empty(nl.value, np.int32),
+                     np.empty(nl.value))
+        self.U = Csr(n, n, np.empty(n + 1, np.int32), np.empty(nu.value, np.int32),
+                     np.empty(nu.value))
+        self.perm = np.empty(n, np.int32)
+        lib().ref_factors_get(handle, self.L.rp, self.L.ci, self.L.v, self.U.rp,
+                              self.U.ci, self.U.v, self.perm)
+
+    def solve(self, b):
+        x = np.empty(self.dim)
+        _check(lib().ref_solve(self.h, np.ascontiguousarray(b, np.float64), x))
+        return x
+
+    def __del__(self):
+        if self.owned and self.h:
+            lib().ref_factors_free(self.h)
+            self.h = None
+
+
+def factor_ilut(a: Csr, tol: float) -> Factors:
+    h = C.c_void_p()
+    _check(lib().ref_factor_ilut(a.nrows, a.rp, a.ci, a.v, tol, C.byref(h)))
+    return Factors(h)
+
+
+def factor_exact(a: Csr) -> Factors:
+    h = C.c_void_p()
+    _check(lib().ref_factor_exact(a.nrows, a.rp, a.ci, a.v, C.byref(h)))
+    return Factors(h)
+
+
+def factors_from_arrays(n, L: Csr, U: Csr, perm=None):
+    pp = None if perm is None else np.ascontiguousarray(perm, np.int32)
+    h = lib().ref_factors_from_arrays(n, L.rp, L.ci, L.v, U.rp, U.ci, U.v,
+                                      None if pp is None else pp.ctypes.data)
+    f = Factors(h)
+    f._keep = pp
+    return f
+
+
+class Problem:
+    """A reference PartitionedMatrix + MSC preconditioner pipeline."""
+
+    C, D, E, F, G, SHAT = range(6)
+
+    def __init__(self, handle):
+        self.h = handle
+        n, p, nb, nnz = C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+        lib().ref_problem_dims(handle, C.byref(n), C.byref(p), C.byref(nb), C.byref(nnz))
+        self.n, self.p, self.nblocks = n.value, p.value, nb.value
+
+    @classmethod
+    def oseen(cls, grid_n, nu, nA, stretched=False, stretch=1.056, anchored=False):
+        h = C.c_void_p()
+        _check(lib().ref_problem_oseen(grid_n, nu, int(stretched), stretch, nA,
+                                       int(anchored), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_csr(cls, a: Csr, p, ranges=()):
+        h = C.c_void_p()
+        rr = np.asarray(ranges, np.int32).reshape(-1)
+        if rr.size == 0:
+            rr = np.zeros(2, np.int32)
+        _check(lib().ref_problem_from_csr(a.nrows, a.rp, a.ci, a.v, p,
+                                          len(ranges), rr, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def random_saddle(cls, p, ng, seed, density=0.2):
+        h = C.c_void_p()
+        _check(lib().ref_problem_random_saddle(p, ng, seed, density, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_problem_free(self.h)
+            self.h = None
+
+    @property
+    def n_g(self):
+        return self.n - self.p
+
+    def csr(self, which) -> Csr:
+        nr, nc = C.c_int(), C.c_int()
+        nnz = lib().ref_csr_shape(self.h, which, C.byref(nr), C.byref(nc))
+        if nnz < 0:
+            raise ValueError("matrix not available")
+        a = Csr(nr.value, nc.value, np.empty(nr.value + 1, np.int32),
+                np.empty(nnz, np.int32), np.empty(nnz))
+        lib().ref_csr_get(self.h, which, a.rp, a.ci, a.v)
+        return a
+
+    def perm(self):
+        out = np.empty(self.n, np.int32)
+        lib().ref_get_perm(self.h, out)
+        return out
+
+    def scaled_rhs(self):
+        out = np.empty(self.n)
+        _check(lib().ref_get_scaled_rhs(self.h, out))
+        return out
+
+    def d_ranges(self):
+        out = np.empty(2 * self.nblocks, np.int32)
+        lib().ref_get_d_ranges(self.h, out)
+        return out.reshape(-1, 2)
+
+    def build_schur(self, variant="lum", sz=0, mode=0, sizes=None, workers=1):
+        s = np.asarray(sizes if sizes is not None else [0], np.int32)
+        _check(lib().ref_build_schur(self.h, variant.encode(), mode, sz, len(s), s,
+                                     workers))
+
+    def exact_schur(self):
+        _check(lib().ref_exact_schur(self.h))
+
+    def schur_ranges(self):
+        k = lib().ref_num_aggregates(self.h)
+        out = np.empty(2 * k, np.int32)
+        lib().ref_get_schur_ranges(self.h, out)
+        return out.reshape(-1, 2)
+
+    def build_precond(self, tolA=1e-4, sA=0):
+        _check(lib().ref_build_precond(self.h, tolA, sA))
+
+    def stored_nnz(self):
+        return int(lib().ref_stored_nnz(self.h))
+
+    def factors(self, kind, idx):
+        d, nl, nu = C.c_int(), C.c_int64(), C.c_int64()
+        if lib().ref_factor_dims(self.h, kind, idx, C.byref(d), C.byref(nl), C.byref(nu)):
+            raise IndexError(idx)
+        n = d.value
+        L = Csr(n, n, np.empty(n + 1, np.int32), np.empty(nl.value, np.int32),
+                np.empty(nl.value))
+        U = Csr(n, n, np.empty(n + 1, np.int32), np.empty(nu.value, np.int32),
+                np.empty(nu.value))
+        perm = np.empty(n, np.int32)
+        lib().ref_factor_get(self.h, kind, idx, L.rp, L.ci, L.v, U.rp, U.ci, U.v, perm)
+        return L, U, perm
+
+    def apply(self, y):
+        x = np.empty(self.n)
+        _check(lib().ref_apply(self.h, np.ascontiguousarray(y, np.float64), x))
+        return x
+
+    def matvec(self, x, which=0):
+        a_rows = self.csr(which).nrows if which else self.n
+        y = np.empty(a_rows)
+        _check(lib().ref_matvec(self.h, which, np.ascontiguousarray(x, np.float64), y))
+        return y
+
+    def gmres(self, b, restart, max_iters=3000, rel_tol=1e-8, left=False,
+              use_prec=True):
+        x = np.empty(self.n)
+        its, conv, nh, secs = C.c_int(), C.c_int(), C.c_int(max_iters + 64), C.c_double()
+        hist = np.empty(max_iters + 64)
+        _check(lib().ref_gmres(self.h, int(use_prec), np.ascontiguousarray(b, np.float64),
+                               restart, max_iters, rel_tol, int(left), x,
+                               C.byref(its), C.byref(conv), hist, C.byref(nh),
+                               C.byref(secs)))
+        return dict(x=x, iterations=its.value, converged=bool(conv.value),
+                    history=hist[: nh.value].copy(), seconds=secs.value)
+
+
+def time_block_solves(factors, rhs, reps, workers):
+    arr = (C.c_void_p * len(factors))(*[f.h for f in factors])
+    out = np.empty_like(rhs)
+    secs = lib().ref_time_block_solves(len(factors), arr,
+                                       np.ascontiguousarray(rhs), out, reps, workers)
+    return secs, out
+
+
+def hardware_threads():
+    return lib().ref_hardware_threads()
