@@ -1,0 +1,183 @@
+/*
+ * mscg.h — C ABI of the B200-native solve phase for the mini-Schur-complement
+ * (MSC) domain-decomposition preconditioner (arXiv:1104.3349).
+ *
+ * The reference (/root/reference/proj, CPU-only C++20) has no FFI: its
+ * boundary is the C++ API in proj/include/msc/.  Each entry point below is the
+ * plain-pointer form of the reference call it replaces (cited per function).
+ * The C++ drop-in layer (include/msc_b200/msc.hpp) re-exposes the reference
+ * signatures over these calls; Python binds them with ctypes
+ * (paper_1104_3349_b200/_capi.py).
+ *
+ * Conventions
+ *   - int32 CSR (row offsets, columns strictly increasing per row), fp64
+ *     values: the reference SparseMatrix layout (sparse_matrix.hpp:77-81).
+ *   - Every function returns an mscg_code; on failure *status (if non-null)
+ *     carries the code, the failing block and the zero-pivot index (reference
+ *     SingularMatrixError{pivot_index}, sparse_matrix.hpp:23-28) and a message
+ *     with the reference's wording (e.g. "build_preconditioner: (1,1) block 3:
+ *     factor_ilut: zero pivot at index 2207").
+ *   - Vectors passed with MSCG_MEM_HOST are host arrays (copied through
+ *     pinned staging); MSCG_MEM_DEVICE are device pointers on the handle's
+ *     device and stream.  There is no CPU fallback: without a CUDA device the
+ *     device entry points fail with MSCG_ERR_CUDA.
+ */
+#ifndef MSCG_H
+#define MSCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSCG_ABI_VERSION 1
+
+typedef enum {
+  MSCG_OK = 0,
+  MSCG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  MSCG_ERR_SINGULAR = 2,         /* SingularMatrixError */
+  MSCG_ERR_CUDA = 3,             /* no device / CUDA runtime failure */
+  MSCG_ERR_OUT_OF_MEMORY = 4,
+  MSCG_ERR_RUNTIME = 5           /* std::runtime_error */
+} mscg_code;
+
+typedef enum { MSCG_MEM_HOST = 0, MSCG_MEM_DEVICE = 1 } mscg_mem;
+
+typedef struct {
+  int code;
+  int block;        /* failing interior / Schur block, -1 if n/a */
+  int pivot_index;  /* zero pivot (local row), -1 if n/a */
+  char message[512];
+} mscg_status;
+
+typedef struct mscg_ctx mscg_ctx;         /* device, stream, scratch */
+typedef struct mscg_csr mscg_csr;         /* device-resident sparse matrix */
+typedef struct mscg_precond mscg_precond; /* device-resident MSC preconditioner */
+typedef struct mscg_problem mscg_problem; /* host setup: partitioned system */
+
+int mscg_abi_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+int mscg_ctx_create(int device, mscg_ctx **out, mscg_status *st);
+void mscg_ctx_destroy(mscg_ctx *ctx);
+/* cudaStream_t of the context (as void*), for callers that pass device ptrs. */
+void *mscg_ctx_stream(mscg_ctx *ctx);
+int mscg_ctx_synchronize(mscg_ctx *ctx, mscg_status *st);
+/* Kernels launched by this library since creation (evidence counter). */
+int64_t mscg_ctx_launches(mscg_ctx *ctx);
+
+/* ---- host problem layer (setup, once) -------------------- */
+/* generate_oseen(grid_n, nu, Uniform|Stretched, Recirculating, stretch)
+ * (oseen.hpp:43-44) -> scale_rows (row_scaling.hpp:23) ->
+ * partition_saddle(.., nA, Interleaved) (partitioned_matrix.hpp:69-70)
+ * [-> SURVEY §8(d) interface anchoring when anchored != 0]. */
+int mscg_problem_oseen(int grid_n, double nu, int stretched, double stretch,
+                       int n_a, int anchored, int threads, mscg_problem **out,
+                       mscg_status *st);
+/* PartitionedMatrix::from_split(C, p, d_ranges) (partitioned_matrix.hpp:28-29). */
+int mscg_problem_from_csr(int n, const int *rp, const int *ci, const double *v,
+                          int p, int nranges, const int *ranges,
+                          mscg_problem **out, mscg_status *st);
+void mscg_problem_destroy(mscg_problem *pb);
+void mscg_problem_dims(const mscg_problem *pb, int *n, int *p, int *nblocks,
+                       int64_t *nnz_c, int *separator_size);
+/* which: 0 = C (final numbering), 5 = S^ (after mscg_problem_build_schur).
+ * Pointers are borrowed (valid until the problem is destroyed). */
+int mscg_problem_csr(const mscg_problem *pb, int which, int *nrows, int *ncols,
+                     int64_t *nnz, const int **rp, const int **ci,
+                     const double **v);
+const int *mscg_problem_perm(const mscg_problem *pb);
+const int *mscg_problem_d_ranges(const mscg_problem *pb);   /* 2*nblocks */
+const double *mscg_problem_scaled_rhs(const mscg_problem *pb); /* or NULL */
+/* build_msc (schur_approx.hpp:45-46) for variant "lum" | "mscn" | "mscnr"
+ * with numbering aggregates.  mode 0: equal_sizes(n_g, sz) (sz<=0 -> n_g/8,
+ * benchmark.cpp:74-77); mode 1: anchored greedy sizes;
+ * mode 2: explicit sizes[nsizes]. */
+int mscg_problem_build_schur(mscg_problem *pb, const char *variant, int mode,
+                             int sz, int nsizes, const int *sizes, int threads,
+                             mscg_status *st);
+int mscg_problem_num_aggregates(const mscg_problem *pb);
+const int *mscg_problem_schur_ranges(const mscg_problem *pb); /* 2*nagg */
+
+/* ---- device sparse matrices ---------------------------------------------- */
+/* Upload CSR to HBM (SELL-32 slices for the SpMV kernel). */
+int mscg_csr_upload(mscg_ctx *ctx, int nrows, int ncols, const int *rp,
+                    const int *ci, const double *v, mscg_csr **out,
+                    mscg_status *st);
+void mscg_csr_destroy(mscg_csr *a);
+/* y = A x with the reference's row-sequential accumulation order
+ * (matvec, sparse_matrix.cpp:110-125): bit-identical results. */
+int mscg_spmv(mscg_csr *a, const double *x, double *y, int mem,
+              mscg_status *st);
+
+/* ---- MSC preconditioner ------------------------------------------------ */
+/* build_preconditioner(c, schur, tolA, sA) (preconditioner.hpp:66-68) over
+ * raw arrays: C (n x n, final numbering) split at p, interior block ranges,
+ * block-diagonal S^ (n_g x n_g) with its owned ranges.  Interior blocks with
+ * dim <= sA get the exact LU (factor_exact), the others ILUT(tolA)
+ * (factor_ilut, factorization.cpp:34-127), batched on the device. */
+int mscg_precond_build(mscg_ctx *ctx, int n, int p, const int *c_rp,
+                       const int *c_ci, const double *c_v, int nblocks,
+                       const int *d_ranges, const int *s_rp, const int *s_ci,
+                       const double *s_v, int nschur, const int *s_ranges,
+                       double tol_a, int s_a, mscg_precond **out,
+                       mscg_status *st);
+int mscg_precond_build_problem(mscg_ctx *ctx, const mscg_problem *pb,
+                               double tol_a, int s_a, mscg_precond **out,
+                               mscg_status *st);
+void mscg_precond_destroy(mscg_precond *pc);
+/* MscPreconditioner::apply (preconditioner.cpp:85-114): x = B^-1 y. */
+int mscg_precond_apply(mscg_precond *pc, const double *y, double *x, int mem,
+                       mscg_status *st);
+/* stored_nnz (preconditioner.cpp:116-121): factor nnz + nnz(E) + nnz(F). */
+int64_t mscg_precond_stored_nnz(const mscg_precond *pc);
+int mscg_precond_dims(const mscg_precond *pc, int *n, int *p, int *nblocks,
+                      int *nschur);
+/* Factor download for the d_factors()/schur_factors() accessors
+ * (preconditioner.hpp:41-44): kind 0 = interior blocks, 1 = Schur blocks.
+ * Reference layout: L strict lower, U with its diagonal first in each row,
+ * row_perm forward map.  Pass NULL arrays to query sizes only. */
+int mscg_precond_factor(const mscg_precond *pc, int kind, int idx, int *dim,
+                        int64_t *nnz_l, int64_t *nnz_u, int *lrp, int *lci,
+                        double *lv, int *urp, int *uci, double *uv, int *perm,
+                        mscg_status *st);
+/* Timing breakdown of the last build (seconds). */
+int mscg_precond_build_times(const mscg_precond *pc, double *ilut_s,
+                             double *schur_lu_s, double *pack_s);
+/* The operator matrix C of the preconditioner, resident on the device. */
+mscg_csr *mscg_precond_matrix(mscg_precond *pc);
+
+/* ---- restarted GMRES (gmres.hpp:44-47, gmres.cpp:35-191) -------------- */
+typedef struct {
+  int restart;      /* default 300 */
+  int max_iters;    /* default 3000 */
+  double rel_tol;   /* default 1e-9 */
+  int side;         /* 0 = right (default), 1 = left */
+  int orth;         /* 0 = MGS (reference order), 1 = CGS2 (fused multi-dot) */
+} mscg_gmres_config;
+
+typedef struct {
+  int iterations;
+  int converged;
+  int history_len;  /* residual_history entries written (<= hist_cap) */
+  int history_total;
+  double solve_seconds;
+  double final_true_residual;
+} mscg_gmres_report;
+
+/* A = operator on the device (usually mscg_precond_matrix(pc)); pc may be
+ * NULL for an unpreconditioned solve. */
+int mscg_gmres(mscg_ctx *ctx, mscg_csr *a, mscg_precond *pc, const double *b,
+               double *x, int mem, const mscg_gmres_config *cfg,
+               mscg_gmres_report *rep, double *history, int hist_cap,
+               mscg_status *st);
+/* true_residual (gmres.cpp:26-33). */
+int mscg_true_residual(mscg_ctx *ctx, mscg_csr *a, const double *x,
+                       const double *b, int mem, double *out, mscg_status *st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSCG_H */

@@ -1,0 +1,410 @@
+// C ABI (include/mscg.h) over the host setup layer and the device solve phase.
+// Maps C++ exceptions to mscg_status with the reference's error categories:
+// std::invalid_argument -> MSCG_ERR_INVALID_ARGUMENT, SingularMatrixError ->
+// MSCG_ERR_SINGULAR (+ block, pivot_index), CUDA failures -> MSCG_ERR_CUDA.
+#include "mscg.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "device/common.cuh"
+#include "device/internal.hpp"
+#include "host/setup.hpp"
+
+struct mscg_ctx {
+  mscg::Ctx ctx;
+  std::mutex mu;
+};
+struct mscg_csr {
+  std::unique_ptr<mscg::DevCsr> owned;
+  mscg::DevCsr* a = nullptr;
+  mscg_ctx* ctx = nullptr;
+};
+struct mscg_precond {
+  std::unique_ptr<mscg::Precond> pc;
+  mscg_ctx* ctx = nullptr;
+  mscg_csr matrix;  // borrowed view of pc->C
+};
+struct mscg_problem {
+  mscg::host::Partitioned pm;
+  std::vector<double> scaled_rhs;
+  bool have_schur = false;
+  mscg::host::SchurApprox schur;
+  std::vector<int> d_ranges_flat, s_ranges_flat;
+};
+
+namespace {
+
+void set_status(mscg_status* st, int code, const std::string& msg, int block = -1, int piv = -1) {
+  if (!st) return;
+  st->code = code;
+  st->block = block;
+  st->pivot_index = piv;
+  std::strncpy(st->message, msg.c_str(), sizeof(st->message) - 1);
+  st->message[sizeof(st->message) - 1] = 0;
+}
+
+template <class F>
+int guard(mscg_status* st, F&& f) {
+  try {
+    f();
+    set_status(st, MSCG_OK, "");
+    return MSCG_OK;
+  } catch (const mscg::Error& e) {
+    set_status(st, e.code, e.what(), e.block, e.pivot);
+    return e.code;
+  } catch (const mscg::host::SingularError& e) {
+    set_status(st, MSCG_ERR_SINGULAR, e.what(), -1, e.pivot);
+    return MSCG_ERR_SINGULAR;
+  } catch (const std::invalid_argument& e) {
+    set_status(st, MSCG_ERR_INVALID_ARGUMENT, e.what());
+    return MSCG_ERR_INVALID_ARGUMENT;
+  } catch (const std::bad_alloc& e) {
+    set_status(st, MSCG_ERR_OUT_OF_MEMORY, "host out of memory");
+    return MSCG_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    set_status(st, MSCG_ERR_RUNTIME, e.what());
+    return MSCG_ERR_RUNTIME;
+  }
+}
+
+void flatten(const std::vector<std::pair<int, int>>& r, std::vector<int>& out) {
+  out.clear();
+  for (auto [b, e] : r) {
+    out.push_back(b);
+    out.push_back(e);
+  }
+}
+
+std::vector<std::pair<int, int>> pairs(int n, const int* flat) {
+  std::vector<std::pair<int, int>> r;
+  for (int i = 0; i < n; ++i) r.push_back({flat[2 * i], flat[2 * i + 1]});
+  return r;
+}
+
+// Run `f(dev_in, dev_out)` with host or device vectors.
+template <class F>
+void with_vectors(mscg_ctx* c, const double* in, size_t nin, double* out, size_t nout, int mem,
+                  F&& f) {
+  cudaStream_t s = c->ctx.stream;
+  if (mem == MSCG_MEM_DEVICE) {
+    f(in, out);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  mscg::DevBuf din(sizeof(double) * std::max<size_t>(1, nin));
+  mscg::DevBuf dout(sizeof(double) * std::max<size_t>(1, nout));
+  double* stage = c->ctx.stage(std::max(nin, nout));
+  std::memcpy(stage, in, sizeof(double) * nin);
+  MSCG_CUDA(cudaMemcpyAsync(din.p, stage, sizeof(double) * nin, cudaMemcpyHostToDevice, s));
+  f(din.as<double>(), dout.as<double>());
+  MSCG_CUDA(cudaMemcpyAsync(stage, dout.p, sizeof(double) * nout, cudaMemcpyDeviceToHost, s));
+  MSCG_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(out, stage, sizeof(double) * nout);
+}
+
+}  // namespace
+
+extern "C" {
+
+int mscg_abi_version(void) { return MSCG_ABI_VERSION; }
+
+int mscg_ctx_create(int device, mscg_ctx** out, mscg_status* st) {
+  return guard(st, [&] {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      throw mscg::Error(MSCG_ERR_CUDA, std::string("no CUDA device available (") +
+                                           cudaGetErrorString(e) + "); this library has no CPU path");
+    if (device < 0 || device >= count) throw std::invalid_argument("mscg_ctx_create: bad device");
+    auto c = std::make_unique<mscg_ctx>();
+    c->ctx.device = device;
+    MSCG_CUDA(cudaSetDevice(device));
+    MSCG_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
+    MSCG_CUDA(cudaDeviceGetAttribute(&c->ctx.sm_count, cudaDevAttrMultiProcessorCount, device));
+    *out = c.release();
+  });
+}
+
+void mscg_ctx_destroy(mscg_ctx* ctx) { delete ctx; }
+void* mscg_ctx_stream(mscg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->ctx.stream) : nullptr; }
+int mscg_ctx_synchronize(mscg_ctx* ctx, mscg_status* st) {
+  return guard(st, [&] { MSCG_CUDA(cudaStreamSynchronize(ctx->ctx.stream)); });
+}
+int64_t mscg_ctx_launches(mscg_ctx* ctx) { return ctx ? ctx->ctx.launches : 0; }
+
+// ---- host problem layer ---------------------------------------------------
+
+int mscg_problem_oseen(int grid_n, double nu, int stretched, double stretch, int n_a,
+                       int anchored, int threads, mscg_problem** out, mscg_status* st) {
+  return guard(st, [&] {
+    auto pb = std::make_unique<mscg_problem>();
+    mscg::host::OseenSystem sys = mscg::host::generate_oseen(grid_n, nu, stretched != 0, stretch);
+    mscg::host::scale_rows(sys.C, sys.rhs);
+    pb->pm = mscg::host::partition_saddle(sys.C, sys.p, n_a, threads);
+    if (anchored) mscg::host::anchor_interface(pb->pm);
+    pb->scaled_rhs.resize(sys.rhs.size());
+    for (size_t k = 0; k < sys.rhs.size(); ++k) pb->scaled_rhs[k] = sys.rhs[pb->pm.perm[k]];
+    flatten(pb->pm.d_ranges, pb->d_ranges_flat);
+    *out = pb.release();
+  });
+}
+
+int mscg_problem_from_csr(int n, const int* rp, const int* ci, const double* v, int p,
+                          int nranges, const int* ranges, mscg_problem** out, mscg_status* st) {
+  return guard(st, [&] {
+    if (n < 0 || p < 0 || p > n) throw std::invalid_argument("PartitionedMatrix: split out of range");
+    auto pb = std::make_unique<mscg_problem>();
+    mscg::host::Csr& c = pb->pm.C;
+    c = mscg::host::Csr(n, n);
+    c.rp.assign(rp, rp + n + 1);
+    c.ci.assign(ci, ci + rp[n]);
+    c.v.assign(v, v + rp[n]);
+    pb->pm.p = p;
+    if (nranges > 0) pb->pm.d_ranges = pairs(nranges, ranges);
+    else pb->pm.d_ranges = {{0, p}};
+    pb->pm.perm.resize(n);
+    for (int i = 0; i < n; ++i) pb->pm.perm[i] = i;
+    flatten(pb->pm.d_ranges, pb->d_ranges_flat);
+    *out = pb.release();
+  });
+}
+
+void mscg_problem_destroy(mscg_problem* pb) { delete pb; }
+
+void mscg_problem_dims(const mscg_problem* pb, int* n, int* p, int* nblocks, int64_t* nnz_c,
+                       int* separator_size) {
+  if (n) *n = pb->pm.n();
+  if (p) *p = pb->pm.p;
+  if (nblocks) *nblocks = static_cast<int>(pb->pm.d_ranges.size());
+  if (nnz_c) *nnz_c = pb->pm.C.nnz();
+  if (separator_size) *separator_size = pb->pm.separator_size;
+}
+
+int mscg_problem_csr(const mscg_problem* pb, int which, int* nrows, int* ncols, int64_t* nnz,
+                     const int** rp, const int** ci, const double** v) {
+  const mscg::host::Csr* a = nullptr;
+  if (which == 0) a = &pb->pm.C;
+  if (which == 5 && pb->have_schur) a = &pb->schur.s_hat;
+  if (!a) return MSCG_ERR_INVALID_ARGUMENT;
+  *nrows = a->nrows;
+  *ncols = a->ncols;
+  *nnz = a->nnz();
+  *rp = a->rp.data();
+  *ci = a->ci.data();
+  *v = a->v.data();
+  return MSCG_OK;
+}
+
+const int* mscg_problem_perm(const mscg_problem* pb) { return pb->pm.perm.data(); }
+const int* mscg_problem_d_ranges(const mscg_problem* pb) { return pb->d_ranges_flat.data(); }
+const double* mscg_problem_scaled_rhs(const mscg_problem* pb) {
+  return pb->scaled_rhs.empty() ? nullptr : pb->scaled_rhs.data();
+}
+
+int mscg_problem_build_schur(mscg_problem* pb, const char* variant, int mode, int sz, int nsizes,
+                             const int* sizes, int threads, mscg_status* st) {
+  return guard(st, [&] {
+    const int ng = pb->pm.n_g();
+    std::vector<int> sz_list;
+    if (mode == 2) {
+      sz_list.assign(sizes, sizes + nsizes);
+    } else if (mode == 1) {
+      sz_list = mscg::host::anchored_sizes(pb->pm, sz);
+    } else {
+      int s = sz <= 0 ? std::max(1, ng / 8) : sz;
+      s = std::min(s, ng);
+      sz_list = mscg::host::equal_sizes(ng, s);
+    }
+    pb->schur = mscg::host::build_msc(pb->pm, sz_list,
+                                      mscg::host::variant_from_name(variant ? variant : ""),
+                                      threads);
+    pb->have_schur = true;
+    flatten(pb->schur.ranges, pb->s_ranges_flat);
+  });
+}
+
+int mscg_problem_num_aggregates(const mscg_problem* pb) {
+  return pb->have_schur ? static_cast<int>(pb->schur.ranges.size()) : -1;
+}
+const int* mscg_problem_schur_ranges(const mscg_problem* pb) {
+  return pb->have_schur ? pb->s_ranges_flat.data() : nullptr;
+}
+
+// ---- device sparse matrices ---------------------------------------------
+
+int mscg_csr_upload(mscg_ctx* ctx, int nrows, int ncols, const int* rp, const int* ci,
+                    const double* v, mscg_csr** out, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx) throw std::invalid_argument("mscg_csr_upload: null context");
+    if (nrows < 0 || ncols < 0) throw std::invalid_argument("SparseMatrix: negative dimension");
+    auto h = std::make_unique<mscg_csr>();
+    h->owned = mscg::upload_csr(&ctx->ctx, nrows, ncols, rp, ci, v);
+    h->a = h->owned.get();
+    h->ctx = ctx;
+    *out = h.release();
+  });
+}
+
+void mscg_csr_destroy(mscg_csr* a) { delete a; }
+
+int mscg_spmv(mscg_csr* a, const double* x, double* y, int mem, mscg_status* st) {
+  return guard(st, [&] {
+    if (!a) throw std::invalid_argument("matvec: null matrix");
+    with_vectors(a->ctx, x, a->a->ncols, y, a->a->nrows, mem, [&](const double* dx, double* dy) {
+      mscg::spmv(*a->a, dx, dy, nullptr, 0, a->ctx->ctx.stream);
+    });
+  });
+}
+
+// ---- preconditioner ------------------------------------------------------
+
+int mscg_precond_build(mscg_ctx* ctx, int n, int p, const int* c_rp, const int* c_ci,
+                       const double* c_v, int nblocks, const int* d_ranges, const int* s_rp,
+                       const int* s_ci, const double* s_v, int nschur, const int* s_ranges,
+                       double tol_a, int s_a, mscg_precond** out, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx) throw std::invalid_argument("build_preconditioner: null context");
+    if (tol_a < 0.0) throw std::invalid_argument("factor_ilut: negative drop tolerance");
+    auto h = std::make_unique<mscg_precond>();
+    h->ctx = ctx;
+    h->pc = mscg::build_precond(&ctx->ctx, n, p, c_rp, c_ci, c_v, pairs(nblocks, d_ranges), s_rp,
+                                s_ci, s_v, pairs(nschur, s_ranges), tol_a, s_a);
+    h->matrix.a = h->pc->C.get();
+    h->matrix.ctx = ctx;
+    *out = h.release();
+  });
+}
+
+int mscg_precond_build_problem(mscg_ctx* ctx, const mscg_problem* pb, double tol_a, int s_a,
+                               mscg_precond** out, mscg_status* st) {
+  if (!pb || !pb->have_schur) {
+    set_status(st, MSCG_ERR_INVALID_ARGUMENT,
+               "build_preconditioner: Schur approximation does not match the split");
+    return MSCG_ERR_INVALID_ARGUMENT;
+  }
+  const auto& c = pb->pm.C;
+  const auto& s = pb->schur.s_hat;
+  return mscg_precond_build(ctx, c.nrows, pb->pm.p, c.rp.data(), c.ci.data(), c.v.data(),
+                            static_cast<int>(pb->pm.d_ranges.size()), pb->d_ranges_flat.data(),
+                            s.rp.data(), s.ci.data(), s.v.data(),
+                            static_cast<int>(pb->schur.ranges.size()), pb->s_ranges_flat.data(),
+                            tol_a, s_a, out, st);
+}
+
+void mscg_precond_destroy(mscg_precond* pc) { delete pc; }
+
+int mscg_precond_apply(mscg_precond* pc, const double* y, double* x, int mem, mscg_status* st) {
+  return guard(st, [&] {
+    if (!pc) throw std::invalid_argument("MscPreconditioner::apply: null preconditioner");
+    const size_t n = pc->pc->n;
+    with_vectors(pc->ctx, y, n, x, n, mem, [&](const double* dy, double* dx) {
+      pc->pc->apply(dy, dx, pc->ctx->ctx.stream);
+    });
+  });
+}
+
+int64_t mscg_precond_stored_nnz(const mscg_precond* pc) { return pc ? pc->pc->stored_nnz : -1; }
+
+int mscg_precond_dims(const mscg_precond* pc, int* n, int* p, int* nblocks, int* nschur) {
+  if (!pc) return MSCG_ERR_INVALID_ARGUMENT;
+  if (n) *n = pc->pc->n;
+  if (p) *p = pc->pc->p;
+  if (nblocks) *nblocks = pc->pc->D ? pc->pc->D->nblocks : 0;
+  if (nschur) *nschur = pc->pc->S ? pc->pc->S->nblocks : 0;
+  return MSCG_OK;
+}
+
+int mscg_precond_factor(const mscg_precond* pc, int kind, int idx, int* dim, int64_t* nnz_l,
+                        int64_t* nnz_u, int* lrp, int* lci, double* lv, int* urp, int* uci,
+                        double* uv, int* perm, mscg_status* st) {
+  return guard(st, [&] {
+    const mscg::FactorSet* fs = kind == 0 ? pc->pc->D.get() : pc->pc->S.get();
+    if (!fs || idx < 0 || idx >= fs->nblocks) throw std::invalid_argument("factor index out of range");
+    const int d = fs->h_dim[idx];
+    if (dim) *dim = d;
+    if (nnz_l) *nnz_l = fs->h_loff[idx + 1] - fs->h_loff[idx];
+    if (nnz_u) *nnz_u = fs->h_uoff[idx + 1] - fs->h_uoff[idx] + d;
+    if (!lrp) return;
+    std::vector<int> a, b2, c2, d2, e2;
+    std::vector<double> f2, g2;
+    mscg::download_factor(*fs, idx, a, b2, f2, c2, d2, g2, e2);
+    std::memcpy(lrp, a.data(), sizeof(int) * a.size());
+    std::memcpy(lci, b2.data(), sizeof(int) * b2.size());
+    std::memcpy(lv, f2.data(), sizeof(double) * f2.size());
+    std::memcpy(urp, c2.data(), sizeof(int) * c2.size());
+    std::memcpy(uci, d2.data(), sizeof(int) * d2.size());
+    std::memcpy(uv, g2.data(), sizeof(double) * g2.size());
+    if (perm) std::memcpy(perm, e2.data(), sizeof(int) * e2.size());
+  });
+}
+
+int mscg_precond_build_times(const mscg_precond* pc, double* ilut_s, double* schur_lu_s,
+                             double* pack_s) {
+  if (!pc) return MSCG_ERR_INVALID_ARGUMENT;
+  if (ilut_s) *ilut_s = pc->pc->times.ilut_s;
+  if (schur_lu_s) *schur_lu_s = pc->pc->times.lu_s;
+  if (pack_s) *pack_s = pc->pc->times.pack_s;
+  return MSCG_OK;
+}
+
+mscg_csr* mscg_precond_matrix(mscg_precond* pc) { return pc ? &pc->matrix : nullptr; }
+
+// ---- GMRES -----------------------------------------------------------------
+
+int mscg_gmres(mscg_ctx* ctx, mscg_csr* a, mscg_precond* pc, const double* b, double* x, int mem,
+               const mscg_gmres_config* cfg, mscg_gmres_report* rep, double* history,
+               int hist_cap, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx || !a) throw std::invalid_argument("gmres: null context or matrix");
+    mscg::GmresConfig c;
+    if (cfg) {
+      c.restart = cfg->restart;
+      c.max_iters = cfg->max_iters;
+      c.rel_tol = cfg->rel_tol;
+      c.left = cfg->side == 1;
+      c.orth = cfg->orth;
+    }
+    const size_t n = a->a->nrows;
+    if (a->a->ncols != static_cast<int>(n)) throw std::invalid_argument("gmres: dimension mismatch");
+    mscg::GmresResult r;
+    auto run = [&](const double* db, double* dx) {
+      r = mscg::gmres(&ctx->ctx, *a->a, pc ? pc->pc.get() : nullptr, db, dx, c);
+    };
+    with_vectors(ctx, b, n, x, n, mem, run);
+    if (rep) {
+      rep->iterations = r.iterations;
+      rep->converged = r.converged ? 1 : 0;
+      rep->history_total = static_cast<int>(r.history.size());
+      rep->history_len = std::min<int>(hist_cap, rep->history_total);
+      rep->solve_seconds = r.seconds;
+      rep->final_true_residual = r.final_true;
+    }
+    if (history)
+      for (int i = 0; i < std::min<int>(hist_cap, static_cast<int>(r.history.size())); ++i)
+        history[i] = r.history[i];
+  });
+}
+
+int mscg_true_residual(mscg_ctx* ctx, mscg_csr* a, const double* x, const double* b, int mem,
+                       double* out, mscg_status* st) {
+  return guard(st, [&] {
+    const size_t n = a->a->nrows;
+    if (mem == MSCG_MEM_DEVICE) {
+      *out = mscg::true_residual(&ctx->ctx, *a->a, x, b);
+      return;
+    }
+    mscg::DevBuf dx(sizeof(double) * std::max<size_t>(1, a->a->ncols)),
+        db(sizeof(double) * std::max<size_t>(1, n));
+    MSCG_CUDA(cudaMemcpy(dx.p, x, sizeof(double) * a->a->ncols, cudaMemcpyHostToDevice));
+    MSCG_CUDA(cudaMemcpy(db.p, b, sizeof(double) * n, cudaMemcpyHostToDevice));
+    *out = mscg::true_residual(&ctx->ctx, *a->a, dx.as<double>(), db.as<double>());
+  });
+}
+
+}  // extern "C"

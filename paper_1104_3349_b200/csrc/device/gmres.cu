@@ -1,0 +1,435 @@
+// Restarted GMRES on the device (reference gmres, proj/src/gmres.cpp:35-191).
+//
+// The Arnoldi step keeps every vector in HBM and every scalar on the device:
+//   w = A B^-1 v_j            (precond apply + SELL SpMV, right preconditioning)
+//   orthogonalisation         CGS2: two fused multi-dot + multi-axpy passes
+//                             (h = V^T w; w -= V h, twice), or MGS in the
+//                             reference's order (one fused axpy+dot kernel per
+//                             basis vector)
+//   h_{j+1,j} = ||w||, v_{j+1} = w / h_{j+1,j}
+//   Givens rotation + residual estimate: one single-thread kernel
+// Reductions are two-stage and deterministic (fixed per-CTA partials summed in
+// CTA order by the last CTA).  The host reads one 32-byte status record per
+// iteration (the reference's convergence test needs it); no other host
+// synchronisation happens inside a cycle.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace mscg {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Reducer {
+  double* partials;        // [nvec][nblk]
+  unsigned int* counter;   // last-block detection
+  int nblk;
+};
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kThreads / 32; ++w) r += sh[w];
+  return r;  // valid in thread 0
+}
+
+// Finalise: the last CTA to arrive sums partials[i][*] in CTA order.
+__device__ __forceinline__ bool last_block(Reducer red) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(red.counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  return is_last;
+}
+
+// out[i] (i < nvec) = sum over CTAs of partials[i][cta]; scale: out = f(sum).
+__device__ void finish(Reducer red, int nvec, double* out, int mode) {
+  __threadfence();
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < red.nblk; ++c) s += red.partials[static_cast<size_t>(i) * red.nblk + c];
+    out[i] = mode == 1 ? sqrt(s) : s;
+  }
+  if (threadIdx.x == 0) *red.counter = 0u;
+}
+
+// ||x||_2 -> *out
+__global__ void __launch_bounds__(kThreads) nrm2_kernel(int n, const double* __restrict__ x,
+                                                        Reducer red, double* out) {
+  __shared__ double sh[kThreads / 32];
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    acc = fma(x[i], x[i], acc);
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) red.partials[blockIdx.x] = s;
+  if (last_block(red)) finish(red, 1, out, 1);
+}
+
+// h[i] = V_i . w for i < nv  (one pass over w and the nv basis vectors)
+__global__ void __launch_bounds__(kThreads) multidot_kernel(int n, int nv, const double* __restrict__ V,
+                                                            size_t ld, const double* __restrict__ w,
+                                                            Reducer red, double* h) {
+  __shared__ double sh[kThreads / 32];
+  for (int i = 0; i < nv; ++i) {
+    const double* vi = V + ld * i;
+    double acc = 0.0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+      acc = fma(vi[r], w[r], acc);
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) red.partials[static_cast<size_t>(i) * red.nblk + blockIdx.x] = s;
+  }
+  if (last_block(red)) finish(red, nv, h, 0);
+}
+
+// w -= sum_i h[i] V_i ; optionally H(:,j) += h (accum into column) by CTA 0.
+__global__ void __launch_bounds__(kThreads) multiaxpy_kernel(int n, int nv, const double* __restrict__ V,
+                                                             size_t ld, const double* __restrict__ h,
+                                                             double* __restrict__ w, double* hcol,
+                                                             int accumulate) {
+  __shared__ double sh[512];
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) sh[i] = h[i];
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double acc = w[r];
+    for (int i = 0; i < nv; ++i) acc = fma(-sh[i], V[ld * i + r], acc);
+    w[r] = acc;
+  }
+  if (blockIdx.x == 0 && hcol)
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hcol[i] = accumulate ? hcol[i] + sh[i] : sh[i];
+}
+
+// MGS step (reference order, gmres.cpp:112-116), fused: apply the previous
+// projection w -= h_prev v_{i-1} and accumulate v_i . w in the same pass.
+__global__ void __launch_bounds__(kThreads) mgs_kernel(int n, const double* __restrict__ vprev,
+                                                       const double* hprev, const double* __restrict__ vi,
+                                                       double* __restrict__ w, Reducer red, double* hout) {
+  __shared__ double sh[kThreads / 32];
+  const double hp = vprev ? *hprev : 0.0;
+  double acc = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double wr = w[r];
+    if (vprev) {
+      wr = __dsub_rn(wr, __dmul_rn(hp, vprev[r]));
+      w[r] = wr;
+    }
+    if (vi) acc = fma(vi[r], wr, acc);
+  }
+  if (!vi) return;
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) red.partials[blockIdx.x] = s;
+  if (last_block(red)) finish(red, 1, hout, 0);
+}
+
+// y = x / s  (s on device)
+__global__ void scale_div_kernel(int n, const double* __restrict__ x, const double* s,
+                                 double* __restrict__ y) {
+  const double d = *s;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = x[i] / d;
+}
+
+// z = sum_j y_j V_j with the reference's per-entry order (gmres.cpp:158-161).
+__global__ void combine_kernel(int n, int m, const double* __restrict__ V, size_t ld,
+                               const double* __restrict__ y, double* __restrict__ z) {
+  __shared__ double sy[512];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) sy[j] = y[j];
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, __dmul_rn(sy[j], V[ld * j + r]));
+    z[r] = acc;
+  }
+}
+
+__global__ void axpy1_kernel(int n, const double* __restrict__ z, double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = x[i] + z[i];
+}
+
+__global__ void fill_kernel(int n, double v, double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = v;
+}
+
+// Small dense state: H column-major (m+1) x m, cs, sn, g.
+struct Small {
+  double* H;
+  double* cs;
+  double* sn;
+  double* g;
+  double* y;
+  double* scal;   // [0] hnext, [1] beta, [2] tmp norm, ...
+  double* status; // [0] rel, [1] breakdown, [2] hnext, [3] |g_{j+1}|
+  int m;
+};
+
+// v_{j+1} = w / hnext (if hnext >= 1e-14), Givens update of column j
+// (gmres.cpp:117-148), single thread.
+__global__ void givens_kernel(Small s, int j, double denom) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int ld = s.m + 1;
+  double* Hc = s.H + static_cast<size_t>(j) * ld;
+  const double hnext = s.scal[0];
+  Hc[j + 1] = hnext;
+  const bool breakdown = !(hnext >= 1e-14);
+  for (int i = 0; i < j; ++i) {
+    const double t1 = s.cs[i] * Hc[i] + s.sn[i] * Hc[i + 1];
+    const double t2 = -s.sn[i] * Hc[i] + s.cs[i] * Hc[i + 1];
+    Hc[i] = t1;
+    Hc[i + 1] = t2;
+  }
+  const double dr = hypot(Hc[j], Hc[j + 1]);
+  s.cs[j] = dr == 0.0 ? 1.0 : Hc[j] / dr;
+  s.sn[j] = dr == 0.0 ? 0.0 : Hc[j + 1] / dr;
+  Hc[j] = dr;
+  Hc[j + 1] = 0.0;
+  s.g[j + 1] = -s.sn[j] * s.g[j];
+  s.g[j] = s.cs[j] * s.g[j];
+  s.status[0] = fabs(s.g[j + 1]) / denom;
+  s.status[1] = breakdown ? 1.0 : 0.0;
+  s.status[2] = hnext;
+}
+
+// Back substitution H y = g (gmres.cpp:152-157).
+__global__ void backsolve_kernel(Small s, int m) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int ld = s.m + 1;
+  for (int i = m - 1; i >= 0; --i) {
+    double acc = s.g[i];
+    for (int j = i + 1; j < m; ++j) acc -= s.H[static_cast<size_t>(j) * ld + i] * s.y[j];
+    s.y[i] = acc / s.H[static_cast<size_t>(i) * ld + i];
+  }
+}
+
+__global__ void init_cycle_kernel(Small s, const double* beta) {
+  for (int i = threadIdx.x; i <= s.m; i += blockDim.x) s.g[i] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) s.g[0] = *beta;
+}
+
+struct Vec {
+  DevBuf buf;
+  double* p() const { return buf.as<double>(); }
+};
+
+struct Workspace {
+  Ctx* ctx;
+  int n, nblk;
+  DevBuf partials, counter, small;
+  Reducer red;
+  explicit Workspace(Ctx* c, int n_, int maxvec) : ctx(c), n(n_) {
+    nblk = std::max(1, std::min(c->sm_count * 4, (n + kThreads - 1) / kThreads));
+    partials = DevBuf(sizeof(double) * static_cast<size_t>(nblk) * std::max(1, maxvec));
+    counter = DevBuf(sizeof(unsigned int) * 4);
+    MSCG_CUDA(cudaMemsetAsync(counter.p, 0, counter.bytes, c->stream));
+    red = {partials.as<double>(), counter.as<unsigned int>(), nblk};
+  }
+  void nrm2(const double* x, double* out) {
+    nrm2_kernel<<<nblk, kThreads, 0, ctx->stream>>>(n, x, red, out);
+    MSCG_CUDA(cudaGetLastError());
+    ctx->launches++;
+  }
+  double host_nrm2(const double* x, double* dev_slot) {
+    nrm2(x, dev_slot);
+    double h = 0;
+    MSCG_CUDA(cudaMemcpyAsync(&h, dev_slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MSCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return h;
+  }
+  int grid() const { return nblk; }
+};
+
+}  // namespace
+
+double true_residual(Ctx* ctx, const DevCsr& a, const double* x, const double* b) {
+  const int n = a.nrows;
+  Workspace ws(ctx, n, 1);
+  DevBuf r(sizeof(double) * std::max(1, n)), slot(sizeof(double) * 2);
+  spmv(a, x, r.as<double>(), b, 1, ctx->stream);
+  const double rn = ws.host_nrm2(r.as<double>(), slot.as<double>());
+  const double bn = ws.host_nrm2(b, slot.as<double>() + 1);
+  return bn == 0.0 ? rn : rn / bn;
+}
+
+GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, double* x,
+                  const GmresConfig& cfg) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  const int n = a.nrows;
+  if (a.ncols != n) throw Error(1, "gmres: dimension mismatch");
+  if (pc && pc->n != n) throw Error(1, "gmres: preconditioner dimension mismatch");
+  if (cfg.restart < 1 || !(cfg.rel_tol > 0.0) || cfg.max_iters < 1)
+    throw Error(1, "gmres: bad solver configuration");
+  if (cfg.restart > 500) throw Error(1, "gmres: restart above 500 is not supported");
+  cudaStream_t s = ctx->stream;
+  const int m = cfg.restart;
+  const bool left = pc && cfg.left, right = pc && !cfg.left;
+  GmresResult res;
+
+  Workspace ws(ctx, n, m + 2);
+  const int G = ws.grid();
+  const size_t ld = static_cast<size_t>(n);
+  DevBuf V(sizeof(double) * ld * (m + 1)), w(sizeof(double) * n), tmp(sizeof(double) * n);
+  DevBuf small(sizeof(double) * (static_cast<size_t>(m + 1) * m + 4 * (m + 1) + 64));
+  double* sp = small.as<double>();
+  Small st;
+  st.m = m;
+  st.H = sp;
+  st.cs = st.H + static_cast<size_t>(m + 1) * m;
+  st.sn = st.cs + (m + 1);
+  st.g = st.sn + (m + 1);
+  st.y = st.g + (m + 1);
+  st.scal = st.y + (m + 1);
+  st.status = st.scal + 16;
+  double* hbuf = st.scal + 32;  // scratch for multidot results (<= m+1)
+  DevBuf hscratch(sizeof(double) * (m + 2));
+  MSCG_CUDA(cudaMemsetAsync(small.p, 0, small.bytes, s));
+  fill_kernel<<<G, kThreads, 0, s>>>(n, 0.0, x);
+  ctx->launches++;
+  (void)hbuf;
+
+  auto apply_op = [&](const double* in, double* out) {
+    // out = A B^-1 in (right) | B^-1 A in (left) | A in
+    if (right) {
+      pc->apply(in, tmp.as<double>(), s);
+      spmv(a, tmp.as<double>(), out, nullptr, 0, s);
+    } else if (left) {
+      spmv(a, in, tmp.as<double>(), nullptr, 0, s);
+      pc->apply(tmp.as<double>(), out, s);
+    } else {
+      spmv(a, in, out, nullptr, 0, s);
+    }
+  };
+
+  const double norm_b = ws.host_nrm2(b, st.scal + 2);
+  if (norm_b == 0.0) {
+    res.converged = true;
+    res.history.push_back(0.0);
+    res.seconds = std::chrono::duration<double>(clk::now() - t0).count();
+    return res;
+  }
+  double denom = norm_b;
+  if (left) {
+    pc->apply(b, w.as<double>(), s);
+    denom = ws.host_nrm2(w.as<double>(), st.scal + 2);
+  }
+  if (denom == 0.0) denom = norm_b;
+
+  double last_true = 1.0, prev_cycle_true = -1.0;
+  bool done = false;
+  double* vbase = V.as<double>();
+  while (!done) {
+    // r = b - A x (into V_0), left: B^-1 r.
+    spmv(a, x, vbase, b, 1, s);
+    if (left) {
+      MSCG_CUDA(cudaMemcpyAsync(tmp.as<double>(), vbase, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      pc->apply(tmp.as<double>(), vbase, s);
+    }
+    const double beta = ws.host_nrm2(vbase, st.scal + 1);
+    const double rel0 = beta / denom;
+    if (res.history.empty()) res.history.push_back(rel0);
+    if (rel0 <= cfg.rel_tol) {
+      last_true = true_residual(ctx, a, x, b);
+      res.converged = last_true <= cfg.rel_tol;
+      break;
+    }
+    scale_div_kernel<<<G, kThreads, 0, s>>>(n, vbase, st.scal + 1, vbase);
+    init_cycle_kernel<<<1, 128, 0, s>>>(st, st.scal + 1);
+    ctx->launches += 2;
+
+    int mm = 0;
+    bool breakdown = false, inner_conv = false;
+    for (int j = 0; j < m && res.iterations < cfg.max_iters; ++j) {
+      double* vj = vbase + ld * j;
+      double* wp = w.as<double>();
+      apply_op(vj, wp);
+      double* Hc = st.H + static_cast<size_t>(j) * (m + 1);
+      if (cfg.orth == 0) {
+        // MGS: for i <= j: h_ij = v_i . w ; w -= h_ij v_i (fused pairwise).
+        for (int i = 0; i <= j; ++i) {
+          mgs_kernel<<<G, kThreads, 0, s>>>(n, i ? vbase + ld * (i - 1) : nullptr,
+                                            i ? Hc + (i - 1) : nullptr, vbase + ld * i, wp,
+                                            ws.red, Hc + i);
+          ctx->launches++;
+        }
+        mgs_kernel<<<G, kThreads, 0, s>>>(n, vbase + ld * j, Hc + j, nullptr, wp, ws.red, nullptr);
+        ctx->launches++;
+      } else {
+        // CGS2: h = V^T w; w -= V h; twice, H(:,j) = h1 + h2.
+        for (int pass = 0; pass < 2; ++pass) {
+          multidot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
+                                                 hscratch.as<double>());
+          multiaxpy_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, hscratch.as<double>(), wp,
+                                                  Hc, pass);
+          ctx->launches += 2;
+        }
+      }
+      ws.nrm2(wp, st.scal + 0);
+      // v_{j+1} = w / hnext, enqueued before the status read so it overlaps;
+      // on breakdown the (unused) vector is simply never referenced.
+      scale_div_kernel<<<G, kThreads, 0, s>>>(n, wp, st.scal + 0, vbase + ld * (j + 1));
+      givens_kernel<<<1, 32, 0, s>>>(st, j, denom);
+      ctx->launches += 2;
+      double status[3];
+      MSCG_CUDA(cudaMemcpyAsync(status, st.status, sizeof(status), cudaMemcpyDeviceToHost, s));
+      MSCG_CUDA(cudaStreamSynchronize(s));
+      breakdown = status[1] != 0.0;
+      ++res.iterations;
+      mm = j + 1;
+      const double rel = status[0];
+      res.history.push_back(rel);
+      if (breakdown || rel <= cfg.rel_tol) {
+        inner_conv = rel <= cfg.rel_tol;
+        break;
+      }
+    }
+    backsolve_kernel<<<1, 32, 0, s>>>(st, mm);
+    double* z = w.as<double>();
+    combine_kernel<<<G, kThreads, 0, s>>>(n, mm, vbase, ld, st.y, z);
+    ctx->launches += 2;
+    if (right) {
+      pc->apply(z, tmp.as<double>(), s);
+      z = tmp.as<double>();
+    }
+    axpy1_kernel<<<G, kThreads, 0, s>>>(n, z, x);
+    ctx->launches++;
+    last_true = true_residual(ctx, a, x, b);
+    if (last_true <= cfg.rel_tol) {
+      res.converged = true;
+      done = true;
+    } else if (breakdown) {
+      res.converged = false;
+      done = true;
+    } else if (res.iterations >= cfg.max_iters) {
+      res.converged = false;
+      done = true;
+    } else if (inner_conv) {
+      if (prev_cycle_true >= 0.0 && last_true >= 0.999 * prev_cycle_true) {
+        res.converged = false;
+        done = true;
+      }
+    }
+    prev_cycle_true = last_true;
+  }
+  res.history.push_back(last_true);
+  res.final_true = last_true;
+  MSCG_CUDA(cudaStreamSynchronize(s));
+  res.seconds = std::chrono::duration<double>(clk::now() - t0).count();
+  return res;
+}
+
+}  // namespace mscg

@@ -1,0 +1,151 @@
+// Internal C++ interfaces between the C ABI (csrc/capi.cpp) and the device
+// code (csrc/device/*.cu).  Nothing here is exported.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <utility>
+#include <vector>
+
+namespace mscg {
+
+// Owning device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n);
+  ~DevBuf();
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept;
+  template <class T> T* as() const { return static_cast<T*>(p); }
+  void reset();
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  int64_t launches = 0;
+  // pinned staging for host<->device vector traffic
+  double* pinned = nullptr;
+  size_t pinned_elems = 0;
+  double* stage(size_t elems);
+  ~Ctx();
+};
+
+// Device CSR kept in SELL-32 (slices of 32 rows, column-major inside a slice)
+// so that a warp reads 32 consecutive entries per step while each lane keeps
+// the reference's row-sequential accumulation order.
+struct DevCsr {
+  Ctx* ctx = nullptr;
+  int nrows = 0, ncols = 0;
+  int64_t nnz = 0;
+  int nslices = 0;
+  DevBuf slice_ptr;    // int64[nslices+1] entry offsets
+  DevBuf slice_width;  // int32[nslices]
+  DevBuf col;          // int32 (-1 = padding)
+  DevBuf val;          // fp64
+  int64_t padded = 0;
+};
+std::unique_ptr<DevCsr> upload_csr(Ctx* ctx, int nrows, int ncols, const int* rp,
+                                   const int* ci, const double* v);
+// y = A x                        (mode 0)
+// y = base - A x                 (mode 1)
+void spmv(const DevCsr& a, const double* x, double* y, const double* base, int mode,
+          cudaStream_t s);
+
+// Per-block factors in the solve layout: every block's L (and U) rows are
+// contiguous; columns are block-local uint16; U rows hold only off-diagonal
+// entries, the diagonal sits in udiag.  Row metadata is indexed by
+// row0[b] + b + i (dim+1 offsets per block, relative to the block base).
+struct FactorSet {
+  int nblocks = 0;
+  int total_rows = 0;
+  int max_dim = 0;
+  bool has_perm = false;
+  std::vector<int> h_row0, h_dim;          // host copies
+  std::vector<int64_t> h_loff, h_uoff;     // per block entry offsets (+1 total)
+  std::vector<char> h_exact;               // per block: exact LU (1) or ILUT (0)
+  DevBuf row0, dim;                        // int32[nblocks]
+  DevBuf loff, uoff;                       // int64[nblocks+1]
+  DevBuf lrp, urp;                         // int32[total_rows + nblocks]
+  DevBuf lval, uval;                       // fp64
+  DevBuf lcol, ucol;                       // uint16
+  DevBuf udiag;                            // fp64[total_rows]
+  DevBuf perm;                             // int32[total_rows] (local), if has_perm
+  int64_t nnz_l() const { return h_loff.empty() ? 0 : h_loff.back(); }
+  int64_t nnz_u() const { return h_uoff.empty() ? 0 : h_uoff.back(); }
+};
+
+// Block descriptor for factorisation input: rows [row0, row0+dim) of a CSR
+// matrix whose block-local columns are [col0, col0+dim).
+struct BlockSpec {
+  int row0, dim, col0;
+};
+
+struct FactorTimes {
+  double ilut_s = 0, lu_s = 0, pack_s = 0;
+};
+
+// Factor all blocks of `a_rp/a_ci/a_v` (device CSR arrays, int32) listed in
+// `blocks`: ILUT(tol) where exact[b] == 0, dense partial-pivoting LU where
+// exact[b] == 1.  Throws Error(SINGULAR) naming the first failing block.
+// `what` prefixes error messages ("(1,1) block" / "Schur block").
+std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a_ci,
+                                         const double* a_v,
+                                         const std::vector<BlockSpec>& blocks,
+                                         const std::vector<char>& exact, double tol,
+                                         const char* what, FactorTimes* times);
+
+// x_b = U_b^-1 L_b^-1 P_b rhs_b for every block b, launched as one kernel
+// (one CTA per block).  out = x, or out = sub - x when sub != nullptr.
+void block_trisolve(const FactorSet& fs, const double* rhs, double* out,
+                    const double* sub, cudaStream_t s);
+
+struct Precond {
+  Ctx* ctx = nullptr;
+  int n = 0, p = 0;
+  std::unique_ptr<DevCsr> C, E, F;
+  std::unique_ptr<FactorSet> D, S;
+  int64_t stored_nnz = 0;
+  FactorTimes times;
+  DevBuf z1, t, w;  // scratch (apply is stream-ordered on ctx->stream)
+  void apply(const double* y_dev, double* x_dev, cudaStream_t s);
+};
+
+std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
+                                       const int* c_ci, const double* c_v,
+                                       const std::vector<std::pair<int, int>>& d_ranges,
+                                       const int* s_rp, const int* s_ci,
+                                       const double* s_v,
+                                       const std::vector<std::pair<int, int>>& s_ranges,
+                                       double tol_a, int s_a);
+
+// Download one block's factors in the reference layout.
+void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
+                     std::vector<int>& lci, std::vector<double>& lv,
+                     std::vector<int>& urp, std::vector<int>& uci,
+                     std::vector<double>& uv, std::vector<int>& perm);
+
+struct GmresConfig {
+  int restart = 300, max_iters = 3000;
+  double rel_tol = 1e-9;
+  bool left = false;
+  int orth = 1;
+};
+struct GmresResult {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> history;
+  double seconds = 0, final_true = 0;
+};
+GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b_dev,
+                  double* x_dev, const GmresConfig& cfg);
+double true_residual(Ctx* ctx, const DevCsr& a, const double* x_dev, const double* b_dev);
+
+}  // namespace mscg

@@ -1,0 +1,145 @@
+// MSC preconditioner on the device: build (build_preconditioner,
+// proj/src/preconditioner.cpp:26-83) and apply (MscPreconditioner::apply,
+// proj/src/preconditioner.cpp:85-114, the paper's Alg. 2):
+//
+//   z1 = D^-1 y1                 block_trisolve over the interior blocks
+//   t  = y2 - F z1               SELL SpMV with fused subtraction
+//   z2 = S^-1 t  (-> x2)         block_trisolve over the Schur blocks (row_perm)
+//   w  = E z2                    SELL SpMV
+//   x1 = z1 - D^-1 w             block_trisolve with fused subtraction
+//
+// Five stream-ordered launches, no host synchronisation.
+#include <algorithm>
+#include <chrono>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace mscg {
+
+namespace {
+
+// Extract the rectangular block A[rb:re, cb:ce) of a host CSR (re-indexed).
+void extract(const int* rp, const int* ci, const double* v, int rb, int re, int cb, int ce,
+             std::vector<int>& orp, std::vector<int>& oci, std::vector<double>& ov) {
+  orp.assign(re - rb + 1, 0);
+  oci.clear();
+  ov.clear();
+  for (int i = rb; i < re; ++i) {
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] >= cb && ci[k] < ce) {
+        oci.push_back(ci[k] - cb);
+        ov.push_back(v[k]);
+      }
+    orp[i - rb + 1] = static_cast<int>(oci.size());
+  }
+}
+
+struct DevArrays {
+  DevBuf rp, ci, v;
+  DevArrays(Ctx* ctx, int nrows, const int* hrp, const int* hci, const double* hv) {
+    const int64_t nnz = hrp[nrows];
+    rp = DevBuf(sizeof(int) * (nrows + 1));
+    ci = DevBuf(sizeof(int) * std::max<int64_t>(1, nnz));
+    v = DevBuf(sizeof(double) * std::max<int64_t>(1, nnz));
+    MSCG_CUDA(cudaMemcpyAsync(rp.p, hrp, sizeof(int) * (nrows + 1), cudaMemcpyHostToDevice, ctx->stream));
+    if (nnz) {
+      MSCG_CUDA(cudaMemcpyAsync(ci.p, hci, sizeof(int) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+      MSCG_CUDA(cudaMemcpyAsync(v.p, hv, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+    }
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
+                                       const int* c_ci, const double* c_v,
+                                       const std::vector<std::pair<int, int>>& d_ranges,
+                                       const int* s_rp, const int* s_ci,
+                                       const double* s_v,
+                                       const std::vector<std::pair<int, int>>& s_ranges,
+                                       double tol_a, int s_a) {
+  if (p < 0 || p > n) throw Error(1, "build_preconditioner: split out of range");
+  if (d_ranges.empty()) throw Error(1, "build_preconditioner: no interior D blocks");
+  const int ng = n - p;
+  {
+    int cov = 0;
+    for (auto [b, e] : d_ranges) {
+      if (b != cov || e <= b || e > p)
+        throw Error(1, "build_preconditioner: interior block ranges must tile [0, p)");
+      cov = e;
+    }
+    if (cov != p) throw Error(1, "build_preconditioner: interior block ranges must tile [0, p)");
+    cov = 0;
+    for (auto [b, e] : s_ranges) {
+      if (b != cov || e <= b || e > ng)
+        throw Error(1, "build_preconditioner: Schur ranges must tile [0, n_g)");
+      cov = e;
+    }
+    if (cov != ng)
+      throw Error(1, "build_preconditioner: Schur approximation does not match the split");
+  }
+  auto pc = std::make_unique<Precond>();
+  pc->ctx = ctx;
+  pc->n = n;
+  pc->p = p;
+  pc->C = upload_csr(ctx, n, n, c_rp, c_ci, c_v);
+  {
+    std::vector<int> rp, ci;
+    std::vector<double> v;
+    extract(c_rp, c_ci, c_v, 0, p, p, n, rp, ci, v);  // E = C[0:p, p:n]
+    pc->E = upload_csr(ctx, p, ng, rp.data(), ci.data(), v.data());
+    extract(c_rp, c_ci, c_v, p, n, 0, p, rp, ci, v);  // F = C[p:n, 0:p]
+    pc->F = upload_csr(ctx, ng, p, rp.data(), ci.data(), v.data());
+  }
+  // Interior blocks: ILUT(tolA) or exact LU when dim <= sA (:44-56).
+  {
+    DevArrays c(ctx, n, c_rp, c_ci, c_v);
+    std::vector<BlockSpec> blocks;
+    std::vector<char> exact;
+    for (auto [b, e] : d_ranges) {
+      blocks.push_back({b, e - b, b});
+      exact.push_back((e - b) <= s_a ? 1 : 0);
+    }
+    pc->D = factor_blocks(ctx, c.rp.as<int>(), c.ci.as<int>(), c.v.as<double>(), blocks, exact,
+                          tol_a, "build_preconditioner: (1,1) block", &pc->times);
+  }
+  // Schur blocks: exact LU per owned range (:68-81).
+  if (ng > 0) {
+    DevArrays sm(ctx, ng, s_rp, s_ci, s_v);
+    std::vector<BlockSpec> blocks;
+    std::vector<char> exact;
+    for (auto [b, e] : s_ranges) {
+      blocks.push_back({b, e - b, b});
+      exact.push_back(1);
+    }
+    pc->S = factor_blocks(ctx, sm.rp.as<int>(), sm.ci.as<int>(), sm.v.as<double>(), blocks, exact,
+                          0.0, "build_preconditioner: Schur block", &pc->times);
+  }
+  pc->stored_nnz = pc->E->nnz + pc->F->nnz + pc->D->nnz_l() + pc->D->nnz_u() + p;
+  if (pc->S) pc->stored_nnz += pc->S->nnz_l() + pc->S->nnz_u() + ng;
+  pc->z1 = DevBuf(sizeof(double) * std::max(1, p));
+  pc->t = DevBuf(sizeof(double) * std::max(1, ng));
+  pc->w = DevBuf(sizeof(double) * std::max(1, p));
+  return pc;
+}
+
+void Precond::apply(const double* y, double* x, cudaStream_t s) {
+  double* z1 = this->z1.as<double>();
+  double* t = this->t.as<double>();
+  double* w = this->w.as<double>();
+  block_trisolve(*D, y, z1, nullptr, s);
+  ctx->launches++;
+  if (S) {
+    spmv(*F, z1, t, y + p, 1, s);
+    block_trisolve(*S, t, x + p, nullptr, s);
+    ctx->launches++;
+    spmv(*E, x + p, w, nullptr, 0, s);
+    block_trisolve(*D, w, x, z1, s);
+    ctx->launches++;
+  } else {
+    MSCG_CUDA(cudaMemcpyAsync(x, z1, sizeof(double) * p, cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+}  // namespace mscg

@@ -1,0 +1,263 @@
+// Host problem layer, part 3: aggregates over the interface numbering and
+// the mini-Schur-complement approximation S^ (setup, once).
+//
+//   equal_sizes              proj/src/aggregates.cpp:132-141
+//   aggregate_by_numbering   proj/src/aggregates.cpp:36-48
+//   build_msc (MSCN/MSCNR/LUM, numbering aggregates)
+//                            proj/src/schur_approx.cpp:88-161
+// MSCN/MSCNR need an exact LU of each aggregate's D-side companion block;
+// that is done here with the reference's dense LU (dense_matrix.cpp:85-123)
+// and sparse multi-RHS triangular solve (factorization.cpp:160-199), in the
+// reference's operation order, so S^ is bit-identical.  This is setup work
+// over blocks of size sz; the device path starts at the factorisation of
+// the interior blocks and of S^ (csrc/device/).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <thread>
+
+#include "setup.hpp"
+
+namespace mscg::host {
+
+std::vector<int> equal_sizes(int n_g, int sz) {
+  if (sz < 1 || n_g < 1) throw std::invalid_argument("equal_sizes: sz and n_g must be positive");
+  sz = std::min(sz, n_g);
+  const int k = std::max(1, n_g / sz);
+  std::vector<int> sizes(k, sz);
+  sizes.back() = n_g - sz * (k - 1);
+  return sizes;
+}
+
+std::vector<int> anchored_sizes(const Partitioned& pm, int sz) {
+  const int ng = pm.n_g(), p = pm.p;
+  if (sz <= 0) sz = std::max(1, ng / 8);
+  std::vector<char> is_p(ng, 0);
+  for (int q = 0; q < ng; ++q) {
+    bool diag = false;
+    for (int k = pm.C.rp[p + q]; k < pm.C.rp[p + q + 1]; ++k)
+      if (pm.C.ci[k] == p + q) {
+        diag = true;
+        break;
+      }
+    is_p[q] = !diag;
+  }
+  std::vector<int> sizes;
+  int cur = 0;
+  for (int q = 0; q < ng; ++q) {
+    ++cur;
+    const bool next_is_p = (q + 1 < ng) && is_p[q + 1];
+    if (cur >= sz && !next_is_p && q + 1 < ng) {
+      sizes.push_back(cur);
+      cur = 0;
+    }
+  }
+  if (cur > 0) sizes.push_back(cur);
+  return sizes;
+}
+
+Variant variant_from_name(const std::string& name) {
+  if (name == "mscn") return Variant::Mscn;
+  if (name == "mscnr") return Variant::Mscnr;
+  if (name == "lum") return Variant::Lum;
+  throw std::invalid_argument("unknown or unsupported MSC variant: " + name);
+}
+
+namespace {
+
+struct Dense {
+  int r = 0, c = 0;
+  std::vector<double> a;
+  Dense() = default;
+  Dense(int rr, int cc) : r(rr), c(cc), a(static_cast<size_t>(rr) * cc, 0.0) {}
+  double& operator()(int i, int j) { return a[static_cast<size_t>(i) * c + j]; }
+  double operator()(int i, int j) const { return a[static_cast<size_t>(i) * c + j]; }
+};
+
+// A[rows, cols] for a contiguous row range and a contiguous column range
+// (extract_submatrix, sparse_matrix.cpp:146-172, for numbering aggregates).
+Dense dense_range(const Csr& a, int rb, int re, int cb, int ce) {
+  Dense d(re - rb, ce - cb);
+  for (int i = rb; i < re; ++i)
+    for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+      if (a.ci[k] >= cb && a.ci[k] < ce) d(i - rb, a.ci[k] - cb) = a.v[k];
+  return d;
+}
+
+struct SparseRows {
+  std::vector<std::vector<std::pair<int, double>>> rows;
+};
+
+struct LuFactors {
+  SparseRows L, U;
+  std::vector<int> perm;
+};
+
+// dense_lu (dense_matrix.cpp:85-123) re-stored sparse (factorization.cpp:11-32).
+LuFactors factor_exact(Dense a, int agg) {
+  const int n = a.r;
+  LuFactors f;
+  f.perm.resize(n);
+  for (int i = 0; i < n; ++i) f.perm[i] = i;
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    double best = std::abs(a(k, k));
+    for (int i = k + 1; i < n; ++i)
+      if (std::abs(a(i, k)) > best) {
+        best = std::abs(a(i, k));
+        piv = i;
+      }
+    if (best == 0.0)
+      throw SingularError("build_msc: singular D block of aggregate " + std::to_string(agg) +
+                              " (dense_lu: zero pivot at index " + std::to_string(k) + ")",
+                          k);
+    if (piv != k) {
+      for (int j = 0; j < n; ++j) std::swap(a(k, j), a(piv, j));
+      std::swap(f.perm[k], f.perm[piv]);
+    }
+    const double pivot = a(k, k);
+    for (int i = k + 1; i < n; ++i) {
+      const double lik = a(i, k) / pivot;
+      a(i, k) = lik;
+      if (lik == 0.0) continue;
+      for (int j = k + 1; j < n; ++j) a(i, j) -= lik * a(k, j);
+    }
+  }
+  f.L.rows.resize(n);
+  f.U.rows.resize(n);
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < i; ++j)
+      if (a(i, j) != 0.0) f.L.rows[i].push_back({j, a(i, j)});
+    for (int j = i; j < n; ++j)
+      if (a(i, j) != 0.0) f.U.rows[i].push_back({j, a(i, j)});
+  }
+  return f;
+}
+
+// Multi-RHS solve (factorization.cpp:160-199).
+Dense solve(const LuFactors& f, const Dense& b) {
+  const int n = b.r, m = b.c;
+  Dense x(n, m);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < m; ++j) x(i, j) = b(f.perm[i], j);
+  for (int i = 0; i < n; ++i)
+    for (auto [c, lik] : f.L.rows[i])
+      for (int j = 0; j < m; ++j) x(i, j) -= lik * x(c, j);
+  for (int i = n - 1; i >= 0; --i) {
+    double diag = 0.0;
+    for (auto [c, uik] : f.U.rows[i]) {
+      if (c == i) {
+        diag = uik;
+        continue;
+      }
+      for (int j = 0; j < m; ++j) x(i, j) -= uik * x(c, j);
+    }
+    for (int j = 0; j < m; ++j) x(i, j) /= diag;
+  }
+  return x;
+}
+
+}  // namespace
+
+SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes, Variant v,
+                      int threads) {
+  const int ng = pm.n_g(), p = pm.p;
+  int total = 0;
+  for (int s : sizes) {
+    if (s < 1) throw std::invalid_argument("aggregates: sizes must be >= 1");
+    total += s;
+  }
+  if (sizes.empty() || total != ng)
+    throw std::invalid_argument("aggregates: sizes sum to " + std::to_string(total) +
+                                ", expected " + std::to_string(ng));
+  SchurApprox out;
+  int b = 0;
+  for (int s : sizes) {
+    out.ranges.push_back({b, b + s});
+    b += s;
+  }
+  const int k = static_cast<int>(sizes.size());
+  if (v != Variant::Lum) {
+    for (int i = 0; i < k; ++i)
+      if (out.ranges[i].second > p)
+        throw std::invalid_argument("build_msc: aggregate " + std::to_string(i) +
+                                    " has a D-side index outside the (1,1) block");
+  }
+  std::vector<Dense> local(k);
+  if (threads <= 0) threads = hardware_threads();
+  std::atomic<int> next{0};
+  std::exception_ptr err;
+  std::atomic<bool> failed{false};
+  auto work = [&] {
+    for (int i = next++; i < k && !failed; i = next++) {
+      try {
+        const auto [sb, se] = out.ranges[i];
+        const int m = se - sb;
+        // G = C[p:, p:]; D = C[:p, :p]; E = C[:p, p:]; F = C[p:, :p].
+        Dense s = dense_range(pm.C, p + sb, p + se, p + sb, p + se);
+        if (v != Variant::Lum) {
+          LuFactors dlu = factor_exact(dense_range(pm.C, sb, se, sb, se), i);
+          Dense e = dense_range(pm.C, sb, se, p + sb, p + se);
+          Dense rhs;
+          if (v == Variant::Mscnr) {
+            // E_ii compressed to diag(E_ii * 1) (schur_approx.cpp:112-126).
+            rhs = Dense(m, m);
+            for (int r = 0; r < m; ++r) {
+              double acc = 0.0;
+              for (int t = pm.C.rp[sb + r]; t < pm.C.rp[sb + r + 1]; ++t) {
+                const int c = pm.C.ci[t];
+                if (c >= p + sb && c < p + se) acc += pm.C.v[t] * 1.0;
+              }
+              rhs(r, r) = acc;
+            }
+          } else {
+            rhs = std::move(e);
+          }
+          Dense x = solve(dlu, rhs);
+          // correction = F_ii x (dense_matrix.cpp:62-77), then S - correction.
+          Dense corr(m, m);
+          for (int r = 0; r < m; ++r)
+            for (int t = pm.C.rp[p + sb + r]; t < pm.C.rp[p + sb + r + 1]; ++t) {
+              const int c = pm.C.ci[t];
+              if (c < sb || c >= se) continue;
+              const double aik = pm.C.v[t];
+              for (int j = 0; j < m; ++j) corr(r, j) += aik * x(c - sb, j);
+            }
+          for (size_t t = 0; t < s.a.size(); ++t) s.a[t] = s.a[t] - corr.a[t];
+        }
+        local[i] = std::move(s);
+      } catch (...) {
+        if (!failed.exchange(true)) err = std::current_exception();
+      }
+    }
+  };
+  {
+    std::vector<std::thread> pool;
+    const int t = std::max(1, std::min(threads, k));
+    for (int w = 1; w < t; ++w) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+  }
+  if (err) std::rethrow_exception(err);
+
+  // Sequential merge (schur_approx.cpp:141-160): block diagonal, each row
+  // holds the nonzeros of its own aggregate in column order.
+  Csr& s = out.s_hat;
+  s = Csr(ng, ng);
+  for (int i = 0; i < k; ++i) {
+    const auto [sb, se] = out.ranges[i];
+    for (int r = sb; r < se; ++r) {
+      for (int c = sb; c < se; ++c) {
+        const double val = local[i](r - sb, c - sb);
+        if (val != 0.0) {
+          s.ci.push_back(c);
+          s.v.push_back(val);
+        }
+      }
+      s.rp[r + 1] = static_cast<int>(s.ci.size());
+    }
+  }
+  return out;
+}
+
+}  // namespace mscg::host

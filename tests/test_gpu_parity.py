@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle
+restatement (oracle/restate.c, pinned to the compiled reference).
+
+Bars (BASELINE.json north_star):
+  * SpMV, ILUT factors, Schur LU factors: bit-identical (integer/byte work and
+    order-preserving fp64 replay);
+  * preconditioner apply: relative 2-norm error <= 1e-10 (fp64);
+  * GMRES: iteration count within +-1 of the oracle, both true residuals
+    below the requested tolerance.
+"""
+import numpy as np
+import pytest
+
+from helpers import csr_tuple, oracle_msc, rel_err, same_bits, split_blocks
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def cfg1(msc):
+    pb = msc.oseen_problem(32, 0.1, 8)
+    pb.build_msc("lum")
+    return pb
+
+
+@pytest.fixture(scope="module")
+def cfg1_pc(msc, ctx, cfg1):
+    return msc.build_preconditioner(cfg1, tolA=1e-4, sA=0, ctx=ctx)
+
+
+@pytest.fixture(scope="module")
+def cfg1_oracle(rs, cfg1):
+    return oracle_msc(rs, cfg1, 1e-4, 0)
+
+
+def test_spmv_bit_identical(msc, ctx, rs, cfg1, ref):
+    C = cfg1.C
+    A = msc.DeviceMatrix(ctx, C)
+    for seed in (0, 1, 2):
+        x = ref.random_vector(C.ncols, seed)
+        y = msc.matvec(A, x)
+        assert same_bits(y, rs.matvec(*csr_tuple(C), x))
+
+
+def test_spmv_rectangular_and_empty_rows(msc, ctx, rs):
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((70, 45)) * (rng.random((70, 45)) < 0.1)
+    a[3, :] = 0.0
+    a[40:, :] = 0.0  # trailing empty rows, ragged slices
+    A = msc.SparseMatrix.from_dense(a)
+    x = rng.standard_normal(45)
+    y = msc.matvec(msc.DeviceMatrix(ctx, A), x)
+    assert same_bits(y, rs.matvec(*csr_tuple(A), x))
+
+
+def test_ilut_factors_bit_identical(cfg1_pc, cfg1_oracle, cfg1):
+    assert cfg1_pc.nblocks == cfg1.nblocks
+    for b in range(cfg1.nblocks):
+        f = cfg1_pc.d_factors(b)
+        o = cfg1_oracle.dfac[b]
+        assert np.array_equal(f.lower.row_offsets, o.lrp)
+        assert np.array_equal(f.lower.col_indices, o.lci)
+        assert same_bits(f.lower.values, o.lv)
+        assert np.array_equal(f.upper.row_offsets, o.urp)
+        assert np.array_equal(f.upper.col_indices, o.uci)
+        assert same_bits(f.upper.values, o.uv)
+
+
+def test_schur_factors_bit_identical(cfg1_pc, cfg1_oracle):
+    assert cfg1_pc.nschur == len(cfg1_oracle.sfac)
+    for b in range(cfg1_pc.nschur):
+        f = cfg1_pc.schur_factors(b)
+        o = cfg1_oracle.sfac[b]
+        assert np.array_equal(f.row_perm, o.perm)
+        assert np.array_equal(f.lower.row_offsets, o.lrp)
+        assert np.array_equal(f.lower.col_indices, o.lci)
+        assert same_bits(f.lower.values, o.lv)
+        assert np.array_equal(f.upper.col_indices, o.uci)
+        assert same_bits(f.upper.values, o.uv)
+
+
+def test_stored_nnz_matches_oracle(cfg1_pc, cfg1_oracle, msc, cfg1):
+    assert cfg1_pc.stored_nnz() == cfg1_oracle.stored_nnz
+    assert msc.fill_factor(cfg1_pc, cfg1.C) == cfg1_oracle.stored_nnz / cfg1.C.nnz
+
+
+def test_apply_matches_oracle(cfg1_pc, cfg1_oracle, ref, cfg1):
+    for seed in (0, 1, 7):
+        y = ref.random_vector(cfg1.n, seed)
+        got = cfg1_pc.apply(y)
+        want = cfg1_oracle.apply(y)
+        assert rel_err(got, want) <= APPLY_TOL
+
+
+def test_apply_zero_and_linearity(cfg1_pc, ref, cfg1):
+    z = np.zeros(cfg1.n)
+    assert np.array_equal(cfg1_pc.apply(z), z)
+    y1 = ref.random_vector(cfg1.n, 11)
+    y2 = ref.random_vector(cfg1.n, 12)
+    a, b = 0.75, -1.25
+    lhs = cfg1_pc.apply(a * y1 + b * y2)
+    rhs = a * cfg1_pc.apply(y1) + b * cfg1_pc.apply(y2)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * max(1.0, np.max(np.abs(lhs)))
+
+
+def test_apply_device_tensor(cfg1_pc, cfg1_oracle, ref, cfg1):
+    import torch
+    y = ref.random_vector(cfg1.n, 3)
+    x = cfg1_pc.apply(torch.from_numpy(y).cuda())
+    assert x.is_cuda
+    assert rel_err(x.cpu().numpy(), cfg1_oracle.apply(y)) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("orth", ["cgs2", "mgs"])
+def test_gmres_cfg1_iterations(msc, cfg1_pc, cfg1_oracle, cfg1, ref, rs, orth):
+    b = ref.random_vector(cfg1.n, 0)
+    want = rs.gmres(csr_tuple(cfg1.C), b, 30, 3000, 1e-8, msc=cfg1_oracle)
+    cfg = msc.SolverConfig(restart=30, max_iters=3000, rel_tol=1e-8, orth=orth)
+    x, rep = msc.gmres(cfg1_pc.matrix, cfg1_pc, b, cfg)
+    assert want["iterations"] == 88  # SURVEY §8(d) target (LUM, seed 0)
+    assert abs(rep.iterations - want["iterations"]) <= 1
+    assert rep.converged and want["converged"]
+    tr = msc.true_residual(cfg1_pc.matrix, x, b)
+    assert tr <= 1e-8
+    assert rep.residual_history[-1] <= 1e-8
+    # the recurrence history tracks the oracle's closely
+    h1 = np.asarray(rep.residual_history[:-1])
+    h2 = np.asarray(want["history"][:-1])
+    k = min(len(h1), len(h2)) - 2
+    assert np.allclose(h1[:k], h2[:k], rtol=1e-6, atol=0)
+
+
+def test_gmres_unpreconditioned_identity(msc, ctx, ref):
+    n = 12
+    I = msc.SparseMatrix.from_dense(np.eye(n))
+    A = msc.DeviceMatrix(ctx, I)
+    b = ref.random_vector(n, 3)
+    x, rep = msc.gmres(A, None, b, msc.SolverConfig(rel_tol=1e-9))
+    assert rep.converged and rep.iterations == 1
+    assert rel_err(x, b) < 1e-12
+
+
+def test_gmres_zero_rhs(msc, cfg1_pc, cfg1):
+    x, rep = msc.gmres(cfg1_pc.matrix, cfg1_pc, np.zeros(cfg1.n), msc.SolverConfig())
+    assert rep.converged and np.all(x == 0) and rep.residual_history == [0.0]
+
+
+def test_gmres_iteration_cap(msc, ctx, ref):
+    # test_krylov.cpp:101-116: cap => NC with exactly 4 iterations.
+    n = 60
+    a = np.zeros((n, n))
+    for i in range(n):
+        a[i, i] = 1.0 + 0.01 * i
+        a[i, (i + 1) % n] = -0.99
+    A = msc.DeviceMatrix(ctx, msc.SparseMatrix.from_dense(a))
+    b = np.random.default_rng(19).uniform(-1, 1, n)
+    x, rep = msc.gmres(A, None, b, msc.SolverConfig(restart=2, max_iters=4, rel_tol=1e-9))
+    assert not rep.converged and rep.iterations == 4
+
+
+@pytest.mark.parametrize("seed,variant", [(37, "mscn"), (23, "lum"), (47, "mscnr")])
+def test_random_saddle_exact_blocks(msc, ctx, ref, rs, seed, variant):
+    """Random saddles (tests/oracles.hpp:122-142) with sA = inf: exact LU of
+    D, Schur blocks from build_msc; apply vs the oracle."""
+    R = ref.Problem.random_saddle(20, 8, seed, 0.3)
+    Cr = R.csr(0)
+    C = msc.SparseMatrix(Cr.nrows, Cr.ncols, Cr.rp, Cr.ci, Cr.v)
+    pb = msc.partitioned_problem(C, R.p)
+    pb.build_msc(variant, mode="explicit", sizes=[4, 4])
+    pc = msc.build_preconditioner(pb, tolA=0.0, sA=1 << 30, ctx=ctx)
+    M = oracle_msc(rs, pb, 0.0, 1 << 30)
+    for s in range(3):
+        y = ref.random_vector(R.n, 100 + s)
+        assert rel_err(pc.apply(y), M.apply(y)) <= APPLY_TOL
+    # reference preconditioner on the same system agrees too
+    R.build_schur(variant, 0, 2, sizes=[4, 4])
+    R.build_precond(0.0, 1 << 30)
+    y = ref.random_vector(R.n, 9)
+    assert rel_err(pc.apply(y), R.apply(y)) <= APPLY_TOL
+
+
+def test_ilut_policy_switch(msc, ctx, rs, ref):
+    """sA decides exact vs ILUT per interior block (preconditioner.cpp:44-56)."""
+    pb = msc.oseen_problem(16, 0.1, 4)
+    pb.build_msc("lum")
+    dims = np.diff(pb.d_ranges(), axis=1).ravel()
+    sA = int(np.sort(dims)[1])  # some blocks exact, some ILUT
+    pc = msc.build_preconditioner(pb, tolA=1e-4, sA=sA, ctx=ctx)
+    M = oracle_msc(rs, pb, 1e-4, sA)
+    for b, d in enumerate(dims):
+        f = pc.d_factors(b)
+        assert f.kind == ("exact" if d <= sA else "incomplete")
+        o = M.dfac[b]
+        assert same_bits(f.upper.values, o.uv) and np.array_equal(f.row_perm, o.perm)
+    y = ref.random_vector(pb.n, 4)
+    assert rel_err(pc.apply(y), M.apply(y)) <= APPLY_TOL
+
+
+def test_cfg3_zero_pivot_error(msc, ctx):
+    """BASELINE cfg3 as written (stretch 1.1): the reference's ILUT raises
+    SingularMatrixError in block 0 at local row 2207; the GPU
+    ILUT must raise the identical error."""
+    pb = msc.oseen_problem(256, 0.002, 64, stretched=True, stretch=1.1)
+    pb.build_msc("lum", sz=795)
+    with pytest.raises(msc.SingularMatrixError) as e:
+        msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=ctx)
+    assert e.value.pivot_index == 2207
+    assert e.value.block == 0
+    assert str(e.value) == ("build_preconditioner: (1,1) block 0: "
+                            "factor_ilut: zero pivot at index 2207")
+
+
+def test_cfg2_ilut_and_apply(msc, ctx, rs, ref):
+    pb = msc.oseen_problem(128, 0.01, 16)
+    pb.build_msc("lum")
+    pc = msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=ctx)
+    M = oracle_msc(rs, pb, 1e-4, 0)
+    for b in range(pb.nblocks):
+        f = pc.d_factors(b)
+        o = M.dfac[b]
+        assert np.array_equal(f.lower.row_offsets, o.lrp)
+        assert np.array_equal(f.upper.col_indices, o.uci)
+        assert same_bits(f.lower.values, o.lv) and same_bits(f.upper.values, o.uv)
+    # SURVEY §6 (measured on the reference): nnz(L+U) of D at cfg2
+    assert sum(pc.d_factors(b).nnz() for b in range(pb.nblocks)) == 21083149
+    y = ref.random_vector(pb.n, 0)
+    assert rel_err(pc.apply(y), M.apply(y)) <= APPLY_TOL
