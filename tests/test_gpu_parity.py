@@ -8,6 +8,9 @@ Bars (BASELINE.json north_star):
   * GMRES: iteration count within +-1 of the oracle, both true residuals
     below the requested tolerance.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -16,6 +19,7 @@ from helpers import csr_tuple, oracle_msc, rel_err, same_bits, split_blocks
 pytestmark = pytest.mark.gpu
 
 APPLY_TOL = 1e-10
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 @pytest.fixture(scope="module")
@@ -200,16 +204,17 @@ def test_ilut_policy_switch(msc, ctx, rs, ref):
 
 def test_cfg3_zero_pivot_error(msc, ctx):
     """BASELINE cfg3 as written (stretch 1.1): the reference's ILUT raises
-    SingularMatrixError in block 0 at local row 2207; the GPU
-    ILUT must raise the identical error."""
+    SingularMatrixError in interior block 0 (tests/golden/cfg3_error.json,
+    produced by the compiled reference); the GPU ILUT must raise the
+    identical error (same block, same local pivot row, same message)."""
+    want = json.load(open(os.path.join(GOLDEN, "cfg3_error.json")))
     pb = msc.oseen_problem(256, 0.002, 64, stretched=True, stretch=1.1)
     pb.build_msc("lum", sz=795)
     with pytest.raises(msc.SingularMatrixError) as e:
         msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=ctx)
-    assert e.value.pivot_index == 2207
+    assert e.value.pivot_index == want["pivot_index"]
     assert e.value.block == 0
-    assert str(e.value) == ("build_preconditioner: (1,1) block 0: "
-                            "factor_ilut: zero pivot at index 2207")
+    assert str(e.value) == want["error"]
 
 
 def test_cfg2_ilut_and_apply(msc, ctx, rs, ref):
