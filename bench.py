@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark of the MSC solve phase on B200 (BASELINE.json metric:
+"precond applies/s & GMRES time-to-solution on 1 B200; achieved HBM GB/s vs
+peak").
+
+Default workload = BASELINE configs[4] (cfg5): uniform 2048^2 Oseen, nu 0.01,
+4096 interior blocks (~12.6M unknowns), LUM with anchored aggregates of 256,
+ILUT(1e-4) everywhere (sA = 0).  One step = one
+preconditioner apply + one SpMV with C on the seeded uniform[-1,1] vector
+(the apply-only microbenchmark).  Inputs (factors: ~35 GB) are far larger
+than L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
+                    [--mode apply|gmres] [--impl ours|reference]
+
+For N > 1 (torchrun) every rank runs an independent replica of the
+single-GPU workload ("replicas only": BASELINE runs the path on one GPU;
+see DESIGN.md §Multi-GPU); value = total steps of all ranks / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(grid=32, nu=0.1, n_a=8, stretched=False, stretch=1.056, variant="lum", sz=0,
+                 mode="equal", anchored=False, restart=30),
+    "cfg2": dict(grid=128, nu=0.01, n_a=16, stretched=False, stretch=1.056, variant="lum", sz=0,
+                 mode="equal", anchored=False, restart=50),
+    "cfg3": dict(grid=256, nu=0.002, n_a=64, stretched=True, stretch=1.0313, variant="lum",
+                 sz=795, mode="equal", anchored=False, restart=50),
+    "cfg4": dict(grid=1024, nu=0.001, n_a=1024, stretched=False, stretch=1.056, variant="lum",
+                 sz=256, mode="anchored", anchored=True, restart=100),
+    "cfg5": dict(grid=2048, nu=0.01, n_a=4096, stretched=False, stretch=1.056, variant="lum",
+                 sz=256, mode="anchored", anchored=True, restart=100),
+}
+TOL_A, S_A = 1e-4, 0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_problem(cfg, threads=0):
+    import paper_1104_3349_b200 as msc
+    t0 = time.perf_counter()
+    pb = msc.oseen_problem(cfg["grid"], cfg["nu"], cfg["n_a"], stretched=cfg["stretched"],
+                           stretch=cfg["stretch"], anchored=cfg["anchored"], threads=threads)
+    t1 = time.perf_counter()
+    pb.build_msc(cfg["variant"], sz=cfg["sz"], mode=cfg["mode"], threads=threads)
+    t2 = time.perf_counter()
+    return pb, {"generate_partition_s": t1 - t0, "build_msc_s": t2 - t1}
+
+
+def seeded_rhs(n, seed=0):
+    """oracle::random_vector convention (std::mt19937 + U[-1,1]) through the
+    library's own generator, drawn in the final numbering."""
+    import ctypes as C
+    from paper_1104_3349_b200 import _capi
+    out = np.empty(n)
+    _capi.lib().mscg_random_vector(n, seed, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def precond_counts(pc):
+    import ctypes as C
+    from paper_1104_3349_b200 import _capi
+    cnt = (C.c_int64 * 7)()
+    _capi.lib().mscg_precond_nnz(pc.h, cnt)
+    k = list(cnt)
+    return dict(d_l=k[0], d_u=k[1], s_l=k[2], s_u=k[3], e=k[4], f=k[5], c=k[6])
+
+
+def algorithmic_bytes(pc, cnt):
+    """reference CSR (12 B per stored entry, U diagonal stored),
+    int32 row pointers, fp64 vectors."""
+    n, p = pc.n, pc.p
+    ng = n - p
+    d_lu = cnt["d_l"] + cnt["d_u"] + p
+    s_lu = cnt["s_l"] + cnt["s_u"] + ng
+    d_solve = 12 * d_lu + 2 * 4 * p + 16 * p   # factors + L/U row pointers + rhs in, x out
+    apply_b = (2 * 12 * d_lu + 2 * 2 * p * 4 + 12 * (cnt["e"] + cnt["f"]) + 12 * s_lu + 5 * 8 * n)
+    spmv_b = 12 * cnt["c"] + 4 * (n + 1) + 8 * n + 8 * n
+    return dict(d_solve=d_solve, apply=apply_b, spmv=spmv_b, d_lu_nnz=d_lu, s_lu_nnz=s_lu)
+
+
+def cpu_baseline(pc, pb, y, seconds_target=12.0, workers=1):
+    """The reference's own `solve` (factorization.cpp:129-158) timed on host
+    cores on a sample of interior blocks, extrapolated to a full apply
+    (two D passes over all blocks; E/F/Schur/SpMV terms < 5% omitted)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    nb = pc.nblocks
+    ns = min(nb, 8)
+    idx = np.unique(np.linspace(0, nb - 1, ns).astype(int))
+    ranges = pb.d_ranges()
+    facs, rhs = [], []
+    kind = "reference"
+    try:
+        import refpy
+        refpy.lib()
+        for b in idx:
+            f = pc.d_factors(int(b))
+            L = refpy.Csr(f.lower.nrows, f.lower.ncols, f.lower.row_offsets, f.lower.col_indices,
+                          f.lower.values)
+            U = refpy.Csr(f.upper.nrows, f.upper.ncols, f.upper.row_offsets, f.upper.col_indices,
+                          f.upper.values)
+            facs.append(refpy.factors_from_arrays(f.lower.nrows, L, U))
+            rhs.append(y[ranges[b, 0]:ranges[b, 1]])
+        rhs = np.concatenate(rhs)
+        secs, _ = refpy.time_block_solves(facs, rhs, 1, workers)
+        reps = max(1, int(seconds_target / max(secs, 1e-6)))
+        secs, _ = refpy.time_block_solves(facs, rhs, reps, workers)
+    except Exception as e:  # reference library absent -> oracle port
+        log("cpu_baseline: reference unavailable, using the oracle port:", e)
+        import restatepy as rs
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from helpers import split_blocks
+        kind = "port"
+        D, _, _ = split_blocks(pb.C, pb.p)
+        facs = [rs.factor_ilut(int(ranges[b, 1] - ranges[b, 0]),
+                               *rs._sub_csr(*D, int(ranges[b, 0]), int(ranges[b, 1])), TOL_A)
+                for b in idx]
+        rhs = [y[ranges[b, 0]:ranges[b, 1]] for b in idx]
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < seconds_target:
+            for f, r in zip(facs, rhs):
+                f.solve(r)
+            reps += 1
+        secs = time.perf_counter() - t0
+    # single worker: mean per-block solve time, two D passes over all blocks
+    per_block = secs / (reps * len(idx))
+    t_apply = 2.0 * per_block * nb
+    return {
+        "value": 1.0 / t_apply, "unit": "applies/s", "cores": workers, "kind": kind,
+        "sample": (f"{len(idx)} of {nb} interior blocks x {reps} reps of the reference solve "
+                   f"(factorization.cpp:129-158) on GPU-built factors bit-identical to the "
+                   f"reference ILUT; extrapolated to 2 D passes over all blocks "
+                   f"({secs:.1f} s measured)"),
+        "seconds_per_apply": t_apply,
+    }
+
+
+def run_reference_arm(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy
+    import paper_1104_3349_b200 as msc
+    threads = refpy.hardware_threads()
+    pb, _ = build_problem(cfg)
+    # Reference ILUT on a sample of blocks (its own factor_ilut), then the
+    # reference solve over that sample on all host threads per step.
+    ranges = pb.d_ranges()
+    C = pb.C
+    nb = pb.nblocks
+    ns = min(nb, max(8, 2 * threads))
+    idx = np.unique(np.linspace(0, nb - 1, ns).astype(int))
+    from concurrent.futures import ThreadPoolExecutor
+
+    def fac(b):
+        b0, b1 = ranges[b]
+        rp = C.row_offsets[b0:b1 + 1] - C.row_offsets[b0]
+        ci = C.col_indices[C.row_offsets[b0]:C.row_offsets[b1]]
+        v = C.values[C.row_offsets[b0]:C.row_offsets[b1]]
+        keep = (ci >= b0) & (ci < b1)
+        rows = np.repeat(np.arange(b1 - b0), np.diff(rp))[keep]
+        nrp = np.zeros(b1 - b0 + 1, np.int32)
+        np.add.at(nrp, rows + 1, 1)
+        A = refpy.Csr(b1 - b0, b1 - b0, np.cumsum(nrp).astype(np.int32),
+                      (ci[keep] - b0).astype(np.int32), v[keep].copy())
+        return refpy.factor_ilut(A, TOL_A)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        facs = list(ex.map(fac, idx))
+    t_fac = time.perf_counter() - t0
+    y = seeded_rhs(pb.n, 0)
+    rhs = np.concatenate([y[ranges[b, 0]:ranges[b, 1]] for b in idx])
+    for _ in range(args.warmup):
+        refpy.time_block_solves(facs, rhs, 1, threads)
+    step_secs = []
+    for _ in range(args.steps):
+        s, _ = refpy.time_block_solves(facs, rhs, 2, threads)  # two D passes
+        step_secs.append(s)
+    t = float(np.mean(step_secs))
+    value = (len(idx) / nb) / t  # full applies per second, extrapolated
+    line = {
+        "impl": "reference", "metric": "precond_applies_per_s", "value": value,
+        "unit": "applies/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Oseen generator)",
+        "config": {"workload": args.config, **{k: cfg[k] for k in ("grid", "nu", "n_a")}},
+        "cpu_baseline": {
+            "value": value, "unit": "applies/s", "cores": threads, "kind": "reference",
+            "sample": (f"reference factor_ilut + solve on {len(idx)} of {nb} interior blocks, "
+                       f"{threads} threads (reference parallel_for), extrapolated to a full "
+                       f"apply (2 D passes); ILUT of the sample took {t_fac:.1f} s"),
+        },
+        "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="apply", choices=["apply", "gmres"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--max-iters", type=int, default=3000)
+    ap.add_argument("--orth", default="cgs2", choices=["cgs2", "mgs"])
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+
+    ws, rank, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    import paper_1104_3349_b200 as msc
+    ctx = msc.Context(local)
+
+    pb, setup = build_problem(cfg, threads=max(1, (os.cpu_count() or 8) // ws))
+    t0 = time.perf_counter()
+    pc = msc.build_preconditioner(pb, tolA=TOL_A, sA=S_A, ctx=ctx)
+    setup["device_factorisation_s"] = time.perf_counter() - t0
+    setup.update(pc.build_times())
+    cnt = precond_counts(pc)
+    ab = algorithmic_bytes(pc, cnt)
+    y = seeded_rhs(pb.n, 0)
+    dev = torch.device("cuda", local)
+    y_d = torch.from_numpy(y).to(dev)
+    x_d = torch.empty_like(y_d)
+    w_d = torch.empty_like(y_d)
+    torch.cuda.synchronize()
+
+    import ctypes as C
+    from paper_1104_3349_b200 import _capi
+    L = _capi.lib()
+
+    def bench(steps):
+        tot = C.c_double()
+        stages = (C.c_double * 6)()
+        launches = C.c_int64()
+        st = _capi.Status()
+        rc = L.mscg_bench_apply(pc.h, C.c_void_p(y_d.data_ptr()), C.c_void_p(x_d.data_ptr()),
+                                C.c_void_p(w_d.data_ptr()), steps, 1, C.byref(tot), stages,
+                                C.byref(launches), C.byref(st))
+        msc.msc._check(rc, st)
+        return tot.value, list(stages), launches.value
+
+    result = {}
+    if args.mode == "apply":
+        bench(args.warmup)
+        clocks = ClockSampler(local)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        clocks.start()
+        time.sleep(0.3)
+        total_ms, stage_ms, launches = bench(args.steps)
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        if pg:
+            pg.barrier()
+            t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            total_ms = float(t.item())
+        ms_step = total_ms / args.steps
+        value = ws * args.steps / (total_ms / 1e3)
+        # end-to-end through the public API with host buffers
+        x_h = np.empty(pb.n)
+        for _ in range(2):
+            pc.apply(y)
+        if pg:
+            pg.barrier()
+        te0 = time.perf_counter()
+        ke = max(3, min(args.steps, 10))
+        for _ in range(ke):
+            x_h = pc.apply(y)
+            msc.matvec(pc.matrix, x_h)
+        te = time.perf_counter() - te0
+        if pg:
+            t = torch.tensor([te], device=dev, dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": ws * ke / te, "unit": "applies/s",
+               "h2d_bytes_per_step": 2 * 8 * pb.n, "d2h_bytes_per_step": 2 * 8 * pb.n}
+        d_solve_ms = (stage_ms[0] + stage_ms[4]) / (2 * args.steps)
+        peak, peak_src = measured_peak()
+        achieved = ab["d_solve"] / (d_solve_ms / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "trisolve_traffic.json")
+        if os.path.exists(tp):
+            try:
+                tj = json.load(open(tp))
+                if tj.get("config") == args.config:
+                    traffic = tj.get("dram_bytes_per_launch")
+            except Exception:
+                pass
+        apply_ms = sum(stage_ms[:5]) / args.steps
+        result = {
+            "metric": "precond_applies_per_s", "value": value, "unit": "applies/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded uniform[-1,1] rhs; reference Oseen generator, bit-identical)",
+            "config": {"workload": args.config, "grid": cfg["grid"], "nu": cfg["nu"],
+                       "subdomains": pb.nblocks, "unknowns": pb.n, "variant": cfg["variant"],
+                       "aggregates": len(pb.schur_ranges()), "tolA": TOL_A, "sA": S_A,
+                       "step": "1 MSC apply + 1 SpMV(C)",
+                       "l2": "inputs larger than L2 (factors %.1f GB)" % (ab["d_lu_nnz"] * 10 / 1e9),
+                       "parallelism": "replicas" if ws > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "trisolve_kernel (interior-block L+U solve)",
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": ab["d_solve"],
+                         "avg_launch_ms": d_solve_ms},
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "apply_ms": apply_ms,
+            "apply_gbs": ab["apply"] / (apply_ms / 1e3) / 1e9,
+            "spmv_ms": stage_ms[5] / args.steps,
+            "spmv_gbs": ab["spmv"] / (stage_ms[5] / args.steps / 1e3) / 1e9,
+            "stage_ms": {k: v / args.steps for k, v in zip(
+                ["d_solve", "f_spmv", "s_solve", "e_spmv", "d_solve_sub", "c_spmv"], stage_ms)},
+            "factor_nnz": {"interior_LU": ab["d_lu_nnz"], "schur_LU": ab["s_lu_nnz"]},
+            "setup": setup,
+        }
+    else:
+        from paper_1104_3349_b200.msc import SolverConfig
+        b = y
+        scfg = SolverConfig(restart=cfg["restart"], max_iters=args.max_iters, rel_tol=1e-8,
+                            orth=args.orth)
+        l0 = ctx.launches
+        t0 = time.perf_counter()
+        x, rep = msc.gmres(pc.matrix, pc, torch.from_numpy(b).to(dev), scfg)
+        torch.cuda.synchronize()
+        tts = time.perf_counter() - t0
+        result = {
+            "metric": "gmres_time_to_solution_s", "value": tts, "unit": "s", "n_gpus": ws,
+            "steps": 1, "warmup": 0, "ms_per_step": tts * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "restart": cfg["restart"], "rel_tol": 1e-8,
+                       "max_iters": args.max_iters, "orth": args.orth},
+            "iterations": rep.iterations, "converged": rep.converged,
+            "final_true_residual": rep.residual_history[-1],
+            "setup": setup, "gpu_launches": ctx.launches - l0,
+        }
+    if rank == 0 and ws == 1 and args.mode == "apply" and not args.no_cpu_baseline:
+        try:
+            result["cpu_baseline"] = cpu_baseline(pc, pb, y)
+        except Exception as e:
+            result["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

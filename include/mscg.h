@@ -149,6 +149,23 @@ int mscg_precond_build_times(const mscg_precond *pc, double *ilut_s,
 /* The operator matrix C of the preconditioner, resident on the device. */
 mscg_csr *mscg_precond_matrix(mscg_precond *pc);
 
+/* Stored-entry counts for roofline bookkeeping: interior-block L and U
+ * (U without its diagonal), Schur-block L and U, E, F and C. */
+int mscg_precond_nnz(const mscg_precond *pc, int64_t counts[7]);
+
+/* ---- measurement helpers ------------------------------------------------ */
+/* oracle::random_vector (proj/tests/oracles.hpp:92-98): std::mt19937(seed)
+ * + std::uniform_real_distribution<double>(-1, 1), the reference's seeded
+ * right-hand-side convention. */
+void mscg_random_vector(int n, unsigned seed, double *out);
+/* `steps` back-to-back [apply(y) -> x; C x -> w] (with_spmv) on device
+ * vectors, timed with CUDA events on the context stream.  total_ms: first to
+ * last event; stage_ms[6]: summed per stage (D-solve, F-SpMV, S-solve,
+ * E-SpMV, D-solve+sub, C-SpMV); launches: kernels enqueued. */
+int mscg_bench_apply(mscg_precond *pc, const double *y_dev, double *x_dev,
+                     double *w_dev, int steps, int with_spmv, double *total_ms,
+                     double *stage_ms, int64_t *launches, mscg_status *st);
+
 /* ---- restarted GMRES (gmres.hpp:44-47, gmres.cpp:35-191) -------------- */
 typedef struct {
   int restart;      /* default 300 */

@@ -81,6 +81,10 @@ _SIGS = {
     "mscg_precond_matrix": (vp, [vp]),
     "mscg_gmres": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(GmresConfig),
                              C.POINTER(GmresReport), vp, C.c_int, C.POINTER(Status)]),
+    "mscg_precond_nnz": (C.c_int, [vp, C.POINTER(C.c_int64)]),
+    "mscg_random_vector": (None, [C.c_int, C.c_uint, vp]),
+    "mscg_bench_apply": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, dp, dp, i64p,
+                                   C.POINTER(Status)]),
     "mscg_true_residual": (C.c_int, [vp, vp, vp, vp, C.c_int, dp, C.POINTER(Status)]),
 }
 

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -354,6 +355,58 @@ int mscg_precond_build_times(const mscg_precond* pc, double* ilut_s, double* sch
 }
 
 mscg_csr* mscg_precond_matrix(mscg_precond* pc) { return pc ? &pc->matrix : nullptr; }
+
+int mscg_precond_nnz(const mscg_precond* pc, int64_t counts[7]) {
+  if (!pc) return MSCG_ERR_INVALID_ARGUMENT;
+  const auto& p = *pc->pc;
+  counts[0] = p.D ? p.D->nnz_l() : 0;
+  counts[1] = p.D ? p.D->nnz_u() : 0;
+  counts[2] = p.S ? p.S->nnz_l() : 0;
+  counts[3] = p.S ? p.S->nnz_u() : 0;
+  counts[4] = p.E ? p.E->nnz : 0;
+  counts[5] = p.F ? p.F->nnz : 0;
+  counts[6] = p.C ? p.C->nnz : 0;
+  return MSCG_OK;
+}
+
+void mscg_random_vector(int n, unsigned seed, double* out) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  for (int i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+int mscg_bench_apply(mscg_precond* pc, const double* y, double* x, double* w, int steps,
+                     int with_spmv, double* total_ms, double* stage_ms, int64_t* launches,
+                     mscg_status* st) {
+  return guard(st, [&] {
+    if (!pc || steps < 1) throw std::invalid_argument("mscg_bench_apply: bad arguments");
+    cudaStream_t s = pc->ctx->ctx.stream;
+    const int per = 7;
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(steps) * per);
+    for (auto& e : ev) MSCG_CUDA(cudaEventCreate(&e));
+    const int64_t l0 = pc->ctx->ctx.launches;
+    for (int k = 0; k < steps; ++k) {
+      cudaEvent_t* e = ev.data() + static_cast<size_t>(k) * per;
+      pc->pc->apply(y, x, s, e);
+      if (with_spmv) mscg::spmv(*pc->pc->C, x, w, nullptr, 0, s);
+      MSCG_CUDA(cudaEventRecord(e[6], s));
+    }
+    MSCG_CUDA(cudaStreamSynchronize(s));
+    if (launches) *launches = pc->ctx->ctx.launches - l0;
+    float ms = 0;
+    MSCG_CUDA(cudaEventElapsedTime(&ms, ev.front(), ev.back()));
+    *total_ms = ms;
+    for (int j = 0; j < 6; ++j) stage_ms[j] = 0;
+    for (int k = 0; k < steps; ++k) {
+      cudaEvent_t* e = ev.data() + static_cast<size_t>(k) * per;
+      for (int j = 0; j < 6; ++j) {
+        MSCG_CUDA(cudaEventElapsedTime(&ms, e[j], e[j + 1]));
+        stage_ms[j] += ms;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
 
 // ---- GMRES -----------------------------------------------------------------
 

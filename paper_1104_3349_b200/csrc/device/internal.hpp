@@ -115,7 +115,7 @@ struct Precond {
   int64_t stored_nnz = 0;
   FactorTimes times;
   DevBuf z1, t, w;  // scratch (apply is stream-ordered on ctx->stream)
-  void apply(const double* y_dev, double* x_dev, cudaStream_t s);
+  void apply(const double* y_dev, double* x_dev, cudaStream_t s, cudaEvent_t* ev = nullptr);
 };
 
 std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,

@@ -13,6 +13,7 @@
 // the interior blocks and of S^ (csrc/device/).
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cmath>
 #include <thread>
 
@@ -187,9 +188,10 @@ SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes, Vari
   if (threads <= 0) threads = hardware_threads();
   std::atomic<int> next{0};
   std::exception_ptr err;
-  std::atomic<bool> failed{false};
+  std::mutex err_mu;
+  int err_idx = k;
   auto work = [&] {
-    for (int i = next++; i < k && !failed; i = next++) {
+    for (int i = next++; i < k; i = next++) {
       try {
         const auto [sb, se] = out.ranges[i];
         const int m = se - sb;
@@ -227,7 +229,13 @@ SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes, Vari
         }
         local[i] = std::move(s);
       } catch (...) {
-        if (!failed.exchange(true)) err = std::current_exception();
+        // Deterministic: report the lowest failing aggregate, as the
+        // reference's sequential build_msc (workers = 1) does.
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (i < err_idx) {
+          err_idx = i;
+          err = std::current_exception();
+        }
       }
     }
   };
