@@ -85,6 +85,7 @@ _SIGS = {
     "mscg_random_vector": (None, [C.c_int, C.c_uint, vp]),
     "mscg_bench_apply": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, dp, dp, i64p,
                                    C.POINTER(Status)]),
+    "mscg_debug_trace_dsolve": (C.c_int, [vp, vp, vp, vp, C.c_int, C.POINTER(Status)]),
     "mscg_true_residual": (C.c_int, [vp, vp, vp, vp, C.c_int, dp, C.POINTER(Status)]),
 }
 

@@ -329,8 +329,8 @@ int mscg_precond_factor(const mscg_precond* pc, int kind, int idx, int* dim, int
     if (!fs || idx < 0 || idx >= fs->nblocks) throw std::invalid_argument("factor index out of range");
     const int d = fs->h_dim[idx];
     if (dim) *dim = d;
-    if (nnz_l) *nnz_l = fs->h_loff[idx + 1] - fs->h_loff[idx];
-    if (nnz_u) *nnz_u = fs->h_uoff[idx + 1] - fs->h_uoff[idx] + d;
+    if (nnz_l) *nnz_l = fs->h_nnz_l[idx];
+    if (nnz_u) *nnz_u = fs->h_nnz_u[idx] + d;
     if (!lrp) return;
     std::vector<int> a, b2, c2, d2, e2;
     std::vector<double> f2, g2;
@@ -373,6 +373,23 @@ void mscg_random_vector(int n, unsigned seed, double* out) {
   std::mt19937 rng(seed);
   std::uniform_real_distribution<double> dist(-1.0, 1.0);
   for (int i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+int mscg_debug_trace_dsolve(mscg_precond* pc, const double* y, double* x, int64_t* out, int cap,
+                            mscg_status* st) {
+  int dim0 = -1;
+  int rc = guard(st, [&] {
+    const mscg::FactorSet& fs = *pc->pc->D;
+    dim0 = fs.h_dim[0];
+    if (cap < 6 * dim0) throw std::invalid_argument("trace buffer too small");
+    mscg::DevBuf tr(sizeof(long long) * 6 * dim0);
+    cudaStream_t s = pc->ctx->ctx.stream;
+    MSCG_CUDA(cudaMemsetAsync(tr.p, 0, tr.bytes, s));
+    mscg::block_trisolve(fs, y, x, nullptr, s, tr.as<long long>());
+    MSCG_CUDA(cudaMemcpyAsync(out, tr.p, tr.bytes, cudaMemcpyDeviceToHost, s));
+    MSCG_CUDA(cudaStreamSynchronize(s));
+  });
+  return rc == MSCG_OK ? dim0 : -rc;
 }
 
 int mscg_bench_apply(mscg_precond* pc, const double* y, double* x, double* w, int steps,

@@ -51,6 +51,19 @@ __device__ __forceinline__ double wait_ready(const double* p) {
   while (is_pending(v)) v = *vp;
   return v;
 }
+
+// Same, for warps off the critical path: back off with __nanosleep so that
+// polling does not steal issue slots and shared-memory bandwidth from the
+// warp that is advancing the dependency chain.
+__device__ __forceinline__ double wait_ready_lazy(const double* p, unsigned ns = 64) {
+  const volatile double* vp = p;
+  double v = *vp;
+  while (is_pending(v)) {
+    __nanosleep(ns);
+    v = *vp;
+  }
+  return v;
+}
 #endif  // __CUDACC__
 
 }  // namespace mscg

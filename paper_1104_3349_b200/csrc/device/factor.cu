@@ -438,43 +438,131 @@ __global__ void __launch_bounds__(kLuThreads) dense_lu_kernel(
   }
 }
 
-// ---- pack pools -> solve layout --------------------------------------------
+// ---- pools -> tiled solve layout -------------------------------------------
 
-__global__ void __launch_bounds__(256) pack_kernel(
+// Far entries: L columns < 32(t-2), U columns >= 32(t+3) (t = row's tile).
+__device__ __forceinline__ bool l_far(int c, int i) {
+  return c < ((i >> 5) - (kNearTiles - 1)) * kTile;
+}
+__device__ __forceinline__ bool u_far(int c, int i) {
+  return c >= ((i >> 5) + kNearTiles) * kTile;
+}
+
+// Per row far counts (into lrp/urp scratch slots) and per block totals.
+__global__ void __launch_bounds__(256) count_far_kernel(
     const int* __restrict__ set_row0, const int* __restrict__ blk_dim, PoolView pool,
+    int* __restrict__ lcnt, int* __restrict__ ucnt, long long* __restrict__ far_l,
+    long long* __restrict__ far_u) {
+  const int b = blockIdx.x;
+  const int r0 = set_row0[b], n = blk_dim[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ unsigned long long sl, su;
+  if (threadIdx.x == 0) {
+    sl = 0;
+    su = 0;
+  }
+  __syncthreads();
+  unsigned long long tl = 0, tu = 0;
+  for (int i = warp; i < n; i += blockDim.x / 32) {
+    const uint32_t ls = pool.lstart[r0 + i], us = pool.ustart[r0 + i];
+    const int ll = pool.llen[r0 + i], ul = pool.ulen[r0 + i];
+    int cl = 0, cu = 0;
+    for (int q = lane; q < ll; q += 32) cl += l_far(pool.lcol[ls + q], i);
+    for (int q = lane; q < ul; q += 32) cu += u_far(pool.ucol[us + q], i);
+    cl = __reduce_add_sync(0xffffffffu, cl);
+    cu = __reduce_add_sync(0xffffffffu, cu);
+    if (lane == 0) {
+      lcnt[r0 + i] = cl;
+      ucnt[r0 + i] = cu;
+      tl += cl;
+      tu += cu;
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(&sl, tl);
+    atomicAdd(&su, tu);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    far_l[b] = static_cast<long long>(sl);
+    far_u[b] = static_cast<long long>(su);
+  }
+}
+
+// Scatter pool rows into near tiles (dense) and far CSR.
+__global__ void __launch_bounds__(256) pack_tiled_kernel(
+    const int* __restrict__ set_row0, const int* __restrict__ blk_dim, PoolView pool,
+    const int* __restrict__ lcnt, const int* __restrict__ ucnt,
     const long long* __restrict__ loff, const long long* __restrict__ uoff,
-    int* __restrict__ lrp, int* __restrict__ urp, double* __restrict__ lval,
-    uint16_t* __restrict__ lcol, double* __restrict__ uval, uint16_t* __restrict__ ucol) {
+    const long long* __restrict__ toff, int* __restrict__ lrp, int* __restrict__ urp,
+    double* __restrict__ lval, uint16_t* __restrict__ lcol, double* __restrict__ uval,
+    uint16_t* __restrict__ ucol, double* __restrict__ ltile, double* __restrict__ utile,
+    double* __restrict__ urdiag) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   int* lr = lrp + r0 + b;
   int* ur = urp + r0 + b;
-  // Block-local exclusive prefix of row lengths (thread 0; n <= a few 1000).
   if (threadIdx.x == 0) {
     int sl = 0, su = 0;
     for (int i = 0; i < n; ++i) {
       lr[i] = sl;
       ur[i] = su;
-      sl += pool.llen[r0 + i];
-      su += pool.ulen[r0 + i];
+      sl += lcnt[r0 + i];
+      su += ucnt[r0 + i];
     }
     lr[n] = sl;
     ur[n] = su;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned ltmask = (1u << lane) - 1u;
   const long long lb = loff[b], ub = uoff[b];
+  double* lt = ltile + toff[b] * kTileElems;
+  double* ut = utile + toff[b] * kTileElems;
   for (int i = warp; i < n; i += blockDim.x / 32) {
-    const uint32_t ls = pool.lstart[r0 + i], us = pool.ustart[r0 + i];
-    const int ll = pool.llen[r0 + i], ul = pool.ulen[r0 + i];
-    const long long ld = lb + lr[i], ud = ub + ur[i];
-    for (int q = lane; q < ll; q += 32) {
-      lval[ld + q] = pool.lval[ls + q];
-      lcol[ld + q] = pool.lcol[ls + q];
+    const int t = i >> 5, j = i & 31;
+    if (lane == 0) urdiag[r0 + i] = 1.0 / pool.udiag[r0 + i];
+    {
+      const uint32_t ls = pool.lstart[r0 + i];
+      const int ll = pool.llen[r0 + i];
+      long long w = lb + lr[i];
+      for (int q0 = 0; q0 < ll; q0 += 32) {
+        const int q = q0 + lane;
+        const bool in = q < ll;
+        const int c = in ? pool.lcol[ls + q] : 0;
+        const double v = in ? pool.lval[ls + q] : 0.0;
+        const bool far = in && l_far(c, i);
+        const unsigned bf = __ballot_sync(0xffffffffu, far);
+        if (far) {
+          lval[w + __popc(bf & ltmask)] = v;
+          lcol[w + __popc(bf & ltmask)] = static_cast<uint16_t>(c);
+        } else if (in) {
+          const int k = c - (t - (kNearTiles - 1)) * kTile;  // 0..95
+          lt[static_cast<long long>(t) * kTileElems + k * kTile + j] = v;
+        }
+        w += __popc(bf);
+      }
     }
-    for (int q = lane; q < ul; q += 32) {
-      uval[ud + q] = pool.uval[us + q];
-      ucol[ud + q] = pool.ucol[us + q];
+    {
+      const uint32_t us = pool.ustart[r0 + i];
+      const int ul = pool.ulen[r0 + i];
+      long long w = ub + ur[i];
+      for (int q0 = 0; q0 < ul; q0 += 32) {
+        const int q = q0 + lane;
+        const bool in = q < ul;
+        const int c = in ? pool.ucol[us + q] : 0;
+        const double v = in ? pool.uval[us + q] : 0.0;
+        const bool far = in && u_far(c, i);
+        const unsigned bf = __ballot_sync(0xffffffffu, far);
+        if (far) {
+          uval[w + __popc(bf & ltmask)] = v;
+          ucol[w + __popc(bf & ltmask)] = static_cast<uint16_t>(c);
+        } else if (in) {
+          const int k = c - t * kTile;  // 0..95
+          ut[static_cast<long long>(t) * kTileElems + k * kTile + j] = v;
+        }
+        w += __popc(bf);
+      }
     }
   }
 }
@@ -660,49 +748,82 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
     break;
   }
 
-  // Pack into the solve layout.
+  // Tiled solve layout (FactorSet, internal.hpp).
   auto t3 = clk::now();
+  fs->h_nnz_l.resize(nb);
+  fs->h_nnz_u.resize(nb);
+  MSCG_CUDA(cudaMemcpyAsync(fs->h_nnz_l.data(), nnzl.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
+  MSCG_CUDA(cudaMemcpyAsync(fs->h_nnz_u.data(), nnzu.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
+  PoolView pv{};
+  pv.lcol = lpool_c.as<uint16_t>();
+  pv.lval = lpool_v.as<double>();
+  pv.ucol = upool_c.as<uint16_t>();
+  pv.uval = upool_v.as<double>();
+  pv.lstart = lstart.as<uint32_t>();
+  pv.llen = llen.as<int>();
+  pv.ustart = ustart.as<uint32_t>();
+  pv.ulen = ulen.as<int>();
+  pv.udiag = fs->udiag.as<double>();
+  DevBuf lcnt(sizeof(int) * total), ucnt(sizeof(int) * total);
+  DevBuf farl(sizeof(long long) * nb), faru(sizeof(long long) * nb);
+  count_far_kernel<<<nb, 256, 0, s>>>(fs->row0.as<int>(), fs->dim.as<int>(), pv, lcnt.as<int>(),
+                                      ucnt.as<int>(), farl.as<long long>(), faru.as<long long>());
+  MSCG_CUDA(cudaGetLastError());
+  ctx->launches++;
   std::vector<long long> hl(nb), hu(nb);
-  MSCG_CUDA(cudaMemcpyAsync(hl.data(), nnzl.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
-  MSCG_CUDA(cudaMemcpyAsync(hu.data(), nnzu.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
+  MSCG_CUDA(cudaMemcpyAsync(hl.data(), farl.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
+  MSCG_CUDA(cudaMemcpyAsync(hu.data(), faru.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
   MSCG_CUDA(cudaStreamSynchronize(s));
   fs->h_loff.assign(nb + 1, 0);
   fs->h_uoff.assign(nb + 1, 0);
+  fs->h_toff.assign(nb + 1, 0);
   for (int b = 0; b < nb; ++b) {
     fs->h_loff[b + 1] = fs->h_loff[b] + hl[b];
     fs->h_uoff[b + 1] = fs->h_uoff[b] + hu[b];
+    fs->h_toff[b + 1] = fs->h_toff[b] + (fs->h_dim[b] + kTile - 1) / kTile;
   }
   fs->loff = upload_vec(fs->h_loff, s);
   fs->uoff = upload_vec(fs->h_uoff, s);
+  fs->toff = upload_vec(fs->h_toff, s);
   fs->lrp = DevBuf(sizeof(int) * (total + nb));
   fs->urp = DevBuf(sizeof(int) * (total + nb));
-  fs->lval = DevBuf(sizeof(double) * std::max<long long>(1, fs->h_loff[nb]));
-  fs->lcol = DevBuf(sizeof(uint16_t) * std::max<long long>(1, fs->h_loff[nb]));
-  fs->uval = DevBuf(sizeof(double) * std::max<long long>(1, fs->h_uoff[nb]));
-  fs->ucol = DevBuf(sizeof(uint16_t) * std::max<long long>(1, fs->h_uoff[nb]));
-  {
-    PoolView pv{};
-    pv.lcol = lpool_c.as<uint16_t>();
-    pv.lval = lpool_v.as<double>();
-    pv.ucol = upool_c.as<uint16_t>();
-    pv.uval = upool_v.as<double>();
-    pv.lstart = lstart.as<uint32_t>();
-    pv.llen = llen.as<int>();
-    pv.ustart = ustart.as<uint32_t>();
-    pv.ulen = ulen.as<int>();
-    pack_kernel<<<nb, 256, 0, s>>>(fs->row0.as<int>(), fs->dim.as<int>(), pv,
-                                   fs->loff.as<long long>(), fs->uoff.as<long long>(),
-                                   fs->lrp.as<int>(), fs->urp.as<int>(), fs->lval.as<double>(),
-                                   fs->lcol.as<uint16_t>(), fs->uval.as<double>(),
-                                   fs->ucol.as<uint16_t>());
-    MSCG_CUDA(cudaGetLastError());
-    ctx->launches++;
-  }
+  fs->lval = DevBuf(sizeof(double) * std::max<long long>(1, fs->far_l()));
+  fs->lcol = DevBuf(sizeof(uint16_t) * std::max<long long>(1, fs->far_l()));
+  fs->uval = DevBuf(sizeof(double) * std::max<long long>(1, fs->far_u()));
+  fs->ucol = DevBuf(sizeof(uint16_t) * std::max<long long>(1, fs->far_u()));
+  const size_t tile_bytes = sizeof(double) * kTileElems * std::max<long long>(1, fs->tiles());
+  fs->ltile = DevBuf(tile_bytes);
+  fs->utile = DevBuf(tile_bytes);
+  fs->urdiag = DevBuf(sizeof(double) * total);
+  MSCG_CUDA(cudaMemsetAsync(fs->ltile.p, 0, tile_bytes, s));
+  MSCG_CUDA(cudaMemsetAsync(fs->utile.p, 0, tile_bytes, s));
+  pack_tiled_kernel<<<nb, 256, 0, s>>>(
+      fs->row0.as<int>(), fs->dim.as<int>(), pv, lcnt.as<int>(), ucnt.as<int>(),
+      fs->loff.as<long long>(), fs->uoff.as<long long>(), fs->toff.as<long long>(),
+      fs->lrp.as<int>(), fs->urp.as<int>(), fs->lval.as<double>(), fs->lcol.as<uint16_t>(),
+      fs->uval.as<double>(), fs->ucol.as<uint16_t>(), fs->ltile.as<double>(),
+      fs->utile.as<double>(), fs->urdiag.as<double>());
+  MSCG_CUDA(cudaGetLastError());
+  ctx->launches++;
   MSCG_CUDA(cudaStreamSynchronize(s));
   if (times) times->pack_s += std::chrono::duration<double>(clk::now() - t3).count();
   return fs;
 }
 
+int64_t FactorSet::nnz_l() const {
+  int64_t s = 0;
+  for (auto v : h_nnz_l) s += v;
+  return s;
+}
+int64_t FactorSet::nnz_u() const {
+  int64_t s = 0;
+  for (auto v : h_nnz_u) s += v;
+  return s;
+}
+
+// Reference layout from the tiled layout: L row = far entries (columns <
+// 32(t-2)) then the nonzeros of the near window; U row = diagonal, near
+// nonzeros, then far entries (columns >= 32(t+3)).
 void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
                      std::vector<int>& lci, std::vector<double>& lv,
                      std::vector<int>& urp, std::vector<int>& uci,
@@ -710,9 +831,11 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
   const int n = fs.h_dim[idx], r0 = fs.h_row0[idx];
   const long long lb = fs.h_loff[idx], le = fs.h_loff[idx + 1];
   const long long ub = fs.h_uoff[idx], ue = fs.h_uoff[idx + 1];
+  const long long t0 = fs.h_toff[idx], nt = fs.h_toff[idx + 1] - t0;
+  const size_t tsz = kTileElems;
   std::vector<int> hlr(n + 1), hur(n + 1);
   std::vector<uint16_t> hlc(le - lb), huc(ue - ub);
-  std::vector<double> hlv(le - lb), huv(ue - ub), hd(n);
+  std::vector<double> hlv(le - lb), huv(ue - ub), hd(n), hlt(tsz * nt), hut(tsz * nt);
   MSCG_CUDA(cudaMemcpy(hlr.data(), fs.lrp.as<int>() + r0 + idx, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
   MSCG_CUDA(cudaMemcpy(hur.data(), fs.urp.as<int>() + r0 + idx, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
   if (le > lb) {
@@ -723,6 +846,8 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
     MSCG_CUDA(cudaMemcpy(huc.data(), fs.ucol.as<uint16_t>() + ub, sizeof(uint16_t) * (ue - ub), cudaMemcpyDeviceToHost));
     MSCG_CUDA(cudaMemcpy(huv.data(), fs.uval.as<double>() + ub, sizeof(double) * (ue - ub), cudaMemcpyDeviceToHost));
   }
+  MSCG_CUDA(cudaMemcpy(hlt.data(), fs.ltile.as<double>() + t0 * tsz, sizeof(double) * tsz * nt, cudaMemcpyDeviceToHost));
+  MSCG_CUDA(cudaMemcpy(hut.data(), fs.utile.as<double>() + t0 * tsz, sizeof(double) * tsz * nt, cudaMemcpyDeviceToHost));
   MSCG_CUDA(cudaMemcpy(hd.data(), fs.udiag.as<double>() + r0, sizeof(double) * n, cudaMemcpyDeviceToHost));
   perm.resize(n);
   if (fs.has_perm && fs.h_exact[idx]) {
@@ -730,16 +855,37 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
   } else {
     std::iota(perm.begin(), perm.end(), 0);
   }
-  lrp.assign(hlr.begin(), hlr.end());
-  lci.assign(hlc.begin(), hlc.end());
-  lv = hlv;
-  // Reference U layout: diagonal first in each row, then the off-diagonals.
+  lrp.assign(n + 1, 0);
   urp.assign(n + 1, 0);
+  lci.clear();
+  lv.clear();
   uci.clear();
   uv.clear();
   for (int i = 0; i < n; ++i) {
+    const int t = i / kTile, j = i % kTile;
+    for (int k = hlr[i]; k < hlr[i + 1]; ++k) {
+      lci.push_back(hlc[k]);
+      lv.push_back(hlv[k]);
+    }
+    for (int k = 0; k < kNearTiles * kTile; ++k) {
+      const int c = (t - (kNearTiles - 1)) * kTile + k;
+      const double v = hlt[t * tsz + k * kTile + j];
+      if (c >= 0 && c < i && v != 0.0) {
+        lci.push_back(c);
+        lv.push_back(v);
+      }
+    }
+    lrp[i + 1] = static_cast<int>(lci.size());
     uci.push_back(i);
     uv.push_back(hd[i]);
+    for (int k = 0; k < kNearTiles * kTile; ++k) {
+      const int c = t * kTile + k;
+      const double v = hut[t * tsz + k * kTile + j];
+      if (c > i && c < n && v != 0.0) {
+        uci.push_back(c);
+        uv.push_back(v);
+      }
+    }
     for (int k = hur[i]; k < hur[i + 1]; ++k) {
       uci.push_back(huc[k]);
       uv.push_back(huv[k]);

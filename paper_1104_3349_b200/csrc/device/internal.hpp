@@ -59,27 +59,46 @@ std::unique_ptr<DevCsr> upload_csr(Ctx* ctx, int nrows, int ncols, const int* rp
 void spmv(const DevCsr& a, const double* x, double* y, const double* base, int mode,
           cudaStream_t s);
 
-// Per-block factors in the solve layout: every block's L (and U) rows are
-// contiguous; columns are block-local uint16; U rows hold only off-diagonal
-// entries, the diagonal sits in udiag.  Row metadata is indexed by
-// row0[b] + b + i (dim+1 offsets per block, relative to the block base).
+// Per-block factors in the tiled solve layout (see trisolve.cu).  Rows of a
+// block are grouped in tiles of kTile = 32 rows.  For tile t:
+//  * L near tile: dense 32 x 96 fp64, column-major (entry [k*32 + j] is row
+//    32t+j, column 32(t-2)+k): tiles t-2, t-1 and the strictly lower
+//    diagonal tile t;
+//  * U near tile: dense 32 x 96, entry [k*32 + j] = row 32t+j, column 32t+k:
+//    the strictly upper diagonal tile t and tiles t+1, t+2;
+//  * far entries (L: columns < 32(t-2); U: columns >= 32(t+3)) in CSR with
+//    block-local uint16 columns, every block's rows contiguous, row offsets
+//    indexed by row0[b] + b + i (dim+1 per block, relative to loff/uoff[b]).
+// The U diagonal is kept apart (udiag) together with its reciprocal.
+// Absent entries are exact zeros in the near tiles (stored factor values are
+// never zero), so the reference CSR is recoverable exactly.
+constexpr int kTile = 32;
+constexpr int kNearTiles = 3;
+constexpr int kTileElems = kNearTiles * kTile * kTile;
 struct FactorSet {
   int nblocks = 0;
   int total_rows = 0;
   int max_dim = 0;
   bool has_perm = false;
   std::vector<int> h_row0, h_dim;          // host copies
-  std::vector<int64_t> h_loff, h_uoff;     // per block entry offsets (+1 total)
+  std::vector<int64_t> h_loff, h_uoff;     // per block far-entry offsets (+1 total)
+  std::vector<int64_t> h_toff;             // per block first tile (+1 total)
+  std::vector<int64_t> h_nnz_l, h_nnz_u;   // true factor counts (U without diagonal)
   std::vector<char> h_exact;               // per block: exact LU (1) or ILUT (0)
   DevBuf row0, dim;                        // int32[nblocks]
   DevBuf loff, uoff;                       // int64[nblocks+1]
+  DevBuf toff;                             // int64[nblocks+1]
   DevBuf lrp, urp;                         // int32[total_rows + nblocks]
-  DevBuf lval, uval;                       // fp64
+  DevBuf lval, uval;                       // fp64 (far entries)
   DevBuf lcol, ucol;                       // uint16
-  DevBuf udiag;                            // fp64[total_rows]
+  DevBuf ltile, utile;                     // fp64 [tiles][2048]
+  DevBuf udiag, urdiag;                    // fp64[total_rows]
   DevBuf perm;                             // int32[total_rows] (local), if has_perm
-  int64_t nnz_l() const { return h_loff.empty() ? 0 : h_loff.back(); }
-  int64_t nnz_u() const { return h_uoff.empty() ? 0 : h_uoff.back(); }
+  int64_t nnz_l() const;
+  int64_t nnz_u() const;
+  int64_t far_l() const { return h_loff.empty() ? 0 : h_loff.back(); }
+  int64_t far_u() const { return h_uoff.empty() ? 0 : h_uoff.back(); }
+  int64_t tiles() const { return h_toff.empty() ? 0 : h_toff.back(); }
 };
 
 // Block descriptor for factorisation input: rows [row0, row0+dim) of a CSR
@@ -105,7 +124,7 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
 // x_b = U_b^-1 L_b^-1 P_b rhs_b for every block b, launched as one kernel
 // (one CTA per block).  out = x, or out = sub - x when sub != nullptr.
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out,
-                    const double* sub, cudaStream_t s);
+                    const double* sub, cudaStream_t s, long long* trace = nullptr);
 
 struct Precond {
   Ctx* ctx = nullptr;
