@@ -452,17 +452,20 @@ __device__ __forceinline__ bool u_far(int c, int i) {
 __global__ void __launch_bounds__(256) count_far_kernel(
     const int* __restrict__ set_row0, const int* __restrict__ blk_dim, PoolView pool,
     int* __restrict__ lcnt, int* __restrict__ ucnt, long long* __restrict__ far_l,
-    long long* __restrict__ far_u) {
+    long long* __restrict__ far_u, long long* __restrict__ items_l,
+    long long* __restrict__ items_u) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ unsigned long long sl, su;
+  __shared__ unsigned long long sl, su, il, iu;
   if (threadIdx.x == 0) {
     sl = 0;
     su = 0;
+    il = 0;
+    iu = 0;
   }
   __syncthreads();
-  unsigned long long tl = 0, tu = 0;
+  unsigned long long tl = 0, tu = 0, jl = 0, ju = 0;
   for (int i = warp; i < n; i += blockDim.x / 32) {
     const uint32_t ls = pool.lstart[r0 + i], us = pool.ustart[r0 + i];
     const int ll = pool.llen[r0 + i], ul = pool.ulen[r0 + i];
@@ -476,16 +479,22 @@ __global__ void __launch_bounds__(256) count_far_kernel(
       ucnt[r0 + i] = cu;
       tl += cl;
       tu += cu;
+      jl += far_segments(cl);
+      ju += far_segments(cu);
     }
   }
   if (lane == 0) {
     atomicAdd(&sl, tl);
     atomicAdd(&su, tu);
+    atomicAdd(&il, jl);
+    atomicAdd(&iu, ju);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     far_l[b] = static_cast<long long>(sl);
     far_u[b] = static_cast<long long>(su);
+    items_l[b] = static_cast<long long>(il);
+    items_u[b] = static_cast<long long>(iu);
   }
 }
 
@@ -497,21 +506,34 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
     const long long* __restrict__ toff, int* __restrict__ lrp, int* __restrict__ urp,
     double* __restrict__ lval, uint16_t* __restrict__ lcol, double* __restrict__ uval,
     uint16_t* __restrict__ ucol, double* __restrict__ ltile, double* __restrict__ utile,
-    double* __restrict__ urdiag) {
+    double* __restrict__ urdiag, const long long* __restrict__ lioff,
+    const long long* __restrict__ uioff, int4* __restrict__ litems, int4* __restrict__ uitems) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   int* lr = lrp + r0 + b;
   int* ur = urp + r0 + b;
   if (threadIdx.x == 0) {
     int sl = 0, su = 0;
+    // Work items {row, segment, begin, end} (entry offsets within the block).
+    auto emit = [](int4*& out, int i, int s, int cnt) {
+      const int ns = far_segments(cnt);
+      for (int k = 0; k < ns; ++k) {
+        const int b0 = s + k * kSeg;
+        *out++ = make_int4(i, k, b0, k == ns - 1 ? s + cnt : b0 + kSeg);
+      }
+    };
+    int4* li = litems + lioff[b];
     for (int i = 0; i < n; ++i) {
       lr[i] = sl;
       ur[i] = su;
+      emit(li, i, sl, lcnt[r0 + i]);
       sl += lcnt[r0 + i];
       su += ucnt[r0 + i];
     }
     lr[n] = sl;
     ur[n] = su;
+    int4* ui = uitems + uioff[b];
+    for (int i = n - 1; i >= 0; --i) emit(ui, i, ur[i], ucnt[r0 + i]);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -766,25 +788,37 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   pv.udiag = fs->udiag.as<double>();
   DevBuf lcnt(sizeof(int) * total), ucnt(sizeof(int) * total);
   DevBuf farl(sizeof(long long) * nb), faru(sizeof(long long) * nb);
+  DevBuf itl(sizeof(long long) * nb), itu(sizeof(long long) * nb);
   count_far_kernel<<<nb, 256, 0, s>>>(fs->row0.as<int>(), fs->dim.as<int>(), pv, lcnt.as<int>(),
-                                      ucnt.as<int>(), farl.as<long long>(), faru.as<long long>());
+                                      ucnt.as<int>(), farl.as<long long>(), faru.as<long long>(),
+                                      itl.as<long long>(), itu.as<long long>());
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
-  std::vector<long long> hl(nb), hu(nb);
+  std::vector<long long> hl(nb), hu(nb), hil(nb), hiu(nb);
   MSCG_CUDA(cudaMemcpyAsync(hl.data(), farl.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
   MSCG_CUDA(cudaMemcpyAsync(hu.data(), faru.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
+  MSCG_CUDA(cudaMemcpyAsync(hil.data(), itl.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
+  MSCG_CUDA(cudaMemcpyAsync(hiu.data(), itu.p, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s));
   MSCG_CUDA(cudaStreamSynchronize(s));
   fs->h_loff.assign(nb + 1, 0);
   fs->h_uoff.assign(nb + 1, 0);
   fs->h_toff.assign(nb + 1, 0);
+  fs->h_lioff.assign(nb + 1, 0);
+  fs->h_uioff.assign(nb + 1, 0);
   for (int b = 0; b < nb; ++b) {
     fs->h_loff[b + 1] = fs->h_loff[b] + hl[b];
     fs->h_uoff[b + 1] = fs->h_uoff[b] + hu[b];
     fs->h_toff[b + 1] = fs->h_toff[b] + (fs->h_dim[b] + kTile - 1) / kTile;
+    fs->h_lioff[b + 1] = fs->h_lioff[b] + hil[b];
+    fs->h_uioff[b + 1] = fs->h_uioff[b] + hiu[b];
   }
   fs->loff = upload_vec(fs->h_loff, s);
   fs->uoff = upload_vec(fs->h_uoff, s);
   fs->toff = upload_vec(fs->h_toff, s);
+  fs->lioff = upload_vec(fs->h_lioff, s);
+  fs->uioff = upload_vec(fs->h_uioff, s);
+  fs->litems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_lioff[nb]));
+  fs->uitems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_uioff[nb]));
   fs->lrp = DevBuf(sizeof(int) * (total + nb));
   fs->urp = DevBuf(sizeof(int) * (total + nb));
   fs->lval = DevBuf(sizeof(double) * std::max<long long>(1, fs->far_l()));
@@ -802,7 +836,8 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
       fs->loff.as<long long>(), fs->uoff.as<long long>(), fs->toff.as<long long>(),
       fs->lrp.as<int>(), fs->urp.as<int>(), fs->lval.as<double>(), fs->lcol.as<uint16_t>(),
       fs->uval.as<double>(), fs->ucol.as<uint16_t>(), fs->ltile.as<double>(),
-      fs->utile.as<double>(), fs->urdiag.as<double>());
+      fs->utile.as<double>(), fs->urdiag.as<double>(), fs->lioff.as<long long>(),
+      fs->uioff.as<long long>(), fs->litems.as<int4>(), fs->uitems.as<int4>());
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
   MSCG_CUDA(cudaStreamSynchronize(s));

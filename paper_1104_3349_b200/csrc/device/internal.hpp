@@ -75,6 +75,16 @@ void spmv(const DevCsr& a, const double* x, double* y, const double* base, int m
 constexpr int kTile = 32;
 constexpr int kNearTiles = 3;
 constexpr int kTileElems = kNearTiles * kTile * kTile;
+// Far entries of a row are cut into work items of kSeg entries (at most
+// kMaxSeg per row; the last item takes the remainder).  Item lists per block
+// and pass (L: rows ascending, U: rows descending) hold int4 {row, seg,
+// begin, end} (far-entry offsets within the block).
+constexpr int kSeg = 512;
+constexpr int kMaxSeg = 4;
+__host__ __device__ inline int far_segments(int nfar) {
+  const int s = (nfar + kSeg - 1) / kSeg;
+  return s < kMaxSeg ? s : kMaxSeg;
+}
 struct FactorSet {
   int nblocks = 0;
   int total_rows = 0;
@@ -91,7 +101,10 @@ struct FactorSet {
   DevBuf lrp, urp;                         // int32[total_rows + nblocks]
   DevBuf lval, uval;                       // fp64 (far entries)
   DevBuf lcol, ucol;                       // uint16
-  DevBuf ltile, utile;                     // fp64 [tiles][2048]
+  DevBuf ltile, utile;                     // fp64 [tiles][kTileElems]
+  std::vector<int64_t> h_lioff, h_uioff;   // per block far work-item offsets (+1)
+  DevBuf lioff, uioff;                     // int64[nblocks+1]
+  DevBuf litems, uitems;                   // int32 (row << 3 | seg)
   DevBuf udiag, urdiag;                    // fp64[total_rows]
   DevBuf perm;                             // int32[total_rows] (local), if has_perm
   int64_t nnz_l() const;

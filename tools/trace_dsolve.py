@@ -1,9 +1,11 @@
-"""Per-row timing trace of the interior-block triangular solve (block 0).
+"""Timing trace of the interior-block triangular solve (block 0).
 
-    python tools/trace_dsolve.py --config cfg2 --out gpurun_out/trace_cfg2.npz
+    python tools/trace_dsolve.py --config cfg2 [--out gpurun_out/trace_cfg2.npz]
 
-Stores clock64 stamps (row start, head reduced, row published) for the L and
-U sweeps plus block 0's factor row lengths, for offline analysis.
+Stores the raw clock64 stamps of block 0 (solver: per tile [data ready, far
+sums ready, tile solved] for the L then U stream; workers: per row [start,
+far dot done, published] at offset 6*ntiles) plus block 0's factor row
+lengths, for offline analysis with tools/trace_tiles.py.
 """
 import argparse
 import ctypes as C
@@ -34,27 +36,18 @@ def main():
     torch.cuda.synchronize()
     f = pc.d_factors(0)
     n = f.upper.nrows
-    buf = np.zeros(6 * n, np.int64)
+    buf = np.zeros(16 * n, np.int64)
     st = _capi.Status()
     for _ in range(3):  # warm
         rc = _capi.lib().mscg_debug_trace_dsolve(pc.h, C.c_void_p(y.data_ptr()),
                                                  C.c_void_p(x.data_ptr()),
-                                                 buf.ctypes.data_as(C.c_void_p), 6 * n,
+                                                 buf.ctypes.data_as(C.c_void_p), 16 * n,
                                                  C.byref(st))
     assert rc == n, (rc, st.message)
-    tr = buf.reshape(2, n, 3)
-    t0 = tr[0, :, 0].min()
-    tr = tr - t0
-    lnnz = np.diff(f.lower.row_offsets)
-    unnz = np.diff(f.upper.row_offsets)
     out = a.out or os.path.join(ROOT, "gpurun_out", f"trace_{a.config}.npz")
-    np.savez_compressed(out, trace=tr, lnnz=lnnz, unnz=unnz)
-    for k, nm in ((0, "L"), (1, "U")):
-        t = tr[k]
-        span = t[:, 2].max() - t[:, 0].min()
-        print(f"{nm}: rows {n} span {span} cyc ({span / 1.9e3:.1f} us @1.9GHz); "
-              f"median row latency {np.median(t[:, 2] - t[:, 0]):.0f} cyc, "
-              f"median head {np.median(t[:, 1] - t[:, 0]):.0f} cyc")
+    np.savez_compressed(out, trace=buf, lnnz=np.diff(f.lower.row_offsets),
+                        unnz=np.diff(f.upper.row_offsets))
+    print("trace written to", out)
 
 
 if __name__ == "__main__":
