@@ -20,6 +20,7 @@
 struct mscg_ctx {
   mscg::Ctx ctx;
   std::mutex mu;
+  mscg::DevBuf scratch;  // device vectors of host-mode calls (guarded by mu)
 };
 struct mscg_csr {
   std::unique_ptr<mscg::DevCsr> owned;
@@ -98,15 +99,33 @@ void with_vectors(mscg_ctx* c, const double* in, size_t nin, double* out, size_t
     return;
   }
   std::lock_guard<std::mutex> lk(c->mu);
-  mscg::DevBuf din(sizeof(double) * std::max<size_t>(1, nin));
-  mscg::DevBuf dout(sizeof(double) * std::max<size_t>(1, nout));
-  double* stage = c->ctx.stage(std::max(nin, nout));
-  std::memcpy(stage, in, sizeof(double) * nin);
-  MSCG_CUDA(cudaMemcpyAsync(din.p, stage, sizeof(double) * nin, cudaMemcpyHostToDevice, s));
-  f(din.as<double>(), dout.as<double>());
-  MSCG_CUDA(cudaMemcpyAsync(stage, dout.p, sizeof(double) * nout, cudaMemcpyDeviceToHost, s));
+  const size_t need = sizeof(double) * (std::max<size_t>(1, nin) + std::max<size_t>(1, nout));
+  if (c->scratch.bytes < need) c->scratch = mscg::DevBuf(need);  // grow-only
+  double* const d_in = c->scratch.as<double>();
+  double* const d_out = d_in + std::max<size_t>(1, nin);
+  // Page-locked caller buffers are copied directly; pageable ones go
+  // through the context's pinned staging buffer.
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool pin_in = pinned(in), pin_out = pinned(out);
+  double* stage = (pin_in && pin_out) ? nullptr : c->ctx.stage(std::max(nin, nout));
+  const double* src = in;
+  if (!pin_in) {
+    std::memcpy(stage, in, sizeof(double) * nin);
+    src = stage;
+  }
+  MSCG_CUDA(cudaMemcpyAsync(d_in, src, sizeof(double) * nin, cudaMemcpyHostToDevice, s));
+  f(d_in, d_out);
+  MSCG_CUDA(cudaMemcpyAsync(pin_out ? out : stage, d_out, sizeof(double) * nout,
+                            cudaMemcpyDeviceToHost, s));
   MSCG_CUDA(cudaStreamSynchronize(s));
-  std::memcpy(out, stage, sizeof(double) * nout);
+  if (!pin_out) std::memcpy(out, stage, sizeof(double) * nout);
 }
 
 }  // namespace

@@ -587,6 +587,23 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
       }
     }
   }
+  // Readiness tile count of every work item (item.y |= need << 8): the solve
+  // must have published `need` tiles of its pass before the item's columns
+  // are all final.  L: highest column's tile + 1; U: tiles above the lowest.
+  __syncthreads();
+  const int nt = (n + kTile - 1) / kTile;
+  for (long long q = lioff[b] + threadIdx.x; q < lioff[b + 1]; q += blockDim.x) {
+    int4 d = litems[q];
+    const int c = lcol[lb + d.w - 1];
+    d.y = (d.y & 0xff) | (((c >> 5) + 1) << 8);
+    litems[q] = d;
+  }
+  for (long long q = uioff[b] + threadIdx.x; q < uioff[b + 1]; q += blockDim.x) {
+    int4 d = uitems[q];
+    const int c = ucol[ub + d.z];
+    d.y = (d.y & 0xff) | ((nt - (c >> 5)) << 8);
+    uitems[q] = d;
+  }
 }
 
 template <class T>

@@ -368,11 +368,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
-      const int i = d.x, k = d.y, ss = d.z, ee = d.w;
+      const int i = d.x, k = d.y & 0xff, ss = d.z, ee = d.w;
       const int item = (i << 3) | k;
       const int t = i / kTile;
       long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
+      // sleep until the tiles this item reads are published (one poll per
+      // warp); per-value sentinels still guard the reads themselves
+      if (lane == 0)
+        while (vload(&done_l) < (d.y >> 8)) __nanosleep(a.sleep_ns);
+      __syncwarp();
       const double acc = seg_dot<kUnroll, kNc>(fv, fc, ss, ee, z, lane, a.sleep_ns);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
@@ -494,12 +499,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
-      const int i = d.x, k = d.y, ss = d.z, ee = d.w;
+      const int i = d.x, k = d.y & 0xff, ss = d.z, ee = d.w;
       const int item = (i << 3) | k;
       const int t = i / kTile;
       const int pos = nt - 1 - t;
       long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
+      if (lane == 0)
+        while (vload(&done_u) < (d.y >> 8)) __nanosleep(a.sleep_ns);
+      __syncwarp();
       const double acc = seg_dot<kUnroll, kNc>(fv, fc, ss, ee, x, lane, a.sleep_ns);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
