@@ -309,10 +309,8 @@ def main():
     torch.cuda.set_device(local)
     pg = None
     if ws > 1:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        pg = dist
+        from paper_1104_3349_b200 import dist as pdist
+        pg = pdist.init("nccl", torch.device("cuda", local))
     import paper_1104_3349_b200 as msc
     ctx = msc.Context(local)
 
@@ -359,9 +357,7 @@ def main():
         clk = clocks.stop()
         if pg:
             pg.barrier()
-            t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            total_ms = float(t.item())
+            total_ms = pdist.max_over_ranks(total_ms, pg, dev)
         ms_step = total_ms / args.steps
         value = ws * args.steps / (total_ms / 1e3)
         # end-to-end through the C ABI with pinned host buffers: every step
@@ -390,9 +386,7 @@ def main():
             e2e_step()
         te = time.perf_counter() - te0
         if pg:
-            t = torch.tensor([te], device=dev, dtype=torch.float64)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            te = float(t.item())
+            te = pdist.max_over_ranks(te, pg, dev)
         e2e = {"value": ws * ke / te, "unit": "applies/s",
                "h2d_bytes_per_step": 2 * 8 * pb.n, "d2h_bytes_per_step": 2 * 8 * pb.n}
         d_solve_ms = (stage_ms[0] + stage_ms[4]) / (2 * args.steps)
