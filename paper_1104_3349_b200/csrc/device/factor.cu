@@ -543,7 +543,16 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   double* ut = utile + toff[b] * kTileElems;
   for (int i = warp; i < n; i += blockDim.x / 32) {
     const int t = i >> 5, j = i & 31;
-    if (lane == 0) urdiag[r0 + i] = 1.0 / pool.udiag[r0 + i];
+    if (lane == 0) {
+      const double rd = 1.0 / pool.udiag[r0 + i];
+      urdiag[r0 + i] = rd;
+      // tile metadata for the solver (see kMetaDiag / kMetaSeg)
+      double* ltm = lt + static_cast<long long>(t) * kTileElems;
+      double* utm = ut + static_cast<long long>(t) * kTileElems;
+      utm[kMetaDiag + j] = rd;
+      ltm[kMetaSeg + j] = __longlong_as_double(far_segments(lcnt[r0 + i]));
+      utm[kMetaSeg + j] = __longlong_as_double(far_segments(ucnt[r0 + i]));
+    }
     {
       const uint32_t ls = pool.lstart[r0 + i];
       const int ll = pool.llen[r0 + i];

@@ -74,7 +74,14 @@ void spmv(const DevCsr& a, const double* x, double* y, const double* base, int m
 // never zero), so the reference CSR is recoverable exactly.
 constexpr int kTile = 32;
 constexpr int kNearTiles = 3;
-constexpr int kTileElems = kNearTiles * kTile * kTile;
+// Each near tile is followed by per-row metadata the chain needs, so that
+// one TMA copy brings everything and the solver warp issues no global loads:
+// [kMetaDiag + j] = 1 / U_jj (U tiles), [kMetaSeg + j] = far work items of
+// row j (int in the low 32 bits).
+constexpr int kNearElems = kNearTiles * kTile * kTile;
+constexpr int kMetaDiag = kNearElems;
+constexpr int kMetaSeg = kNearElems + kTile;
+constexpr int kTileElems = kNearElems + 2 * kTile;
 // Far entries of a row are cut into work items of kSeg entries (at most
 // kMaxSeg per row; the last item takes the remainder).  Item lists per block
 // and pass (L: rows ascending, U: rows descending) hold int4 {row, seg,

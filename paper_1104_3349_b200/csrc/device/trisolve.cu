@@ -9,26 +9,27 @@
 // dependency chain is therefore ~one row deep per row in both triangles,
 // while most bytes sit far from the diagonal.  One CTA (16 warps) per block:
 //
-//  * solver (warp 0) walks the 32-row tiles in order.  The near window of a
-//    tile (diagonal tile + the two neighbour tiles, dense 32 x 96 fp64,
-//    column-major) arrives in shared memory by TMA bulk copy
-//    (cp.async.bulk + mbarrier ring); lane j owns row j, neighbour tiles are
-//    applied from registers through shuffles, and the 32-step diagonal chain
-//    costs one shuffle + one FMA per row.  Per-row scalars of the next tile
-//    are prefetched one tile ahead, and the solver issues no memory fence,
-//    so no outstanding global load ever sits on the chain;
+//  * solver (warp 0) walks the 32-row tiles in order.  Everything a tile
+//    needs — the near window (diagonal tile + the two neighbour tiles, dense
+//    32 x 96 fp64, column-major), the per-row metadata (1/U_jj, number of far
+//    work items) and the tile's slice of the right-hand side / subtrahend —
+//    arrives in shared memory by TMA bulk copies (cp.async.bulk + mbarrier,
+//    double-buffered).  The solver therefore issues no global loads at all:
+//    measured, a solver load queued behind the workers' streaming requests
+//    stalled the chain for ~30K cycles per tile.  Lane j owns row j,
+//    neighbour tiles are applied from registers through shuffles, and the
+//    32-step diagonal chain costs one shuffle + one FMA per row;
 //  * workers (warps 1-15) stream the far entries (L: columns < 32(t-2), U:
 //    columns >= 32(t+3)) from HBM.  Each row's far entries are cut into work
-//    items of kSeg = 512 entries (one 16-deep unrolled round of coalesced
-//    value/column loads per lane), listed per block at setup in the order
-//    the chain consumes them; a worker publishes one partial sum per item
-//    into a shared-memory ring that the solver sums in a fixed order
-//    (deterministic results);
+//    items of kSeg = 512 entries, listed per block at setup in the order the
+//    chain consumes them together with the number of tiles that must be
+//    published first; a worker issues an item's loads, sleeps until its
+//    inputs are final, and publishes one partial sum per item into a
+//    shared-memory ring that the solver sums in a fixed order (deterministic);
 //  * z (L output) and x (U output) live in shared memory.  Readiness is the
 //    value itself: slots start as a signalling-NaN pattern no arithmetic
 //    produces and an aligned 8-byte shared store is single-copy atomic, so
-//    consumers poll the slot (backing off with __nanosleep) and need neither
-//    flags nor fences.
+//    neither flags nor fences sit on the chain.
 // Rounding differs from the reference's sequential row sums by ~1e-16
 // relative, far inside the 1e-10 apply bar.
 #include <cstdlib>
@@ -40,10 +41,11 @@ namespace mscg {
 
 namespace {
 
-// Kernel variants: (warps per CTA, load unroll per lane, read-only path).
-constexpr int kRing = 2;               // near-tile TMA ring depth
+constexpr int kRing = 2;               // TMA ring depth (near tiles + scalars)
 constexpr int kPartRing = 8;           // far-sum ring depth (tiles)
 constexpr int kPartTile = kTile * kMaxSeg;
+constexpr int kVecElems = 40;          // rhs / subtrahend slice: 32 + alignment slack
+constexpr int kSlotElems = kTileElems + 2 * kVecElems;
 constexpr unsigned kTileBytes = kTileElems * sizeof(double);
 
 struct TriArgs {
@@ -62,13 +64,13 @@ struct TriArgs {
   const uint16_t* ucol;
   const double* ltile;
   const double* utile;
-  const double* urdiag;
-  const int4* litems;  // {row, segment, begin, end}
+  const int4* litems;  // {row, segment | need << 8, begin, end}
   const int4* uitems;
-  const int* perm;  // nullable
+  const int* perm;  // nullable (Schur blocks)
   int dim_max;
   long long* trace;  // debug: clock64 stamps for block 0, or null
   unsigned sleep_ns; // worker back-off while polling
+  int pf_items;      // far-data L2 prefetch distance in work items (0 = off)
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -101,6 +103,21 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
+// Fire-and-forget TMA prefetch of [p, p + bytes) into L2.
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// L2 prefetch of far entries [s, e) (values + columns), widened to 16 B.
+__device__ __forceinline__ void prefetch_far(const double* v, const uint16_t* c, int s, int e) {
+  if (e <= s) return;
+  const unsigned long long v0 = reinterpret_cast<unsigned long long>(v + s) & ~15ull;
+  const unsigned long long v1 = (reinterpret_cast<unsigned long long>(v + e) + 15) & ~15ull;
+  const unsigned long long c0 = reinterpret_cast<unsigned long long>(c + s) & ~15ull;
+  const unsigned long long c1 = (reinterpret_cast<unsigned long long>(c + e) + 15) & ~15ull;
+  l2_prefetch(reinterpret_cast<const void*>(v0), static_cast<unsigned>(v1 - v0));
+  l2_prefetch(reinterpret_cast<const void*>(c0), static_cast<unsigned>(c1 - c0));
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -110,43 +127,53 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
-// Fire-and-forget TMA prefetch of [p, p + bytes) into L2 (16-byte granules;
-// allocations are 256-byte aligned, so the rounded range stays inside).
-__device__ __forceinline__ void l2_prefetch(const void* p, long long bytes) {
-  if (bytes <= 0) return;
-  const unsigned long long lo = reinterpret_cast<unsigned long long>(p) & ~15ull;
-  const unsigned long long hi = (reinterpret_cast<unsigned long long>(p) + bytes + 15) & ~15ull;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
-               "r"(static_cast<unsigned>(hi - lo))
-               : "memory");
+// A vector slice [p, p + 32) copied by TMA needs 16-byte aligned ends:
+// copy the enclosing aligned range and remember the offset (0 or 1).
+struct Slice {
+  const double* src;
+  unsigned bytes;
+  int off;
+};
+__device__ __forceinline__ Slice aligned_slice(const double* p, int len) {
+  const unsigned long long a = reinterpret_cast<unsigned long long>(p);
+  const unsigned long long lo = a & ~15ull;
+  const unsigned long long hi = (a + 8ull * len + 15) & ~15ull;
+  return {reinterpret_cast<const double*>(lo), static_cast<unsigned>(hi - lo),
+          static_cast<int>((a - lo) >> 3)};
 }
 
-constexpr int kPrefetchTiles = 4;  // far data / near tiles prefetched ahead
-
-// Partial dot product of entries [s, e) of a far row with the (partially
-// computed) solution vector; all loads of the item are issued before the
-// first wait.
-template <int kUnroll, bool kNc>
+// Partial dot product of far entries [s, e) with the (partially computed)
+// solution vector.  The trip count is warp-uniform (per-lane predicates
+// instead of per-lane loop bounds) so the final reduction runs converged.
+// The first round's loads are issued before the readiness wait (one poll
+// per warp on the tile counter).
+template <int kUnroll>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
-                                          const double* sol, int lane, unsigned ns) {
+                                          const double* sol, int lane, unsigned ns,
+                                          const int* done, int need) {
   double acc = 0.0, acc2 = 0.0;
-  for (int k0 = s + lane; k0 < e; k0 += 32 * kUnroll) {
+  for (int base = s; base < e; base += 32 * kUnroll) {
     double v[kUnroll];
     int c[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int k = k0 + 32 * u;
+      const int k = base + lane + 32 * u;
       if (k < e) {
-        v[u] = kNc ? __ldg(vals + k) : __ldcg(vals + k);
-        c[u] = kNc ? __ldg(cols + k) : __ldcg(cols + k);
+        v[u] = __ldg(vals + k);
+        c[u] = __ldg(cols + k);
       } else {
         v[u] = 0.0;
         c[u] = -1;
       }
     }
-    // Gather all operands first (independent shared loads, pipelined), and
-    // only fall back to polling when one of them is still pending.
+    if (base == s) {
+      if (lane == 0)
+        while (vload(done) < need) __nanosleep(ns);
+      __syncwarp();
+    }
+    // Gather operands (independent shared loads); poll only if one is still
+    // pending (the counter is a hint, the sentinel is the guarantee).
     const volatile double* vs = sol;
     double xv[kUnroll];
     bool pending = false;
@@ -155,10 +182,11 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
       xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
       pending |= is_pending(xv[u]);
     }
-    if (pending) {
+    if (__any_sync(0xffffffffu, pending)) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
         if (c[u] >= 0) xv[u] = wait_ready_lazy(sol + c[u], ns);
+      __syncwarp();
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; u += 2) {
@@ -183,9 +211,7 @@ __device__ __forceinline__ double neighbour(const double* T, int c0, int j, doub
 }
 
 // Solver: lane 0 waits until `expected` far items of the tile were published
-// (one shared-memory poll per warp instead of one per lane and slot), then
-// resets the counter for the ring tile's next use.  Slot values still carry
-// their own readiness (take_far), so no fence orders slot vs counter.
+// (one poll per warp), then resets the counter for the ring tile's next use.
 __device__ __forceinline__ void wait_items(int* counter, int expected, int lane) {
   if (lane == 0 && expected > 0) {
     int spins = 0;
@@ -207,15 +233,18 @@ __device__ __forceinline__ double take_far(double* slots, int nseg, double pend)
   return f;
 }
 
-template <int kWarps, int kUnroll, bool kNc, int kMinBlocks = 1>
-__global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriArgs a,
-                                                            const double* __restrict__ rhs,
-                                                            double* __restrict__ out,
-                                                            const double* __restrict__ sub) {
+__device__ __forceinline__ int meta_int(const double* T, int idx) {
+  return static_cast<int>(__double_as_longlong(T[idx]));
+}
+
+template <int kWarps, int kUnroll, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
+    trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
+                    const double* __restrict__ sub) {
   constexpr int kWorkers = kWarps - 1;
   extern __shared__ __align__(128) double sm[];
-  double* ring = sm;                          // kRing near tiles
-  double* part = ring + kRing * kTileElems;   // [kPartRing][32 rows][kMaxSeg]
+  double* ring = sm;                          // kRing slots: tile | meta | rhs | sub
+  double* part = ring + kRing * kSlotElems;   // [kPartRing][32 rows][kMaxSeg]
   double* z = part + kPartRing * kPartTile;   // dim_max (L output)
   double* x = z + a.dim_max;                  // dim_max (U output)
   __shared__ __align__(8) uint64_t bars[kRing];
@@ -239,92 +268,69 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
   for (int i = threadIdx.x; i < kPartRing * kPartTile; i += blockDim.x) part[i] = pend;
   if (threadIdx.x == 0) {
     done_l = 0;
-    for (int r = 0; r < kPartRing; ++r) cnt[r] = 0;
     done_u = 0;
+    for (int r = 0; r < kPartRing; ++r) cnt[r] = 0;
     for (int r = 0; r < kRing; ++r) mbar_init(&bars[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  // Near-tile stream: items 0..nt-1 = L tiles 0..nt-1, items nt..2nt-1 = U
-  // tiles nt-1..0.  Item q lives in ring slot q % kRing, phase (q / kRing) & 1.
-  auto item_src = [&](int q) -> const double* {
-    return q < nt ? lt + static_cast<long long>(q) * kTileElems
-                  : ut + static_cast<long long>(2 * nt - 1 - q) * kTileElems;
-  };
-  auto refill = [&](int q_done) {  // solver warp: slot of q_done is free
-    __syncwarp();
-    const int q = q_done + kRing;
-    if (lane == 0 && q < 2 * nt) {
-      const int slot = q % kRing;
-      mbar_expect_tx(&bars[slot], kTileBytes);
-      bulk_load(ring + slot * kTileElems, item_src(q), kTileBytes, &bars[slot]);
-    }
-  };
+  // Stream item q: q < nt -> L tile q (+ rhs slice), else U tile 2nt-1-q
+  // (+ subtrahend slice).  Item q lives in slot q % kRing, phase (q/kRing)&1.
   const int* pm = a.perm ? a.perm + r0 : nullptr;
+  auto issue = [&](int q) {  // solver lane 0
+    const int slot = q % kRing;
+    double* dst = ring + slot * kSlotElems;
+    const bool lpass = q < nt;
+    const int t = lpass ? q : 2 * nt - 1 - q;
+    const double* tile = (lpass ? lt : ut) + static_cast<long long>(t) * kTileElems;
+    unsigned bytes = kTileBytes;
+    Slice sr{nullptr, 0, 0};
+    const int len = min(kTile, n - t * kTile);
+    if (lpass && !pm) sr = aligned_slice(rhs + r0 + t * kTile, len);
+    if (!lpass && sub) sr = aligned_slice(sub + r0 + t * kTile, len);
+    bytes += sr.bytes;
+    mbar_expect_tx(&bars[slot], bytes);
+    bulk_load(dst, tile, kTileBytes, &bars[slot]);
+    if (sr.bytes) bulk_load(dst + kTileElems, sr.src, sr.bytes, &bars[slot]);
+    return sr.off;
+  };
+  // Slice offsets of the items in flight (written by solver lane 0).
+  __shared__ int soff[kRing];
   long long* tr = (a.trace && b == 0) ? a.trace : nullptr;
   const int j = lane;
 
   // ================================================================ L pass
   if (warp == 0) {
-    if (lane == 0)
-      for (int q = 0; q < kRing && q < 2 * nt; ++q) {
-        mbar_expect_tx(&bars[q], kTileBytes);
-        bulk_load(ring + q * kTileElems, item_src(q), kTileBytes, &bars[q]);
-      }
-    double zp1 = 0.0, zp2 = 0.0;  // z of tiles t-1, t-2 (lane k = row k)
-    double bnext = 0.0;
-    int fnext = 0;
-    int pf_lo = 0, pf_hi = 0;  // far range of the next prefetch target tile (lane 0)
     if (lane == 0) {
-      // far data of the first kPrefetchTiles tiles, and the item lists
-      const int e0 = lr[min(kPrefetchTiles * kTile, n)];
-      l2_prefetch(a.lval + a.loff[b], 8LL * e0);
-      l2_prefetch(a.lcol + a.loff[b], 2LL * e0);
-      l2_prefetch(a.litems + a.lioff[b], 16LL * (a.lioff[b + 1] - a.lioff[b]));
-      l2_prefetch(a.uitems + a.uioff[b], 16LL * (a.uioff[b + 1] - a.uioff[b]));
-      if (kPrefetchTiles < nt) {
-        pf_lo = lr[kPrefetchTiles * kTile];
-        pf_hi = lr[min((kPrefetchTiles + 1) * kTile, n)];
-      }
+      for (int q = 0; q < kRing && q < 2 * nt; ++q) soff[q] = issue(q);
+      // the block's work-item lists go to L2 once
+      l2_prefetch(reinterpret_cast<const void*>(reinterpret_cast<unsigned long long>(
+                      a.litems + a.lioff[b]) & ~15ull),
+                  16u * static_cast<unsigned>(a.lioff[b + 1] - a.lioff[b]) + 16);
     }
-    if (j < n) {
-      bnext = rhs[r0 + (pm ? pm[j] : j)];
-      fnext = lr[j + 1] - lr[j];
-    }
+    __syncwarp();
+    double zp1 = 0.0, zp2 = 0.0;  // z of tiles t-1, t-2 (lane k = row k)
     for (int t = 0; t < nt; ++t) {
       const int i = t * kTile + j;
       const bool valid = i < n;
-      const double bi = bnext;
-      const int nfar = fnext;
-      const int in = i + kTile;  // prefetch next tile's scalars
-      if (in < n) {
-        bnext = rhs[r0 + (pm ? pm[in] : in)];
-        fnext = lr[in + 1] - lr[in];
-      }
       const int slot = t % kRing;
+      const int off = *reinterpret_cast<volatile int*>(&soff[slot]);
+      // Schur blocks (row_perm): gather the right-hand side directly.
+      double bperm = 0.0;
+      if (pm && valid) bperm = rhs[r0 + pm[i]];
       mbar_wait(&bars[slot], (t / kRing) & 1);
       if (tr && lane == 0) tr[3 * t + 0] = clock64();
-      const double* T = ring + slot * kTileElems;
+      const double* T = ring + slot * kSlotElems;
+      const double bi = valid ? (pm ? bperm : T[kTileElems + off + j]) : 0.0;
+      const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       double nb = 0.0;
       if (t > 1) nb += neighbour(T, 0, j, zp2);
       if (t > 0) nb += neighbour(T, kTile, j, zp1);
-      // diagonal-tile column k of row j (registers when the budget allows)
-      double td[kMinBlocks == 1 ? kTile : 1];
-      if constexpr (kMinBlocks == 1) {
-#pragma unroll
-        for (int k = 0; k < kTile; ++k) td[k] = T[(2 * kTile + k) * kTile + j];
-      }
-      auto dcol = [&](int k) {
-        if constexpr (kMinBlocks == 1) return td[k];
-        else return T[(2 * kTile + k) * kTile + j];
-      };
       double far = 0.0;
-      {
-        const int nseg = (valid && nfar > 0) ? far_segments(nfar) : 0;
-        wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
-        if (nseg) far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
-      }
+      wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
+      if (nseg) far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
+      __syncwarp();
       if (tr && lane == 0) tr[3 * t + 1] = clock64();
       // acc = b_i - (known sums); z_k = acc_k once step k is reached
       double acc = bi - (nb + far);
@@ -333,29 +339,23 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
       for (int k = 0; k < kTile; ++k) {
         const double zk = __shfl_sync(0xffffffffu, acc, k);
         if (j == k) zj = zk;
-        if (j > k) acc = fma(-dcol(k), zk, acc);
+        if (j > k) acc = fma(-T[(2 * kTile + k) * kTile + j], zk, acc);
       }
       if (!valid) zj = 0.0;
       if (valid) *reinterpret_cast<volatile double*>(z + i) = zj;
       zp2 = zp1;
       zp1 = zj;
+      __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
-        *reinterpret_cast<volatile int*>(&done_l) = t + 1;  // part-ring slot reuse only
+        *reinterpret_cast<volatile int*>(&done_l) = t + 1;
         if (tr) tr[3 * t + 2] = clock64();
-        // L2 prefetch ahead of the chain: far data of tile t + kPrefetchTiles
-        // (row pointers loaded one tile earlier) and the near tile stream.
-        const int u = t + kPrefetchTiles;
-        if (u < nt) {
-          l2_prefetch(a.lval + a.loff[b] + pf_lo, 8LL * (pf_hi - pf_lo));
-          l2_prefetch(a.lcol + a.loff[b] + pf_lo, 2LL * (pf_hi - pf_lo));
-          if (u + 1 < nt) {
-            pf_lo = lr[(u + 1) * kTile];
-            pf_hi = lr[min((u + 2) * kTile, n)];
-          }
+        if (t + kRing < 2 * nt) soff[slot] = issue(t + kRing);
+        if (t + kRing + 1 < 2 * nt) {
+          const int q = t + kRing + 1;
+          const int tt = q < nt ? q : 2 * nt - 1 - q;
+          l2_prefetch((q < nt ? lt : ut) + static_cast<long long>(tt) * kTileElems, kTileBytes);
         }
-        if (t + kRing + 1 < 2 * nt) l2_prefetch(item_src(t + kRing + 1), kTileBytes);
       }
-      refill(t);
     }
   } else {
     // workers: far items of L rows, rows ascending
@@ -365,20 +365,22 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
     const int4* items = a.litems + a.lioff[b];
     const int nitems = static_cast<int>(a.lioff[b + 1] - a.lioff[b]);
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
+    if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
+      const int4 d = items[w + kWorkers * lane];
+      prefetch_far(fv, fc, d.z, d.w);
+    }
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
-      const int i = d.x, k = d.y & 0xff, ss = d.z, ee = d.w;
-      const int item = (i << 3) | k;
+      if (lane == 0 && a.pf_items && it + kWorkers * a.pf_items < nitems) {
+        const int4 f = items[it + kWorkers * a.pf_items];
+        prefetch_far(fv, fc, f.z, f.w);
+      }
+      const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
       long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
-      // sleep until the tiles this item reads are published (one poll per
-      // warp); per-value sentinels still guard the reads themselves
-      if (lane == 0)
-        while (vload(&done_l) < (d.y >> 8)) __nanosleep(a.sleep_ns);
-      __syncwarp();
-      const double acc = seg_dot<kUnroll, kNc>(fv, fc, ss, ee, z, lane, a.sleep_ns);
+      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l, d.y >> 8);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
         // ring slot of tile t is free once tile t - kPartRing was consumed
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
         atomicAdd(&cnt[t % kPartRing], 1);
         if (rt) {
           rt[2] = clock64();
-          rt[3] = item;
+          rt[3] = (i << 3) | k;
         }
       }
     }
@@ -398,63 +400,27 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
   // ================================================================ U pass
   if (warp == 0) {
     double xn1 = 0.0, xn2 = 0.0;  // x of tiles t+1, t+2
-    int pf_lo = 0, pf_hi = 0;
-    if (lane == 0) {
-      const int t0 = nt - 1 - kPrefetchTiles;  // tiles above t0 prefetched now
-      const int s0 = ur[max(t0 + 1, 0) * kTile];
-      l2_prefetch(a.uval + a.uoff[b] + s0, 8LL * (ur[n] - s0));
-      l2_prefetch(a.ucol + a.uoff[b] + s0, 2LL * (ur[n] - s0));
-      if (t0 >= 0) {
-        pf_lo = ur[t0 * kTile];
-        pf_hi = ur[min((t0 + 1) * kTile, n)];
-      }
-    }
-    double rdn = 0.0, sin_ = 0.0;
-    int fn = 0;
-    {
-      const int i = (nt - 1) * kTile + j;
-      if (i < n) {
-        rdn = a.urdiag[r0 + i];
-        if (sub) sin_ = sub[r0 + i];
-        fn = ur[i + 1] - ur[i];
-      }
-    }
     for (int tt = 0; tt < nt; ++tt) {
       const int t = nt - 1 - tt;
       const int q = nt + tt;
       const int i = t * kTile + j;
       const bool valid = i < n;
-      const double zi = valid ? z[i] : 0.0;
-      const double rd = rdn, si = sin_;
-      const int nfar = fn;
-      const int ip = i - kTile;  // prefetch next (lower) tile's scalars
-      if (ip >= 0) {
-        rdn = a.urdiag[r0 + ip];
-        if (sub) sin_ = sub[r0 + ip];
-        fn = ur[ip + 1] - ur[ip];
-      }
       const int slot = q % kRing;
+      const int off = *reinterpret_cast<volatile int*>(&soff[slot]);
+      const double zi = valid ? z[i] : 0.0;
       mbar_wait(&bars[slot], (q / kRing) & 1);
       if (tr && lane == 0) tr[3 * q + 0] = clock64();
-      const double* T = ring + slot * kTileElems;
+      const double* T = ring + slot * kSlotElems;
+      const double rd = valid ? T[kMetaDiag + j] : 0.0;
+      const double si = (valid && sub) ? T[kTileElems + off + j] : 0.0;
+      const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       double nb = 0.0;
       if (tt > 0) nb += neighbour(T, kTile, j, xn1);
       if (tt > 1) nb += neighbour(T, 2 * kTile, j, xn2);
-      double td[kMinBlocks == 1 ? kTile : 1];
-      if constexpr (kMinBlocks == 1) {
-#pragma unroll
-        for (int k = 0; k < kTile; ++k) td[k] = T[k * kTile + j];
-      }
-      auto dcol = [&](int k) {
-        if constexpr (kMinBlocks == 1) return td[k];
-        else return T[k * kTile + j];
-      };
       double far = 0.0;
-      {
-        const int nseg = (valid && nfar > 0) ? far_segments(nfar) : 0;
-        wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
-        if (nseg) far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
-      }
+      wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
+      if (nseg) far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
+      __syncwarp();
       if (tr && lane == 0) tr[3 * q + 1] = clock64();
       double acc = zi - (nb + far);
       double xj = 0.0;
@@ -462,7 +428,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
       for (int k = kTile - 1; k >= 0; --k) {
         const double xk = __shfl_sync(0xffffffffu, acc * rd, k);
         if (j == k) xj = xk;
-        if (j < k) acc = fma(-dcol(k), xk, acc);
+        if (j < k) acc = fma(-T[k * kTile + j], xk, acc);
       }
       if (!valid) xj = 0.0;
       if (valid) {
@@ -471,21 +437,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
       }
       xn2 = xn1;
       xn1 = xj;
+      __syncwarp();
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
         if (tr) tr[3 * q + 2] = clock64();
-        const int u = t - kPrefetchTiles;  // far data of the tile kPrefetchTiles below
-        if (u >= 0) {
-          l2_prefetch(a.uval + a.uoff[b] + pf_lo, 8LL * (pf_hi - pf_lo));
-          l2_prefetch(a.ucol + a.uoff[b] + pf_lo, 2LL * (pf_hi - pf_lo));
-          if (u - 1 >= 0) {
-            pf_lo = ur[(u - 1) * kTile];
-            pf_hi = ur[min(u * kTile, n)];
-          }
-        }
-        if (q + kRing + 1 < 2 * nt) l2_prefetch(item_src(q + kRing + 1), kTileBytes);
+        if (q + kRing < 2 * nt) soff[slot] = issue(q + kRing);
+        if (q + kRing + 1 < 2 * nt)
+          l2_prefetch(ut + static_cast<long long>(2 * nt - 1 - (q + kRing + 1)) * kTileElems,
+                      kTileBytes);
       }
-      refill(q);
     }
   } else {
     // workers: far items of U rows, rows descending
@@ -496,19 +456,23 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
     const int nitems = static_cast<int>(a.uioff[b + 1] - a.uioff[b]);
     const long long lit = a.lioff[b + 1] - a.lioff[b];
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
+    if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
+      const int4 d = items[w + kWorkers * lane];
+      prefetch_far(fv, fc, d.z, d.w);
+    }
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
-      const int i = d.x, k = d.y & 0xff, ss = d.z, ee = d.w;
-      const int item = (i << 3) | k;
+      if (lane == 0 && a.pf_items && it + kWorkers * a.pf_items < nitems) {
+        const int4 f = items[it + kWorkers * a.pf_items];
+        prefetch_far(fv, fc, f.z, f.w);
+      }
+      const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
       const int pos = nt - 1 - t;
       long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
-      if (lane == 0)
-        while (vload(&done_u) < (d.y >> 8)) __nanosleep(a.sleep_ns);
-      __syncwarp();
-      const double acc = seg_dot<kUnroll, kNc>(fv, fc, ss, ee, x, lane, a.sleep_ns);
+      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, x, lane, a.sleep_ns, &done_u, d.y >> 8);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
         while (vload(&done_u) < pos - (kPartRing - 1)) __nanosleep(a.sleep_ns);
@@ -517,7 +481,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
         atomicAdd(&cnt[t % kPartRing], 1);
         if (rt) {
           rt[2] = clock64();
-          rt[3] = item;
+          rt[3] = (i << 3) | k;
         }
       }
     }
@@ -527,7 +491,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) trisolve_kernel(TriAr
 }  // namespace
 
 size_t trisolve_smem_bytes(int dim_max) {
-  return sizeof(double) * (static_cast<size_t>(kRing) * kTileElems +
+  return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
                            static_cast<size_t>(kPartRing) * kPartTile +
                            2 * static_cast<size_t>(dim_max));
 }
@@ -551,7 +515,6 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.ucol = fs.ucol.as<uint16_t>();
   a.ltile = fs.ltile.as<double>();
   a.utile = fs.utile.as<double>();
-  a.urdiag = fs.urdiag.as<double>();
   a.litems = fs.litems.as<int4>();
   a.uitems = fs.uitems.as<int4>();
   a.perm = fs.has_perm ? fs.perm.as<int>() : nullptr;
@@ -562,6 +525,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? static_cast<unsigned>(atoi(e)) : 32u;
   }();
   a.sleep_ns = sleep_ns;
+  static const int pf_items = [] {
+    const char* e = getenv("MSCG_TRI_PF");
+    return e ? atoi(e) : 2;
+  }();
+  a.pf_items = pf_items;
   const size_t smem = trisolve_smem_bytes(fs.max_dim);
   if (smem > 227 * 1024)
     throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
@@ -577,17 +545,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     kern<<<fs.nblocks, warps * 32, smem, s>>>(a, rhs, out, sub);
   };
   switch (variant) {
-    case 1: launch(trisolve_kernel<16, 8, true>, 16); break;
-    case 2: launch(trisolve_kernel<16, 16, false>, 16); break;
-    case 3: launch(trisolve_kernel<8, 16, true>, 8); break;
-    case 4: launch(trisolve_kernel<8, 8, true>, 8); break;
-    case 5: launch(trisolve_kernel<8, 16, false>, 8); break;
-    case 6: launch(trisolve_kernel<16, 8, true, 2>, 16); break;
-    case 7: launch(trisolve_kernel<16, 4, true, 2>, 16); break;
-    case 8: launch(trisolve_kernel<12, 8, true, 2>, 12); break;
-    case 9: launch(trisolve_kernel<16, 16, true>, 16); break;
-    // default: 2 CTAs per SM (64 registers) — measured fastest at cfg4
-    default: launch(trisolve_kernel<16, 4, true, 2>, 16); break;
+    case 1: launch(trisolve_kernel<16, 8, 2>, 16); break;   // 2 CTAs/SM, deeper loads
+    case 2: launch(trisolve_kernel<16, 16, 1>, 16); break;  // 1 CTA/SM, 128 registers
+    default: launch(trisolve_kernel<16, 4, 2>, 16); break;  // 2 CTAs/SM (64 registers)
   }
   MSCG_CUDA(cudaGetLastError());
 }
