@@ -71,6 +71,7 @@ struct TriArgs {
   long long* trace;  // debug: clock64 stamps for block 0, or null
   unsigned sleep_ns; // worker back-off while polling
   int pf_items;      // far-data L2 prefetch distance in work items (0 = off)
+  int hint;          // L2 policy: 0 normal, 1 demand evict-first, 2 + prefetch evict-last
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -108,15 +109,49 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// L2 eviction policies (createpolicy) for the far-entry stream: demand loads
+// mark consumed lines evict-first so that lines prefetched for upcoming items
+// survive until they are read.
+__device__ __forceinline__ uint64_t make_policy(int kind) {
+  uint64_t p;
+  if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_far(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_col(const uint16_t* p, uint64_t pol) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+               : "=h"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void l2_prefetch_hint(const void* p, unsigned bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p),
+               "r"(bytes), "l"(pol)
+               : "memory");
+}
+
 // L2 prefetch of far entries [s, e) (values + columns), widened to 16 B.
-__device__ __forceinline__ void prefetch_far(const double* v, const uint16_t* c, int s, int e) {
+__device__ __forceinline__ void prefetch_far(const double* v, const uint16_t* c, int s, int e,
+                                             uint64_t pol) {
   if (e <= s) return;
   const unsigned long long v0 = reinterpret_cast<unsigned long long>(v + s) & ~15ull;
   const unsigned long long v1 = (reinterpret_cast<unsigned long long>(v + e) + 15) & ~15ull;
   const unsigned long long c0 = reinterpret_cast<unsigned long long>(c + s) & ~15ull;
   const unsigned long long c1 = (reinterpret_cast<unsigned long long>(c + e) + 15) & ~15ull;
-  l2_prefetch(reinterpret_cast<const void*>(v0), static_cast<unsigned>(v1 - v0));
-  l2_prefetch(reinterpret_cast<const void*>(c0), static_cast<unsigned>(c1 - c0));
+  l2_prefetch_hint(reinterpret_cast<const void*>(v0), static_cast<unsigned>(v1 - v0), pol);
+  l2_prefetch_hint(reinterpret_cast<const void*>(c0), static_cast<unsigned>(c1 - c0), pol);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -151,7 +186,7 @@ template <int kUnroll>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
-                                          const int* done, int need) {
+                                          const int* done, int need, uint64_t pol) {
   double acc = 0.0, acc2 = 0.0;
   for (int base = s; base < e; base += 32 * kUnroll) {
     double v[kUnroll];
@@ -160,8 +195,8 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
     for (int u = 0; u < kUnroll; ++u) {
       const int k = base + lane + 32 * u;
       if (k < e) {
-        v[u] = __ldg(vals + k);
-        c[u] = __ldg(cols + k);
+        v[u] = ld_far(vals + k, pol);
+        c[u] = ld_col(cols + k, pol);
       } else {
         v[u] = 0.0;
         c[u] = -1;
@@ -260,6 +295,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int* ur = a.urp + r0 + b;
   const double pend = pending_value();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t dpol = make_policy(a.hint >= 1 ? 1 : 0);
+  const uint64_t ppol = make_policy(a.hint >= 2 ? 2 : 0);
 
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     z[i] = pend;
@@ -367,20 +404,20 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
-      prefetch_far(fv, fc, d.z, d.w);
+      prefetch_far(fv, fc, d.z, d.w, ppol);
     }
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
       if (lane == 0 && a.pf_items && it + kWorkers * a.pf_items < nitems) {
         const int4 f = items[it + kWorkers * a.pf_items];
-        prefetch_far(fv, fc, f.z, f.w);
+        prefetch_far(fv, fc, f.z, f.w, ppol);
       }
       const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
       long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l, d.y >> 8);
+      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l, d.y >> 8, dpol);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
         // ring slot of tile t is free once tile t - kPartRing was consumed
@@ -390,7 +427,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         atomicAdd(&cnt[t % kPartRing], 1);
         if (rt) {
           rt[2] = clock64();
-          rt[3] = (i << 3) | k;
+          rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | k;
         }
       }
     }
@@ -458,21 +495,21 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
-      prefetch_far(fv, fc, d.z, d.w);
+      prefetch_far(fv, fc, d.z, d.w, ppol);
     }
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
       if (lane == 0 && a.pf_items && it + kWorkers * a.pf_items < nitems) {
         const int4 f = items[it + kWorkers * a.pf_items];
-        prefetch_far(fv, fc, f.z, f.w);
+        prefetch_far(fv, fc, f.z, f.w, ppol);
       }
       const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
       const int pos = nt - 1 - t;
       long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, x, lane, a.sleep_ns, &done_u, d.y >> 8);
+      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, x, lane, a.sleep_ns, &done_u, d.y >> 8, dpol);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
         while (vload(&done_u) < pos - (kPartRing - 1)) __nanosleep(a.sleep_ns);
@@ -481,7 +518,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         atomicAdd(&cnt[t % kPartRing], 1);
         if (rt) {
           rt[2] = clock64();
-          rt[3] = (i << 3) | k;
+          rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | k;
         }
       }
     }
@@ -527,9 +564,14 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.sleep_ns = sleep_ns;
   static const int pf_items = [] {
     const char* e = getenv("MSCG_TRI_PF");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
   }();
   a.pf_items = pf_items;
+  static const int hint = [] {
+    const char* e = getenv("MSCG_TRI_HINT");
+    return e ? atoi(e) : 0;
+  }();
+  a.hint = hint;
   const size_t smem = trisolve_smem_bytes(fs.max_dim);
   if (smem > 227 * 1024)
     throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
