@@ -166,9 +166,11 @@ int mscg_bench_apply(mscg_precond *pc, const double *y_dev, double *x_dev,
                      double *w_dev, int steps, int with_spmv, double *total_ms,
                      double *stage_ms, int64_t *launches, mscg_status *st);
 
-/* Tracing: one interior-block solve pass with per-row SM clock stamps for
- * block 0 (row start, head reduced, row published) for the L and the U
- * sweep; out holds 6 * dim(block 0) int64.  Returns dim(block 0). */
+/* Tracing (diagnostics): one interior-block solve pass with SM clock stamps
+ * for block 0 — per tile (data landed, far sums in, tile solved) and per far
+ * work item (start, dot done, published, id); see tools/trace_*.py.
+ * cap >= 32 * dim(block 0) int64.
+ * Returns dim(block 0). */
 int mscg_debug_trace_dsolve(mscg_precond *pc, const double *y_dev, double *x_dev,
                             int64_t *out, int cap, mscg_status *st);
 

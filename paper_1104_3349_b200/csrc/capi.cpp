@@ -400,8 +400,8 @@ int mscg_debug_trace_dsolve(mscg_precond* pc, const double* y, double* x, int64_
   int rc = guard(st, [&] {
     const mscg::FactorSet& fs = *pc->pc->D;
     dim0 = fs.h_dim[0];
-    if (cap < 16 * dim0) throw std::invalid_argument("trace buffer too small");
-    mscg::DevBuf tr(sizeof(long long) * 16 * dim0);
+    if (cap < 32 * dim0) throw std::invalid_argument("trace buffer too small");
+    mscg::DevBuf tr(sizeof(long long) * 32 * dim0);
     cudaStream_t s = pc->ctx->ctx.stream;
     MSCG_CUDA(cudaMemsetAsync(tr.p, 0, tr.bytes, s));
     mscg::block_trisolve(fs, y, x, nullptr, s, tr.as<long long>());

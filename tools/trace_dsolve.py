@@ -36,17 +36,29 @@ def main():
     torch.cuda.synchronize()
     f = pc.d_factors(0)
     n = f.upper.nrows
-    buf = np.zeros(16 * n, np.int64)
+    buf = np.zeros(32 * n, np.int64)
     st = _capi.Status()
     for _ in range(3):  # warm
         rc = _capi.lib().mscg_debug_trace_dsolve(pc.h, C.c_void_p(y.data_ptr()),
                                                  C.c_void_p(x.data_ptr()),
-                                                 buf.ctypes.data_as(C.c_void_p), 16 * n,
+                                                 buf.ctypes.data_as(C.c_void_p), 32 * n,
                                                  C.byref(st))
     assert rc == n, (rc, st.message)
     out = a.out or os.path.join(ROOT, "gpurun_out", f"trace_{a.config}.npz")
+    # far work items of block 0 (kSeg = 512 entries, at most 4 per row): the
+    # trace holds 4 stamps per item, then 3 per far chunk
+    def nitems(m, lower):
+        rp, ci = m.row_offsets, m.col_indices
+        tot = 0
+        for i in range(n):
+            c = ci[rp[i]:rp[i + 1]]
+            t = i // 32
+            nf = int((c < 32 * (t - 2)).sum()) if lower else int((c >= 32 * (t + 3)).sum())
+            tot += min(4, (nf + 511) // 512)
+        return tot
     np.savez_compressed(out, trace=buf, lnnz=np.diff(f.lower.row_offsets),
-                        unnz=np.diff(f.upper.row_offsets))
+                        unnz=np.diff(f.upper.row_offsets),
+                        nitems=nitems(f.lower, True) + nitems(f.upper, False))
     print("trace written to", out)
 
 
