@@ -843,6 +843,17 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   fs->toff = upload_vec(fs->h_toff, s);
   fs->lioff = upload_vec(fs->h_lioff, s);
   fs->uioff = upload_vec(fs->h_uioff, s);
+  {
+    // Launch order for the solve: longest blocks first, so the last wave of
+    // CTAs holds the shortest blocks (LPT).  Cost ~ far entries + near tiles.
+    std::vector<int> ord(nb);
+    std::iota(ord.begin(), ord.end(), 0);
+    auto cost = [&](int b) {
+      return hl[b] + hu[b] + 2LL * kTileElems * (fs->h_toff[b + 1] - fs->h_toff[b]);
+    };
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost(x) > cost(y); });
+    fs->order = upload_vec(ord, s);
+  }
   fs->litems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_lioff[nb]));
   fs->uitems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_uioff[nb]));
   fs->lrp = DevBuf(sizeof(int) * (total + nb));

@@ -114,6 +114,7 @@ struct FactorSet {
   DevBuf litems, uitems;                   // int32 (row << 3 | seg)
   DevBuf udiag, urdiag;                    // fp64[total_rows]
   DevBuf perm;                             // int32[total_rows] (local), if has_perm
+  DevBuf order;                            // int32[nblocks] solve launch order (LPT)
   int64_t nnz_l() const;
   int64_t nnz_u() const;
   int64_t far_l() const { return h_loff.empty() ? 0 : h_loff.back(); }

@@ -67,6 +67,7 @@ struct TriArgs {
   const int4* litems;  // {row, segment | need << 8, begin, end}
   const int4* uitems;
   const int* perm;  // nullable (Schur blocks)
+  const int* order; // launch order of the blocks
   int dim_max;
   long long* trace;  // debug: clock64 stamps for block 0, or null
   unsigned sleep_ns; // worker back-off while polling
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   __shared__ int done_l, done_u;
   __shared__ int cnt[kPartRing];  // far items published per ring tile
 
-  const int b = blockIdx.x;
+  const int b = a.order[blockIdx.x];  // heaviest blocks first (LPT)
   const int n = a.dim[b], r0 = a.row0[b];
   const int nt = (n + kTile - 1) / kTile;
   const double* lt = a.ltile + a.toff[b] * kTileElems;
@@ -555,6 +556,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.litems = fs.litems.as<int4>();
   a.uitems = fs.uitems.as<int4>();
   a.perm = fs.has_perm ? fs.perm.as<int>() : nullptr;
+  a.order = fs.order.as<int>();
   a.dim_max = fs.max_dim;
   a.trace = trace;
   static const unsigned sleep_ns = [] {
