@@ -64,6 +64,11 @@ int mscg_ctx_create(int device, mscg_ctx **out, mscg_status *st);
 void mscg_ctx_destroy(mscg_ctx *ctx);
 /* cudaStream_t of the context (as void*), for callers that pass device ptrs. */
 void *mscg_ctx_stream(mscg_ctx *ctx);
+/* Order every later call of this context on `stream` (a cudaStream_t owned by
+ * the caller, e.g. the stream a collective library runs on; NULL is the legacy
+ * default stream); use_own != 0 restores the context's own stream. */
+int mscg_ctx_set_stream(mscg_ctx *ctx, void *stream, int use_own,
+                        mscg_status *st);
 int mscg_ctx_synchronize(mscg_ctx *ctx, mscg_status *st);
 /* Kernels launched by this library since creation (evidence counter). */
 int64_t mscg_ctx_launches(mscg_ctx *ctx);
@@ -128,6 +133,35 @@ int mscg_precond_build_problem(mscg_ctx *ctx, const mscg_problem *pb,
                                double tol_a, int s_a, mscg_precond **out,
                                mscg_status *st);
 void mscg_precond_destroy(mscg_precond *pc);
+/* ---- sharded preconditioner (no reference counterpart) ----
+ * A shard owns interior blocks [block_begin, block_end) of the same split
+ * (its D blocks, E rows and F columns; the Schur factors are replicated).
+ * One apply across ranks, device pointers, global-length vectors:
+ *   apply_shard(phase 0, y, t, -): z1_r = D_r^-1 y1_r, t = F_r z1_r   (n_g)
+ *   caller:  t = sum over ranks of t                    (all-reduce)
+ *   apply_shard(phase 1, y, t, x): x2 = S^-1 (y2 - t), x1_r = z1_r - D_r^-1 E_r x2
+ * Each rank's x holds its interior rows [row_lo, row_hi) and all of x2.
+ * spmv_shard: y1_r = C[rows_r, :] x and y2part = F_r x1_r (+ C22 x2 when
+ * with_interface_block, on exactly one rank); sum y2part over ranks for the
+ * interface rows of C x. */
+int mscg_precond_build_shard(mscg_ctx *ctx, int n, int p, const int *c_rp,
+                             const int *c_ci, const double *c_v, int nblocks,
+                             const int *d_ranges, const int *s_rp,
+                             const int *s_ci, const double *s_v, int nschur,
+                             const int *s_ranges, double tol_a, int s_a,
+                             int block_begin, int block_end, mscg_precond **out,
+                             mscg_status *st);
+int mscg_precond_build_problem_shard(mscg_ctx *ctx, const mscg_problem *pb,
+                                     double tol_a, int s_a, int block_begin,
+                                     int block_end, mscg_precond **out,
+                                     mscg_status *st);
+int mscg_precond_shard_rows(const mscg_precond *pc, int *row_lo, int *row_hi);
+int mscg_precond_apply_shard(mscg_precond *pc, int phase, const double *y_dev,
+                             double *t_dev, double *x_dev, mscg_status *st);
+int mscg_precond_spmv_shard(mscg_precond *pc, const double *x_dev,
+                            double *y_dev, double *y2part_dev,
+                            int with_interface_block, mscg_status *st);
+
 /* MscPreconditioner::apply (preconditioner.cpp:85-114): x = B^-1 y. */
 int mscg_precond_apply(mscg_precond *pc, const double *y, double *x, int mem,
                        mscg_status *st);

@@ -7,6 +7,7 @@ from .msc import (  # noqa: F401
     DeviceMatrix,
     MscError,
     MscPreconditioner,
+    PreconditionerShard,
     Problem,
     SingularMatrixError,
     SolveReport,
@@ -15,6 +16,7 @@ from .msc import (  # noqa: F401
     TriangularFactors,
     build_preconditioner,
     build_preconditioner_arrays,
+    build_preconditioner_shard,
     default_context,
     fill_factor,
     gmres,

@@ -46,6 +46,7 @@ _SIGS = {
     "mscg_ctx_destroy": (None, [vp]),
     "mscg_ctx_stream": (vp, [vp]),
     "mscg_ctx_synchronize": (C.c_int, [vp, C.POINTER(Status)]),
+    "mscg_ctx_set_stream": (C.c_int, [vp, vp, C.c_int, C.POINTER(Status)]),
     "mscg_ctx_launches": (C.c_int64, [vp]),
     "mscg_problem_oseen": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_double, C.c_int,
                                      C.c_int, C.c_int, C.POINTER(vp), C.POINTER(Status)]),
@@ -71,6 +72,14 @@ _SIGS = {
                                      C.POINTER(Status)]),
     "mscg_precond_build_problem": (C.c_int, [vp, vp, C.c_double, C.c_int, C.POINTER(vp),
                                              C.POINTER(Status)]),
+    "mscg_precond_build_shard": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp, vp,
+                                           vp, vp, C.c_int, vp, C.c_double, C.c_int, C.c_int,
+                                           C.c_int, C.POINTER(vp), C.POINTER(Status)]),
+    "mscg_precond_build_problem_shard": (C.c_int, [vp, vp, C.c_double, C.c_int, C.c_int,
+                                                   C.c_int, C.POINTER(vp), C.POINTER(Status)]),
+    "mscg_precond_shard_rows": (C.c_int, [vp, ip, ip]),
+    "mscg_precond_apply_shard": (C.c_int, [vp, C.c_int, vp, vp, vp, C.POINTER(Status)]),
+    "mscg_precond_spmv_shard": (C.c_int, [vp, vp, vp, vp, C.c_int, C.POINTER(Status)]),
     "mscg_precond_destroy": (None, [vp]),
     "mscg_precond_apply": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(Status)]),
     "mscg_precond_stored_nnz": (C.c_int64, [vp]),

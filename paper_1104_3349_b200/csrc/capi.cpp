@@ -145,13 +145,23 @@ int mscg_ctx_create(int device, mscg_ctx** out, mscg_status* st) {
     auto c = std::make_unique<mscg_ctx>();
     c->ctx.device = device;
     MSCG_CUDA(cudaSetDevice(device));
-    MSCG_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
+    MSCG_CUDA(cudaStreamCreateWithFlags(&c->ctx.owned_stream, cudaStreamNonBlocking));
+    c->ctx.stream = c->ctx.owned_stream;
     MSCG_CUDA(cudaDeviceGetAttribute(&c->ctx.sm_count, cudaDevAttrMultiProcessorCount, device));
     *out = c.release();
   });
 }
 
 void mscg_ctx_destroy(mscg_ctx* ctx) { delete ctx; }
+
+int mscg_ctx_set_stream(mscg_ctx* ctx, void* stream, int use_own, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx) throw std::invalid_argument("mscg_ctx_set_stream: null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    MSCG_CUDA(cudaStreamSynchronize(ctx->ctx.stream));
+    ctx->ctx.stream = use_own ? ctx->ctx.owned_stream : static_cast<cudaStream_t>(stream);
+  });
+}
 void* mscg_ctx_stream(mscg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->ctx.stream) : nullptr; }
 int mscg_ctx_synchronize(mscg_ctx* ctx, mscg_status* st) {
   return guard(st, [&] { MSCG_CUDA(cudaStreamSynchronize(ctx->ctx.stream)); });
@@ -275,7 +285,7 @@ void mscg_csr_destroy(mscg_csr* a) { delete a; }
 
 int mscg_spmv(mscg_csr* a, const double* x, double* y, int mem, mscg_status* st) {
   return guard(st, [&] {
-    if (!a) throw std::invalid_argument("matvec: null matrix");
+    if (!a || !a->a) throw std::invalid_argument("matvec: null matrix (a shard has no full C)");
     with_vectors(a->ctx, x, a->a->ncols, y, a->a->nrows, mem, [&](const double* dx, double* dy) {
       mscg::spmv(*a->a, dx, dy, nullptr, 0, a->ctx->ctx.stream);
     });
@@ -315,6 +325,76 @@ int mscg_precond_build_problem(mscg_ctx* ctx, const mscg_problem* pb, double tol
                             s.rp.data(), s.ci.data(), s.v.data(),
                             static_cast<int>(pb->schur.ranges.size()), pb->s_ranges_flat.data(),
                             tol_a, s_a, out, st);
+}
+
+int mscg_precond_build_shard(mscg_ctx* ctx, int n, int p, const int* c_rp, const int* c_ci,
+                             const double* c_v, int nblocks, const int* d_ranges,
+                             const int* s_rp, const int* s_ci, const double* s_v, int nschur,
+                             const int* s_ranges, double tol_a, int s_a, int block_begin,
+                             int block_end, mscg_precond** out, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx) throw std::invalid_argument("build_preconditioner: null context");
+    if (tol_a < 0.0) throw std::invalid_argument("factor_ilut: negative drop tolerance");
+    if (block_begin < 0 || block_end <= block_begin || block_end > nblocks)
+      throw std::invalid_argument("build_preconditioner: shard block range out of range");
+    auto h = std::make_unique<mscg_precond>();
+    h->ctx = ctx;
+    h->pc = mscg::build_precond(&ctx->ctx, n, p, c_rp, c_ci, c_v, pairs(nblocks, d_ranges), s_rp,
+                                s_ci, s_v, pairs(nschur, s_ranges), tol_a, s_a, block_begin,
+                                block_end);
+    h->matrix.a = h->pc->C.get();  // null for a true shard
+    h->matrix.ctx = ctx;
+    *out = h.release();
+  });
+}
+
+int mscg_precond_build_problem_shard(mscg_ctx* ctx, const mscg_problem* pb, double tol_a,
+                                     int s_a, int block_begin, int block_end,
+                                     mscg_precond** out, mscg_status* st) {
+  if (!pb || !pb->have_schur) {
+    set_status(st, MSCG_ERR_INVALID_ARGUMENT,
+               "build_preconditioner: Schur approximation does not match the split");
+    return MSCG_ERR_INVALID_ARGUMENT;
+  }
+  const auto& c = pb->pm.C;
+  const auto& s = pb->schur.s_hat;
+  return mscg_precond_build_shard(
+      ctx, c.nrows, pb->pm.p, c.rp.data(), c.ci.data(), c.v.data(),
+      static_cast<int>(pb->pm.d_ranges.size()), pb->d_ranges_flat.data(), s.rp.data(),
+      s.ci.data(), s.v.data(), static_cast<int>(pb->schur.ranges.size()),
+      pb->s_ranges_flat.data(), tol_a, s_a, block_begin, block_end, out, st);
+}
+
+int mscg_precond_shard_rows(const mscg_precond* pc, int* row_lo, int* row_hi) {
+  if (!pc) return MSCG_ERR_INVALID_ARGUMENT;
+  const auto& sh = pc->pc->shard;
+  if (row_lo) *row_lo = sh.on ? sh.row_lo : 0;
+  if (row_hi) *row_hi = sh.on ? sh.row_hi : pc->pc->p;
+  return MSCG_OK;
+}
+
+int mscg_precond_apply_shard(mscg_precond* pc, int phase, const double* y, double* t, double* x,
+                             mscg_status* st) {
+  return guard(st, [&] {
+    if (!pc || !pc->pc->shard.on)
+      throw std::invalid_argument("mscg_precond_apply_shard: not a shard preconditioner");
+    cudaStream_t s = pc->ctx->ctx.stream;
+    if (phase == 0)
+      pc->pc->apply_shard_begin(y, t, s);
+    else if (phase == 1)
+      pc->pc->apply_shard_end(y, t, x, s);
+    else
+      throw std::invalid_argument("mscg_precond_apply_shard: phase must be 0 or 1");
+  });
+}
+
+int mscg_precond_spmv_shard(mscg_precond* pc, const double* x, double* y, double* y2part,
+                            int with_interface_block, mscg_status* st) {
+  return guard(st, [&] {
+    if (!pc || !pc->pc->shard.on)
+      throw std::invalid_argument("mscg_precond_spmv_shard: not a shard preconditioner");
+    pc->pc->spmv_shard(x, y, y2part, with_interface_block != 0, pc->ctx->ctx.stream);
+  });
 }
 
 void mscg_precond_destroy(mscg_precond* pc) { delete pc; }
@@ -384,7 +464,7 @@ int mscg_precond_nnz(const mscg_precond* pc, int64_t counts[7]) {
   counts[3] = p.S ? p.S->nnz_u() : 0;
   counts[4] = p.E ? p.E->nnz : 0;
   counts[5] = p.F ? p.F->nnz : 0;
-  counts[6] = p.C ? p.C->nnz : 0;
+  counts[6] = p.C ? p.C->nnz : (p.shard.Cr ? p.shard.Cr->nnz : 0);
   return MSCG_OK;
 }
 
@@ -459,6 +539,7 @@ int mscg_gmres(mscg_ctx* ctx, mscg_csr* a, mscg_precond* pc, const double* b, do
       c.left = cfg->side == 1;
       c.orth = cfg->orth;
     }
+    if (!a || !a->a) throw std::invalid_argument("gmres: null matrix");
     const size_t n = a->a->nrows;
     if (a->a->ncols != static_cast<int>(n)) throw std::invalid_argument("gmres: dimension mismatch");
     mscg::GmresResult r;
@@ -483,6 +564,7 @@ int mscg_gmres(mscg_ctx* ctx, mscg_csr* a, mscg_precond* pc, const double* b, do
 int mscg_true_residual(mscg_ctx* ctx, mscg_csr* a, const double* x, const double* b, int mem,
                        double* out, mscg_status* st) {
   return guard(st, [&] {
+    if (!a || !a->a) throw std::invalid_argument("true_residual: null matrix");
     const size_t n = a->a->nrows;
     if (mem == MSCG_MEM_DEVICE) {
       *out = mscg::true_residual(&ctx->ctx, *a->a, x, b);

@@ -28,7 +28,8 @@ struct DevBuf {
 
 struct Ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;        // stream every call is ordered on
+  cudaStream_t owned_stream = nullptr;  // the context's own (destroyed with it)
   int sm_count = 148;
   int64_t launches = 0;
   // pinned staging for host<->device vector traffic
@@ -56,6 +57,7 @@ std::unique_ptr<DevCsr> upload_csr(Ctx* ctx, int nrows, int ncols, const int* rp
                                    const int* ci, const double* v);
 // y = A x                        (mode 0)
 // y = base - A x                 (mode 1)
+// y = base + A x                 (mode 2; base may alias y)
 void spmv(const DevCsr& a, const double* x, double* y, const double* base, int mode,
           cudaStream_t s);
 
@@ -147,6 +149,21 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out,
                     const double* sub, cudaStream_t s, long long* trace = nullptr);
 
+// A shard owns the interior blocks [b0, b1) (rows [row_lo, row_hi)) of a
+// preconditioner split across ranks.  Its D holds only those
+// blocks, E only those rows and F only those columns, so one apply is
+//   rank:      z1_r = D_r^-1 y1_r,  tpart = F_r z1_r          (apply_shard_begin)
+//   exchange:  tsum = sum over ranks of tpart                 (caller: all-reduce)
+//   rank:      z2 = S^-1 (y2 - tsum), x1_r = z1_r - D_r^-1 E_r z2   (apply_shard_end)
+// with S replicated.  Vectors keep the global length; each rank touches its
+// interior rows and the (replicated) interface rows only.
+struct Shard {
+  bool on = false;
+  int b0 = 0, b1 = 0, row_lo = 0, row_hi = 0;
+  std::unique_ptr<DevCsr> Cr;  // C[row_lo:row_hi, :]
+  std::unique_ptr<DevCsr> G;   // C[p:n, p:n]
+};
+
 struct Precond {
   Ctx* ctx = nullptr;
   int n = 0, p = 0;
@@ -154,17 +171,28 @@ struct Precond {
   std::unique_ptr<FactorSet> D, S;
   int64_t stored_nnz = 0;
   FactorTimes times;
+  Shard shard;
   DevBuf z1, t, w;  // scratch (apply is stream-ordered on ctx->stream)
   void apply(const double* y_dev, double* x_dev, cudaStream_t s, cudaEvent_t* ev = nullptr);
+  void apply_shard_begin(const double* y_dev, double* tpart_dev, cudaStream_t s);
+  void apply_shard_end(const double* y_dev, const double* tsum_dev, double* x_dev,
+                       cudaStream_t s);
+  // y1_r = C[rows_r, :] x;  y2part = F_r x1_r (+ G x2 when with_g): the
+  // interface rows of C x are the sum of y2part over ranks.
+  void spmv_shard(const double* x_dev, double* y_dev, double* y2part_dev, bool with_g,
+                  cudaStream_t s);
 };
 
+// Build the whole preconditioner (block_begin = 0, block_end = -1) or the
+// shard owning interior blocks [block_begin, block_end).
 std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
                                        const int* c_ci, const double* c_v,
                                        const std::vector<std::pair<int, int>>& d_ranges,
                                        const int* s_rp, const int* s_ci,
                                        const double* s_v,
                                        const std::vector<std::pair<int, int>>& s_ranges,
-                                       double tol_a, int s_a);
+                                       double tol_a, int s_a, int block_begin = 0,
+                                       int block_end = -1);
 
 // Download one block's factors in the reference layout.
 void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,

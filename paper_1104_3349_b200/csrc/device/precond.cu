@@ -58,7 +58,8 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
                                        const int* s_rp, const int* s_ci,
                                        const double* s_v,
                                        const std::vector<std::pair<int, int>>& s_ranges,
-                                       double tol_a, int s_a) {
+                                       double tol_a, int s_a, int block_begin,
+                                       int block_end) {
   if (p < 0 || p > n) throw Error(1, "build_preconditioner: split out of range");
   if (d_ranges.empty()) throw Error(1, "build_preconditioner: no interior D blocks");
   const int ng = n - p;
@@ -79,25 +80,48 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
     if (cov != ng)
       throw Error(1, "build_preconditioner: Schur approximation does not match the split");
   }
+  const int nb = static_cast<int>(d_ranges.size());
+  const bool sharded = !(block_begin == 0 && (block_end < 0 || block_end == nb));
+  if (block_end < 0) block_end = nb;
+  if (block_begin < 0 || block_begin >= block_end || block_end > nb)
+    throw Error(1, "build_preconditioner: shard block range out of range");
   auto pc = std::make_unique<Precond>();
   pc->ctx = ctx;
   pc->n = n;
   pc->p = p;
-  pc->C = upload_csr(ctx, n, n, c_rp, c_ci, c_v);
+  const int lo = d_ranges[block_begin].first, hi = d_ranges[block_end - 1].second;
   {
     std::vector<int> rp, ci;
     std::vector<double> v;
-    extract(c_rp, c_ci, c_v, 0, p, p, n, rp, ci, v);  // E = C[0:p, p:n]
-    pc->E = upload_csr(ctx, p, ng, rp.data(), ci.data(), v.data());
-    extract(c_rp, c_ci, c_v, p, n, 0, p, rp, ci, v);  // F = C[p:n, 0:p]
-    pc->F = upload_csr(ctx, ng, p, rp.data(), ci.data(), v.data());
+    if (!sharded) {
+      pc->C = upload_csr(ctx, n, n, c_rp, c_ci, c_v);
+      extract(c_rp, c_ci, c_v, 0, p, p, n, rp, ci, v);  // E = C[0:p, p:n]
+      pc->E = upload_csr(ctx, p, ng, rp.data(), ci.data(), v.data());
+      extract(c_rp, c_ci, c_v, p, n, 0, p, rp, ci, v);  // F = C[p:n, 0:p]
+      pc->F = upload_csr(ctx, ng, p, rp.data(), ci.data(), v.data());
+    } else {
+      pc->shard.on = true;
+      pc->shard.b0 = block_begin;
+      pc->shard.b1 = block_end;
+      pc->shard.row_lo = lo;
+      pc->shard.row_hi = hi;
+      extract(c_rp, c_ci, c_v, lo, hi, 0, n, rp, ci, v);  // C[lo:hi, :]
+      pc->shard.Cr = upload_csr(ctx, hi - lo, n, rp.data(), ci.data(), v.data());
+      extract(c_rp, c_ci, c_v, p, n, p, n, rp, ci, v);  // G = C[p:n, p:n]
+      pc->shard.G = upload_csr(ctx, ng, ng, rp.data(), ci.data(), v.data());
+      extract(c_rp, c_ci, c_v, lo, hi, p, n, rp, ci, v);  // E_r = C[lo:hi, p:n]
+      pc->E = upload_csr(ctx, hi - lo, ng, rp.data(), ci.data(), v.data());
+      extract(c_rp, c_ci, c_v, p, n, lo, hi, rp, ci, v);  // F_r = C[p:n, lo:hi]
+      pc->F = upload_csr(ctx, ng, hi - lo, rp.data(), ci.data(), v.data());
+    }
   }
   // Interior blocks: ILUT(tolA) or exact LU when dim <= sA (:44-56).
   {
     DevArrays c(ctx, n, c_rp, c_ci, c_v);
     std::vector<BlockSpec> blocks;
     std::vector<char> exact;
-    for (auto [b, e] : d_ranges) {
+    for (int k = block_begin; k < block_end; ++k) {
+      const auto [b, e] = d_ranges[k];
       blocks.push_back({b, e - b, b});
       exact.push_back((e - b) <= s_a ? 1 : 0);
     }
@@ -116,7 +140,7 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
     pc->S = factor_blocks(ctx, sm.rp.as<int>(), sm.ci.as<int>(), sm.v.as<double>(), blocks, exact,
                           0.0, "build_preconditioner: Schur block", &pc->times);
   }
-  pc->stored_nnz = pc->E->nnz + pc->F->nnz + pc->D->nnz_l() + pc->D->nnz_u() + p;
+  pc->stored_nnz = pc->E->nnz + pc->F->nnz + pc->D->nnz_l() + pc->D->nnz_u() + (hi - lo);
   if (pc->S) pc->stored_nnz += pc->S->nnz_l() + pc->S->nnz_u() + ng;
   pc->z1 = DevBuf(sizeof(double) * std::max(1, p));
   pc->t = DevBuf(sizeof(double) * std::max(1, ng));
@@ -124,7 +148,60 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
   return pc;
 }
 
+namespace {
+__global__ void sub_kernel(int n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __dsub_rn(a[i], b[i]);
+}
+}  // namespace
+
+void Precond::apply_shard_begin(const double* y, double* tpart, cudaStream_t s) {
+  if (!shard.on) throw Error(1, "apply_shard_begin: not a shard");
+  // FactorSet rows are numbered from the set's first row: offset the vectors
+  const int lo = shard.row_lo;
+  double* z1 = this->z1.as<double>();
+  block_trisolve(*D, y + lo, z1 + lo, nullptr, s);
+  ctx->launches++;
+  const int ng = n - p;
+  if (ng > 0) spmv(*F, z1 + lo, tpart, nullptr, 0, s);
+}
+
+void Precond::apply_shard_end(const double* y, const double* tsum, double* x, cudaStream_t s) {
+  if (!shard.on) throw Error(1, "apply_shard_end: not a shard");
+  double* z1 = this->z1.as<double>();
+  double* w = this->w.as<double>();
+  const int ng = n - p;
+  if (S && ng > 0) {
+    double* t = this->t.as<double>();
+    sub_kernel<<<(ng + 255) / 256, 256, 0, s>>>(ng, y + p, tsum, t);
+    MSCG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    block_trisolve(*S, t, x + p, nullptr, s);
+    ctx->launches++;
+    const int lo = shard.row_lo;
+    spmv(*E, x + p, w + lo, nullptr, 0, s);
+    block_trisolve(*D, w + lo, x + lo, z1 + lo, s);
+    ctx->launches++;
+  } else {
+    MSCG_CUDA(cudaMemcpyAsync(x + shard.row_lo, z1 + shard.row_lo,
+                              sizeof(double) * (shard.row_hi - shard.row_lo),
+                              cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+void Precond::spmv_shard(const double* x, double* y, double* y2part, bool with_g,
+                         cudaStream_t s) {
+  if (!shard.on) throw Error(1, "spmv_shard: not a shard");
+  spmv(*shard.Cr, x, y + shard.row_lo, nullptr, 0, s);
+  if (n - p > 0) {
+    spmv(*F, x + shard.row_lo, y2part, nullptr, 0, s);
+    if (with_g) spmv(*shard.G, x + p, y2part, y2part, 2, s);
+  }
+}
+
 void Precond::apply(const double* y, double* x, cudaStream_t s, cudaEvent_t* ev) {
+  if (shard.on) throw Error(1, "MscPreconditioner::apply: this is a shard (use apply_shard_*)");
   // ev (optional): 6 events bracketing the 5 stages (ev[0] before stage 0,
   // ev[k+1] after stage k) for the bench's per-kernel timing.
   double* z1 = this->z1.as<double>();

@@ -36,7 +36,7 @@ double* Ctx::stage(size_t elems) {
 
 Ctx::~Ctx() {
   if (pinned) cudaFreeHost(pinned);
-  if (stream) cudaStreamDestroy(stream);
+  if (owned_stream) cudaStreamDestroy(owned_stream);
 }
 
 }  // namespace mscg

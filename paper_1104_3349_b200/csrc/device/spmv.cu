@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(
     int nrows, int nslices, const int64_t* __restrict__ sptr,
     const int* __restrict__ swidth, const int* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ x,
-    double* __restrict__ y, const double* __restrict__ base, int mode) {
+    double* __restrict__ y, const double* base, int mode) {
   const int slice = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (slice >= nslices) return;
@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(
     const double v = __ldg(val + p0 + 32 * k);
     if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
   }
-  if (row < nrows) y[row] = mode ? __dsub_rn(base[row], acc) : acc;
+  if (row < nrows)
+    y[row] = mode == 0 ? acc : (mode == 1 ? __dsub_rn(base[row], acc) : __dadd_rn(base[row], acc));
 }
 
 }  // namespace

@@ -1,10 +1,11 @@
-"""Multi-process plumbing for bench.py (one process per GPU, torch.distributed).
+"""Multi-process plumbing (one process per GPU, torch.distributed).
 
 The interior blocks of the MSC preconditioner are independent (SURVEY
-§8(e)); the only exchange of a sharded apply is one all-reduce of the n_g
-interface vector.  This round runs replicas (BASELINE puts the path on one
-GPU); these helpers are the rank-level pieces the bench uses and the tests
-exercise with the gloo backend on CPU.
+§8(e)); a sharded apply exchanges one n_g interface vector (all-reduce of the
+per-rank F_r z1_r partials), a sharded SpMV of C one more.  `bench.py --gpus
+N` shards the blocks with `shard_blocks` (libmscg `mscg_precond_*_shard`);
+these helpers are the rank-level pieces the bench uses and the tests exercise
+with the gloo backend on CPU.
 """
 from __future__ import annotations
 

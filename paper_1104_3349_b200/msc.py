@@ -116,6 +116,15 @@ class Context:
     def launches(self) -> int:
         return int(api.lib().mscg_ctx_launches(self.h))
 
+    def set_stream(self, stream_handle: int | None):
+        """Order later calls on an external cudaStream_t (e.g.
+        torch.cuda.current_stream().cuda_stream, so that work and NCCL
+        collectives interleave in stream order); None restores the context's
+        own stream."""
+        st = api.Status()
+        _check(api.lib().mscg_ctx_set_stream(self.h, C.c_void_p(stream_handle or None),
+                                             int(stream_handle is None), C.byref(st)), st)
+
     def torch_stream(self):
         import torch
         return torch.cuda.ExternalStream(self.stream_handle, device=f"cuda:{self.device}")
@@ -395,6 +404,73 @@ def build_preconditioner(problem: Problem, tolA: float = 1e-4, sA: int = 400,
     _check(api.lib().mscg_precond_build_problem(ctx.h, problem.h, tolA, sA, C.byref(h),
                                                 C.byref(st)), st)
     return MscPreconditioner(ctx, h, problem.variant or "msc", sA)
+
+
+class PreconditionerShard:
+    """The interior blocks [block_begin, block_end) of an MSC preconditioner
+    split across ranks: its D blocks, E rows and F columns, with
+    the Schur factors replicated.  Vectors are CUDA float64 tensors of global
+    length n; a rank touches its interior rows `rows` and the interface rows.
+    One apply = apply_begin -> all-reduce(t) over ranks -> apply_end."""
+
+    def __init__(self, ctx: Context, handle, block_begin: int, block_end: int):
+        self.ctx = ctx
+        self.h = handle
+        self.block_begin, self.block_end = block_begin, block_end
+        n, p, nb, ns = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        api.lib().mscg_precond_dims(self.h, C.byref(n), C.byref(p), C.byref(nb), C.byref(ns))
+        self.n, self.p = n.value, p.value
+        lo, hi = C.c_int(), C.c_int()
+        api.lib().mscg_precond_shard_rows(self.h, C.byref(lo), C.byref(hi))
+        self.rows = (lo.value, hi.value)
+
+    @property
+    def n_g(self):
+        return self.n - self.p
+
+    def stored_nnz(self) -> int:
+        return int(api.lib().mscg_precond_stored_nnz(self.h))
+
+    def apply_begin(self, y, t):
+        """z1 = D_r^-1 y1 (own rows); t = F_r z1 (this rank's share of F z1)."""
+        st = api.Status()
+        _check(api.lib().mscg_precond_apply_shard(self.h, 0, C.c_void_p(y.data_ptr()),
+                                                  C.c_void_p(t.data_ptr()), None,
+                                                  C.byref(st)), st)
+
+    def apply_end(self, y, t, x):
+        """With t = F z1 summed over ranks: x2 = S^-1 (y2 - t), x1 = z1 - D_r^-1 E_r x2."""
+        st = api.Status()
+        _check(api.lib().mscg_precond_apply_shard(self.h, 1, C.c_void_p(y.data_ptr()),
+                                                  C.c_void_p(t.data_ptr()),
+                                                  C.c_void_p(x.data_ptr()), C.byref(st)), st)
+
+    def spmv(self, x, y, y2part, with_interface_block: bool):
+        """y[rows] = C[rows, :] x and y2part = F_r x[rows] (+ C22 x2 on one
+        rank); the interface rows of C x are y2part summed over ranks."""
+        st = api.Status()
+        _check(api.lib().mscg_precond_spmv_shard(self.h, C.c_void_p(x.data_ptr()),
+                                                 C.c_void_p(y.data_ptr()),
+                                                 C.c_void_p(y2part.data_ptr()),
+                                                 int(with_interface_block), C.byref(st)), st)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            api.lib().mscg_precond_destroy(self.h)
+            self.h = None
+
+
+def build_preconditioner_shard(problem: Problem, block_begin: int, block_end: int,
+                               tolA: float = 1e-4, sA: int = 400,
+                               ctx: Context | None = None) -> PreconditionerShard:
+    """Factor only the interior blocks [block_begin, block_end) (plus the
+    replicated Schur blocks) on this rank's GPU."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    st = api.Status()
+    _check(api.lib().mscg_precond_build_problem_shard(ctx.h, problem.h, tolA, sA, block_begin,
+                                                      block_end, C.byref(h), C.byref(st)), st)
+    return PreconditionerShard(ctx, h, block_begin, block_end)
 
 
 def build_preconditioner_arrays(ctx: Context, c: SparseMatrix, p: int, d_ranges,

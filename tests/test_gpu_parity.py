@@ -232,3 +232,67 @@ def test_cfg2_ilut_and_apply(msc, ctx, rs, ref):
     assert sum(pc.d_factors(b).nnz() for b in range(pb.nblocks)) == 21083149
     y = ref.random_vector(pb.n, 0)
     assert rel_err(pc.apply(y), M.apply(y)) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_sharded_apply_and_spmv_match_full(msc, ctx, ref, nshards):
+    """the interior blocks split over ranks, one n_g all-reduce
+    per apply.  Ranks are simulated in one process (one GPU); the all-reduce
+    is the sum of the per-shard partials.  The sharded apply must equal the
+    single-GPU apply to the apply bar, the sharded SpMV to rounding of the
+    split interface sums."""
+    import torch
+    from paper_1104_3349_b200 import dist
+    pb = msc.oseen_problem(128, 0.01, 16)
+    pb.build_msc("lum")
+    full = msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=ctx)
+    dr = pb.d_ranges()
+    ranges = dist.shard_blocks(dr[:, 1] - dr[:, 0], nshards)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    try:
+        shards = [msc.build_preconditioner_shard(pb, b0, b1, tolA=1e-4, sA=0, ctx=ctx)
+                  for b0, b1 in ranges]
+        assert sum(s.rows[1] - s.rows[0] for s in shards) == pb.p
+        n, p = pb.n, pb.p
+        y_h = ref.random_vector(n, 3)
+        want = full.apply(y_h)
+        y = torch.from_numpy(y_h).cuda()
+        ts = [torch.empty(n - p, dtype=torch.float64, device="cuda") for _ in shards]
+        xs = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in shards]
+        for s, t in zip(shards, ts):
+            s.apply_begin(y, t)
+        tsum = torch.stack(ts).sum(0)  # the all-reduce
+        for s, x in zip(shards, xs):
+            s.apply_end(y, tsum, x)
+        got = np.empty(n)
+        for s, x in zip(shards, xs):
+            lo, hi = s.rows
+            got[lo:hi] = x[lo:hi].cpu().numpy()
+            assert np.array_equal(x[p:].cpu().numpy(), xs[0][p:].cpu().numpy())
+        got[p:] = xs[0][p:].cpu().numpy()
+        assert rel_err(got, want) <= 1e-12
+        # sharded SpMV of C against the full one
+        A = msc.DeviceMatrix(ctx, pb.C)
+        wy = msc.matvec(A, want)
+        yd = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+        parts = [torch.empty(n - p, dtype=torch.float64, device="cuda") for _ in shards]
+        xd = torch.from_numpy(want).cuda()
+        for k, (s, y2) in enumerate(zip(shards, parts)):
+            s.spmv(xd, yd, y2, with_interface_block=(k == 0))
+        yd[p:] = torch.stack(parts).sum(0)
+        assert rel_err(yd.cpu().numpy(), wy) <= 1e-14
+        assert np.array_equal(yd[:p].cpu().numpy(), wy[:p])  # interior rows: same row sums
+    finally:
+        ctx.set_stream(None)
+
+
+def test_shard_rejects_full_apply(msc, ctx):
+    pb = msc.oseen_problem(32, 0.1, 8)
+    pb.build_msc("lum")
+    s = msc.build_preconditioner_shard(pb, 0, 4, tolA=1e-4, sA=0, ctx=ctx)
+    assert s.rows == (0, int(pb.d_ranges()[3, 1]))
+    from paper_1104_3349_b200 import _capi
+    import ctypes as C
+    st = _capi.Status()
+    rc = _capi.lib().mscg_precond_apply(s.h, None, None, _capi.MEM_DEVICE, C.byref(st))
+    assert rc != 0 and b"shard" in st.message
