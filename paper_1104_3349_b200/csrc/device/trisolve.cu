@@ -204,9 +204,10 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
       }
     }
     if (base == s) {
-      if (lane == 0)
-        while (vload(done) < need) __nanosleep(ns);
-      __syncwarp();
+      // every lane polls the same word: the loop exit is warp-uniform, so
+      // the warp stays converged (divergent spins cost the shuffles below
+      // their fast path)
+      while (vload(done) < need) __nanosleep(ns);
     }
     // Gather operands (independent shared loads); poll only if one is still
     // pending (the counter is a hint, the sentinel is the guarantee).
@@ -218,11 +219,14 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
       xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
       pending |= is_pending(xv[u]);
     }
-    if (__any_sync(0xffffffffu, pending)) {
+    while (__any_sync(0xffffffffu, pending)) {
+      __nanosleep(ns);
+      pending = false;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (c[u] >= 0) xv[u] = wait_ready_lazy(sol + c[u], ns);
-      __syncwarp();
+      for (int u = 0; u < kUnroll; ++u) {
+        if (c[u] >= 0 && is_pending(xv[u])) xv[u] = vs[c[u]];
+        pending |= is_pending(xv[u]);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; u += 2) {
@@ -246,25 +250,36 @@ __device__ __forceinline__ double neighbour(const double* T, int c0, int j, doub
   return (a0 + a1) + (a2 + a3);
 }
 
-// Solver: lane 0 waits until `expected` far items of the tile were published
-// (one poll per warp), then resets the counter for the ring tile's next use.
+// Solver: wait until `expected` far items of the tile were published, then
+// reset the counter for the ring tile's next use.  All lanes poll the same
+// word, so the exit is warp-uniform and the chain that follows keeps the
+// shuffles' converged fast path.
 __device__ __forceinline__ void wait_items(int* counter, int expected, int lane) {
-  if (lane == 0 && expected > 0) {
+  if (expected > 0) {
     int spins = 0;
     while (vload(counter) < expected)
       if (++spins > 8) __nanosleep(20);
-    *reinterpret_cast<volatile int*>(counter) = 0;
+    __syncwarp();
+    if (lane == 0) *reinterpret_cast<volatile int*>(counter) = 0;
   }
   __syncwarp();
 }
 
 // Sum of the published far partial sums of one row, in item order, resetting
-// the slots.
+// the slots.  Warp-uniform trip count (max over the lanes' item counts).
 __device__ __forceinline__ double take_far(double* slots, int nseg, double pend) {
+  const int kmax = __reduce_max_sync(0xffffffffu, nseg);
   double f = 0.0;
-  for (int k = 0; k < nseg; ++k) {
-    f += wait_ready(slots + k);
-    slots[k] = pend;
+  for (int k = 0; k < kmax; ++k) {
+    const bool mine = k < nseg;
+    const volatile double* vp = slots + k;
+    double v = mine ? *vp : 0.0;
+    while (__any_sync(0xffffffffu, mine && is_pending(v)))
+      if (mine) v = *vp;
+    if (mine) {
+      f += v;
+      slots[k] = pend;
+    }
   }
   return f;
 }
@@ -367,7 +382,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (t > 0) nb += neighbour(T, kTile, j, zp1);
       double far = 0.0;
       wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
-      if (nseg) far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
+      far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
       if (tr && lane == 0) tr[3 * t + 1] = clock64();
       // acc = b_i - (known sums); z_k = acc_k once step k is reached
@@ -457,7 +472,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (tt > 1) nb += neighbour(T, 2 * kTile, j, xn2);
       double far = 0.0;
       wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
-      if (nseg) far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
+      far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
       if (tr && lane == 0) tr[3 * q + 1] = clock64();
       double acc = zi - (nb + far);
