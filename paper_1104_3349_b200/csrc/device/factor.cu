@@ -569,7 +569,8 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
           lcol[w + __popc(bf & ltmask)] = static_cast<uint16_t>(c);
         } else if (in) {
           const int k = c - (t - (kNearTiles - 1)) * kTile;  // 0..95
-          lt[static_cast<long long>(t) * kTileElems + k * kTile + j] = v;
+          lt[static_cast<long long>(t) * kTileElems +
+             (k < 2 * kTile ? k * kTile + j : kTriOff + tri_l(j, k - 2 * kTile))] = v;
         }
         w += __popc(bf);
       }
@@ -590,7 +591,8 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
           ucol[w + __popc(bf & ltmask)] = static_cast<uint16_t>(c);
         } else if (in) {
           const int k = c - t * kTile;  // 0..95
-          ut[static_cast<long long>(t) * kTileElems + k * kTile + j] = v;
+          ut[static_cast<long long>(t) * kTileElems +
+             (k < kTile ? kTriOff + tri_u(j, k) : (k - kTile) * kTile + j)] = v;
         }
         w += __popc(bf);
       }
@@ -941,7 +943,9 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
     }
     for (int k = 0; k < kNearTiles * kTile; ++k) {
       const int c = (t - (kNearTiles - 1)) * kTile + k;
-      const double v = hlt[t * tsz + k * kTile + j];
+      const int kd = k - 2 * kTile;
+      if (kd >= j) continue;  // diagonal tile: strictly lower part only
+      const double v = hlt[t * tsz + (kd < 0 ? k * kTile + j : kTriOff + tri_l(j, kd))];
       if (c >= 0 && c < i && v != 0.0) {
         lci.push_back(c);
         lv.push_back(v);
@@ -952,7 +956,8 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
     uv.push_back(hd[i]);
     for (int k = 0; k < kNearTiles * kTile; ++k) {
       const int c = t * kTile + k;
-      const double v = hut[t * tsz + k * kTile + j];
+      if (k < kTile && k <= j) continue;  // diagonal tile: strictly upper part only
+      const double v = hut[t * tsz + (k < kTile ? kTriOff + tri_u(j, k) : (k - kTile) * kTile + j)];
       if (c > i && c < n && v != 0.0) {
         uci.push_back(c);
         uv.push_back(v);

@@ -63,11 +63,10 @@ void spmv(const DevCsr& a, const double* x, double* y, const double* base, int m
 
 // Per-block factors in the tiled solve layout (see trisolve.cu).  Rows of a
 // block are grouped in tiles of kTile = 32 rows.  For tile t:
-//  * L near tile: dense 32 x 96 fp64, column-major (entry [k*32 + j] is row
-//    32t+j, column 32(t-2)+k): tiles t-2, t-1 and the strictly lower
-//    diagonal tile t;
-//  * U near tile: dense 32 x 96, entry [k*32 + j] = row 32t+j, column 32t+k:
-//    the strictly upper diagonal tile t and tiles t+1, t+2;
+//  * L near window: columns 32(t-2) .. 32(t+1): tiles t-2, t-1 and the
+//    strictly lower diagonal tile t;
+//  * U near window: columns 32t .. 32(t+3): the strictly upper diagonal tile
+//    t and tiles t+1, t+2 (stored layout below);
 //  * far entries (L: columns < 32(t-2); U: columns >= 32(t+3)) in CSR with
 //    block-local uint16 columns, every block's rows contiguous, row offsets
 //    indexed by row0[b] + b + i (dim+1 per block, relative to loff/uoff[b]).
@@ -76,11 +75,19 @@ void spmv(const DevCsr& a, const double* x, double* y, const double* base, int m
 // never zero), so the reference CSR is recoverable exactly.
 constexpr int kTile = 32;
 constexpr int kNearTiles = 3;
-// Each near tile is followed by per-row metadata the chain needs, so that
-// one TMA copy brings everything and the solver warp issues no global loads:
-// [kMetaDiag + j] = 1 / U_jj (U tiles), [kMetaSeg + j] = far work items of
-// row j (int in the low 32 bits).
-constexpr int kNearElems = kNearTiles * kTile * kTile;
+// Stored near tile: the two neighbour tiles dense (L: t-2, t-1; U: t+1, t+2;
+// 32 x 64 column-major, entry [k*32 + j]), then the strictly triangular part
+// of the diagonal tile packed by column (tri_l / tri_u), then per-row
+// metadata the chain needs, so that one TMA copy brings everything and the
+// solver warp issues no global loads: [kMetaDiag + j] = 1 / U_jj (U tiles),
+// [kMetaSeg + j] = far work items of row j (int in the low 32 bits).
+constexpr int kNbrElems = 2 * kTile * kTile;
+constexpr int kTriOff = kNbrElems;
+constexpr int kTriElems = kTile * (kTile - 1) / 2;
+// L: column k holds rows k+1..31; U: column k holds rows 0..k-1.
+__host__ __device__ constexpr int tri_l(int j, int k) { return k * (2 * kTile - 1 - k) / 2 + j - k - 1; }
+__host__ __device__ constexpr int tri_u(int j, int k) { return k * (k - 1) / 2 + j; }
+constexpr int kNearElems = kNbrElems + kTriElems;
 constexpr int kMetaDiag = kNearElems;
 constexpr int kMetaSeg = kNearElems + kTile;
 constexpr int kTileElems = kNearElems + 2 * kTile;

@@ -10,9 +10,10 @@
 // while most bytes sit far from the diagonal.  One CTA (16 warps) per block:
 //
 //  * solver (warp 0) walks the 32-row tiles in order.  Everything a tile
-//    needs — the near window (diagonal tile + the two neighbour tiles, dense
-//    32 x 96 fp64, column-major), the per-row metadata (1/U_jj, number of far
-//    work items) and the tile's slice of the right-hand side / subtrahend —
+//    needs — the near window (the two neighbour tiles dense, 32 x 64 fp64
+//    column-major, and the strictly triangular part of the diagonal tile
+//    packed by column), the per-row metadata (1/U_jj, number of far work
+//    items) and the tile's slice of the right-hand side / subtrahend —
 //    arrives in shared memory by TMA bulk copies (cp.async.bulk + mbarrier,
 //    double-buffered).  The solver therefore issues no global loads at all:
 //    measured, a solver load queued behind the workers' streaming requests
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       for (int k = 0; k < kTile; ++k) {
         const double zk = __shfl_sync(0xffffffffu, acc, k);
         if (j == k) zj = zk;
-        if (j > k) acc = fma(-T[(2 * kTile + k) * kTile + j], zk, acc);
+        if (j > k) acc = fma(-T[kTriOff + tri_l(j, k)], zk, acc);
       }
       if (!valid) zj = 0.0;
       if (valid) *reinterpret_cast<volatile double*>(z + i) = zj;
@@ -468,8 +469,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double si = (valid && sub) ? T[kTileElems + off + j] : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       double nb = 0.0;
-      if (tt > 0) nb += neighbour(T, kTile, j, xn1);
-      if (tt > 1) nb += neighbour(T, 2 * kTile, j, xn2);
+      if (tt > 0) nb += neighbour(T, 0, j, xn1);
+      if (tt > 1) nb += neighbour(T, kTile, j, xn2);
       double far = 0.0;
       wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
       far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       for (int k = kTile - 1; k >= 0; --k) {
         const double xk = __shfl_sync(0xffffffffu, acc * rd, k);
         if (j == k) xj = xk;
-        if (j < k) acc = fma(-T[k * kTile + j], xk, acc);
+        if (j < k) acc = fma(-T[kTriOff + tri_u(j, k)], xk, acc);
       }
       if (!valid) xj = 0.0;
       if (valid) {
