@@ -74,6 +74,7 @@ struct TriArgs {
   unsigned sleep_ns; // worker back-off while polling
   int pf_items;      // far-data L2 prefetch distance in work items (0 = off)
   int hint;          // L2 policy: 0 normal, 1 demand evict-first, 2 + prefetch evict-last
+  int near_pf;       // L2 prefetch of the near tile after next (measured: no gain)
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -308,8 +309,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int nt = (n + kTile - 1) / kTile;
   const double* lt = a.ltile + a.toff[b] * kTileElems;
   const double* ut = a.utile + a.toff[b] * kTileElems;
-  const int* lr = a.lrp + r0 + b;
-  const int* ur = a.urp + r0 + b;
   const double pend = pending_value();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t dpol = make_policy(a.hint >= 1 ? 1 : 0);
@@ -374,7 +373,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       double bperm = 0.0;
       if (pm && valid) bperm = rhs[r0 + pm[i]];
       mbar_wait(&bars[slot], (t / kRing) & 1);
-      if (tr && lane == 0) tr[3 * t + 0] = clock64();
+      if (tr && lane == 0) tr[4 * t + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
       const double bi = valid ? (pm ? bperm : T[kTileElems + off + j]) : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
@@ -385,7 +384,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
       far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
-      if (tr && lane == 0) tr[3 * t + 1] = clock64();
+      if (tr && lane == 0) tr[4 * t + 1] = clock64();
       // acc = b_i - (known sums); z_k = acc_k once step k is reached
       double acc = bi - (nb + far);
       double zj = 0.0;
@@ -402,14 +401,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&done_l) = t + 1;
-        if (tr) tr[3 * t + 2] = clock64();
+        if (tr) tr[4 * t + 2] = clock64();
         if (t + kRing < 2 * nt) soff[slot] = issue(t + kRing);
-        if (t + kRing + 1 < 2 * nt) {
+        if (a.near_pf && t + kRing + 1 < 2 * nt) {
           const int q = t + kRing + 1;
           const int tt = q < nt ? q : 2 * nt - 1 - q;
           l2_prefetch((q < nt ? lt : ut) + static_cast<long long>(tt) * kTileElems, kTileBytes);
         }
       }
+      __syncwarp();
+      if (tr && lane == 0) tr[4 * t + 3] = clock64();
     }
   } else {
     // workers: far items of L rows, rows ascending
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       }
       const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
-      long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * it : nullptr;
+      long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
       const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l, d.y >> 8, dpol);
       if (rt) rt[1] = clock64();
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int off = *reinterpret_cast<volatile int*>(&soff[slot]);
       const double zi = valid ? z[i] : 0.0;
       mbar_wait(&bars[slot], (q / kRing) & 1);
-      if (tr && lane == 0) tr[3 * q + 0] = clock64();
+      if (tr && lane == 0) tr[4 * q + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
       const double rd = valid ? T[kMetaDiag + j] : 0.0;
       const double si = (valid && sub) ? T[kTileElems + off + j] : 0.0;
@@ -475,7 +476,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
       far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
-      if (tr && lane == 0) tr[3 * q + 1] = clock64();
+      if (tr && lane == 0) tr[4 * q + 1] = clock64();
       double acc = zi - (nb + far);
       double xj = 0.0;
 #pragma unroll
@@ -494,12 +495,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
-        if (tr) tr[3 * q + 2] = clock64();
+        if (tr) tr[4 * q + 2] = clock64();
         if (q + kRing < 2 * nt) soff[slot] = issue(q + kRing);
-        if (q + kRing + 1 < 2 * nt)
+        if (a.near_pf && q + kRing + 1 < 2 * nt)
           l2_prefetch(ut + static_cast<long long>(2 * nt - 1 - (q + kRing + 1)) * kTileElems,
                       kTileBytes);
       }
+      __syncwarp();
+      if (tr && lane == 0) tr[4 * q + 3] = clock64();
     }
   } else {
     // workers: far items of U rows, rows descending
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
       const int pos = nt - 1 - t;
-      long long* rt = (tr && lane == 0) ? tr + 6LL * nt + 4LL * (lit + it) : nullptr;
+      long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
       const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, x, lane, a.sleep_ns, &done_u, d.y >> 8, dpol);
       if (rt) rt[1] = clock64();
@@ -590,6 +593,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? atoi(e) : 0;
   }();
   a.hint = hint;
+  static const int near_pf = [] {
+    const char* e = getenv("MSCG_TRI_NEARPF");
+    return e ? atoi(e) : 0;
+  }();
+  a.near_pf = near_pf;
   const size_t smem = trisolve_smem_bytes(fs.max_dim);
   if (smem > 227 * 1024)
     throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +

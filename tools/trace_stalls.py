@@ -10,11 +10,11 @@ z = np.load(sys.argv[1])
 buf = z["trace"]
 n = len(z["unnz"])
 nt = (n + 31) // 32
-t = buf[: 6 * nt].reshape(-1, 3)
+t = buf[: 8 * nt].reshape(-1, 4)
 base = t[0, 0]
 t = t - base
 ni = int(z["nitems"])
-it = buf[6 * nt: 6 * nt + 4 * ni].reshape(-1, 4)
+it = buf[8 * nt: 8 * nt + 4 * ni].reshape(-1, 4)
 pe = it[:, 2] - base
 row = (it[:, 3] & 0xffffffff) >> 3
 cut = np.nonzero(np.diff(row) < -40)[0]

@@ -15,14 +15,14 @@ z = np.load(sys.argv[1])
 buf = z["trace"].astype(np.int64)
 n = len(z["unnz"])
 nt = (n + 31) // 32
-t = buf[: 6 * nt].reshape(-1, 3)
+t = buf[: 8 * nt].reshape(-1, 4)
 base = t[0, 0]
 t = t - base
 if "nitems" in z:
     last = int(z["nitems"])
-    items = buf[6 * nt: 6 * nt + 4 * last].reshape(-1, 4)
+    items = buf[8 * nt: 8 * nt + 4 * last].reshape(-1, 4)
 else:
-    items = buf[6 * nt:].reshape(-1, 4)
+    items = buf[8 * nt:].reshape(-1, 4)
     valid = items[:, 0] != 0
     last = np.nonzero(valid)[0].max() + 1
     items = items[:last]
@@ -57,22 +57,3 @@ for name, sl, q0 in (("L", slice(0, nl), 0), ("U", slice(nl, last), nt)):
         lo, hi = np.maximum(np.maximum(s, ready), a), np.minimum(d, b)
         occ.append(np.clip(hi - lo, 0, None).sum() / (KW * (b - a)))
     print("   computing fraction per tenth:", " ".join(f"{o:.2f}" for o in occ))
-
-# far chunk ring (issued, landed, released) if present
-nitems = last
-rest = buf[6 * nt + 4 * nitems:]
-ch = rest[: len(rest) // 3 * 3].reshape(-1, 3) if "nitems" in z else None
-if ch is not None:
-    m = ch[:, 0] != 0
-    ch = ch[: np.nonzero(m)[0].max() + 1] - base if m.any() else ch[:0]
-    ok = (ch[:, 0] > -base) & (ch[:, 1] > -base) & (ch[:, 2] > -base)
-    c = ch[ok]
-    if len(c):
-        land = c[:, 1] - c[:, 0]
-        use = c[:, 2] - c[:, 1]
-        print(f"chunks {len(c)}: issue->first use median {np.median(land):.0f} p90 "
-              f"{np.percentile(land, 90):.0f}; first use->released median {np.median(use):.0f} "
-              f"p90 {np.percentile(use, 90):.0f}")
-        gap = np.diff(c[:, 0])
-        print(f"   issue spacing median {np.median(gap):.0f} cyc "
-              f"-> {2560 / max(1, np.median(gap)):.2f} B/cyc")
