@@ -75,6 +75,7 @@ struct TriArgs {
   int pf_items;      // far-data L2 prefetch distance in work items (0 = off)
   int hint;          // L2 policy: 0 normal, 1 demand evict-first, 2 + prefetch evict-last
   int near_pf;       // L2 prefetch of the near tile after next (measured: no gain)
+  int skip0;         // keep workers off the solver's SM sub-partition
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -239,15 +240,20 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
   return warp_sum(acc + acc2);
 }
 
-// sum_k T[(c0 + k) * 32 + j] * shfl(v, k) over one 32-column neighbour tile.
-__device__ __forceinline__ double neighbour(const double* T, int c0, int j, double v) {
+// sum_k T[(c0 + k) * 32 + j] * v[k] over one 32-column neighbour tile; v is
+// the neighbour tile's solution in shared memory, read as broadcast 16-byte
+// loads (measured: a shuffle costs 3x the issue slots of a broadcast load, and
+// the chain is issue-bound).
+__device__ __forceinline__ double neighbour(const double* T, int c0, int j, const double* v) {
+  const double2* v2 = reinterpret_cast<const double2*>(v);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int k = 0; k < kTile; k += 4) {
-    a0 = fma(T[(c0 + k + 0) * kTile + j], __shfl_sync(0xffffffffu, v, k + 0), a0);
-    a1 = fma(T[(c0 + k + 1) * kTile + j], __shfl_sync(0xffffffffu, v, k + 1), a1);
-    a2 = fma(T[(c0 + k + 2) * kTile + j], __shfl_sync(0xffffffffu, v, k + 2), a2);
-    a3 = fma(T[(c0 + k + 3) * kTile + j], __shfl_sync(0xffffffffu, v, k + 3), a3);
+    const double2 p = v2[k / 2], q = v2[k / 2 + 1];
+    a0 = fma(T[(c0 + k + 0) * kTile + j], p.x, a0);
+    a1 = fma(T[(c0 + k + 1) * kTile + j], p.y, a1);
+    a2 = fma(T[(c0 + k + 2) * kTile + j], q.x, a2);
+    a3 = fma(T[(c0 + k + 3) * kTile + j], q.y, a3);
   }
   return (a0 + a1) + (a2 + a3);
 }
@@ -294,12 +300,15 @@ template <int kWarps, int kUnroll, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
-  constexpr int kWorkers = kWarps - 1;
+  // Workers: warps 1..kWarps-1, or (skip0) only warps off the solver's SM
+  // sub-partition (warp % 4 != 0) so the chain does not share issue slots.
+  const bool skip0 = a.skip0 != 0;
+  const int kWorkers = skip0 ? kWarps - 1 - (kWarps - 1) / 4 : kWarps - 1;
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                          // kRing slots: tile | meta | rhs | sub
   double* part = ring + kRing * kSlotElems;   // [kPartRing][32 rows][kMaxSeg]
   double* z = part + kPartRing * kPartTile;   // dim_max (L output)
-  double* x = z + a.dim_max;                  // dim_max (U output)
+  double* x = z + ((a.dim_max + kTile - 1) & ~(kTile - 1));  // U output
   __shared__ __align__(8) uint64_t bars[kRing];
   __shared__ int done_l, done_u;
   __shared__ int cnt[kPartRing];  // far items published per ring tile
@@ -314,9 +323,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const uint64_t dpol = make_policy(a.hint >= 1 ? 1 : 0);
   const uint64_t ppol = make_policy(a.hint >= 2 ? 2 : 0);
 
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    z[i] = pend;
-    x[i] = pend;
+  for (int i = threadIdx.x; i < nt * kTile; i += blockDim.x) {
+    // rows past the block's end read as zero by the neighbour products
+    z[i] = i < n ? pend : 0.0;
+    x[i] = i < n ? pend : 0.0;
   }
   for (int i = threadIdx.x; i < kPartRing * kPartTile; i += blockDim.x) part[i] = pend;
   if (threadIdx.x == 0) {
@@ -363,7 +373,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
                   16u * static_cast<unsigned>(a.lioff[b + 1] - a.lioff[b]) + 16);
     }
     __syncwarp();
-    double zp1 = 0.0, zp2 = 0.0;  // z of tiles t-1, t-2 (lane k = row k)
     for (int t = 0; t < nt; ++t) {
       const int i = t * kTile + j;
       const bool valid = i < n;
@@ -378,8 +387,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double bi = valid ? (pm ? bperm : T[kTileElems + off + j]) : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       double nb = 0.0;
-      if (t > 1) nb += neighbour(T, 0, j, zp2);
-      if (t > 0) nb += neighbour(T, kTile, j, zp1);
+      if (t > 1) nb += neighbour(T, 0, j, z + (t - 2) * kTile);
+      if (t > 0) nb += neighbour(T, kTile, j, z + (t - 1) * kTile);
       double far = 0.0;
       wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
       far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
@@ -396,8 +405,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       }
       if (!valid) zj = 0.0;
       if (valid) *reinterpret_cast<volatile double*>(z + i) = zj;
-      zp2 = zp1;
-      zp1 = zj;
       __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&done_l) = t + 1;
@@ -414,11 +421,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     }
   } else {
     // workers: far items of L rows, rows ascending
-    const int w = warp - 1;
+    int w = skip0 ? ((warp & 3) ? warp - 1 - (warp >> 2) : -1) : warp - 1;
     const double* fv = a.lval + a.loff[b];
     const uint16_t* fc = a.lcol + a.loff[b];
     const int4* items = a.litems + a.lioff[b];
     const int nitems = static_cast<int>(a.lioff[b + 1] - a.lioff[b]);
+    if (w < 0) w = nitems;  // idle warp on the solver's sub-partition
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
@@ -454,7 +462,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 
   // ================================================================ U pass
   if (warp == 0) {
-    double xn1 = 0.0, xn2 = 0.0;  // x of tiles t+1, t+2
     for (int tt = 0; tt < nt; ++tt) {
       const int t = nt - 1 - tt;
       const int q = nt + tt;
@@ -470,8 +477,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double si = (valid && sub) ? T[kTileElems + off + j] : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       double nb = 0.0;
-      if (tt > 0) nb += neighbour(T, 0, j, xn1);
-      if (tt > 1) nb += neighbour(T, kTile, j, xn2);
+      if (tt > 0) nb += neighbour(T, 0, j, x + (t + 1) * kTile);
+      if (tt > 1) nb += neighbour(T, kTile, j, x + (t + 2) * kTile);
       double far = 0.0;
       wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
       far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
@@ -490,8 +497,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         *reinterpret_cast<volatile double*>(x + i) = xj;
         out[r0 + i] = sub ? si - xj : xj;
       }
-      xn2 = xn1;
-      xn1 = xj;
       __syncwarp();
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
@@ -506,11 +511,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     }
   } else {
     // workers: far items of U rows, rows descending
-    const int w = warp - 1;
+    int w = skip0 ? ((warp & 3) ? warp - 1 - (warp >> 2) : -1) : warp - 1;
     const double* fv = a.uval + a.uoff[b];
     const uint16_t* fc = a.ucol + a.uoff[b];
     const int4* items = a.uitems + a.uioff[b];
     const int nitems = static_cast<int>(a.uioff[b + 1] - a.uioff[b]);
+    if (w < 0) w = nitems;
     const long long lit = a.lioff[b + 1] - a.lioff[b];
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
@@ -550,7 +556,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 size_t trisolve_smem_bytes(int dim_max) {
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
                            static_cast<size_t>(kPartRing) * kPartTile +
-                           2 * static_cast<size_t>(dim_max));
+                           2 * static_cast<size_t>((dim_max + kTile - 1) & ~(kTile - 1)));
 }
 
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const double* sub,
@@ -598,6 +604,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? atoi(e) : 0;
   }();
   a.near_pf = near_pf;
+  static const int skip0 = [] {
+    const char* e = getenv("MSCG_TRI_SKIP0");
+    return e ? atoi(e) : 0;
+  }();
+  a.skip0 = skip0;
   const size_t smem = trisolve_smem_bytes(fs.max_dim);
   if (smem > 227 * 1024)
     throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
