@@ -89,6 +89,15 @@ std::vector<std::pair<int, int>> pairs(int n, const int* flat) {
   return r;
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 // Run `f(dev_in, dev_out)` with host or device vectors.
 template <class F>
 void with_vectors(mscg_ctx* c, const double* in, size_t nin, double* out, size_t nout, int mem,
@@ -105,15 +114,7 @@ void with_vectors(mscg_ctx* c, const double* in, size_t nin, double* out, size_t
   double* const d_out = d_in + std::max<size_t>(1, nin);
   // Page-locked caller buffers are copied directly; pageable ones go
   // through the context's pinned staging buffer.
-  auto pinned = [](const void* p) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    return at.type == cudaMemoryTypeHost;
-  };
-  const bool pin_in = pinned(in), pin_out = pinned(out);
+  const bool pin_in = is_pinned(in), pin_out = is_pinned(out);
   double* stage = (pin_in && pin_out) ? nullptr : c->ctx.stage(std::max(nin, nout));
   const double* src = in;
   if (!pin_in) {
@@ -403,9 +404,31 @@ int mscg_precond_apply(mscg_precond* pc, const double* y, double* x, int mem, ms
   return guard(st, [&] {
     if (!pc) throw std::invalid_argument("MscPreconditioner::apply: null preconditioner");
     const size_t n = pc->pc->n;
-    with_vectors(pc->ctx, y, n, x, n, mem, [&](const double* dy, double* dx) {
-      pc->pc->apply(dy, dx, pc->ctx->ctx.stream);
-    });
+    if (mem == MSCG_MEM_DEVICE) {
+      pc->pc->apply(y, x, pc->ctx->ctx.stream);
+      return;
+    }
+    // Host vectors: chunked apply, copies of one block chunk overlap the
+    // solves of the others (pageable buffers go through pinned staging).
+    mscg_ctx* c = pc->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    const size_t need = sizeof(double) * 2 * std::max<size_t>(1, n);
+    if (c->scratch.bytes < need) c->scratch = mscg::DevBuf(need);
+    double* d_y = c->scratch.as<double>();
+    double* d_x = d_y + std::max<size_t>(1, n);
+    const bool pin_in = is_pinned(y), pin_out = is_pinned(x);
+    double* stage = (pin_in && pin_out) ? nullptr : c->ctx.stage(2 * n);
+    const double* src = y;
+    double* dst = x;
+    if (!pin_in) {
+      std::memcpy(stage, y, sizeof(double) * n);
+      src = stage;
+    }
+    if (!pin_out) dst = stage + n;
+    cudaStream_t s = c->ctx.stream;
+    pc->pc->apply_host(src, dst, d_y, d_x, s);
+    MSCG_CUDA(cudaStreamSynchronize(s));
+    if (!pin_out) std::memcpy(x, dst, sizeof(double) * n);
   });
 }
 

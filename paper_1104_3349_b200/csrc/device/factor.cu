@@ -853,7 +853,12 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
     auto cost = [&](int b) {
       return hl[b] + hu[b] + 2LL * kTileElems * (fs->h_toff[b + 1] - fs->h_toff[b]);
     };
-    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost(x) > cost(y); });
+    fs->h_chunk.assign(kSolveChunks + 1, 0);
+    for (int c = 0; c <= kSolveChunks; ++c)
+      fs->h_chunk[c] = static_cast<int>(static_cast<long long>(nb) * c / kSolveChunks);
+    for (int c = 0; c < kSolveChunks; ++c)
+      std::stable_sort(ord.begin() + fs->h_chunk[c], ord.begin() + fs->h_chunk[c + 1],
+                       [&](int x, int y) { return cost(x) > cost(y); });
     fs->order = upload_vec(ord, s);
   }
   fs->litems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_lioff[nb]));

@@ -95,6 +95,7 @@ constexpr int kTileElems = kNearElems + 2 * kTile;
 // kMaxSeg per row; the last item takes the remainder).  Item lists per block
 // and pass (L: rows ascending, U: rows descending) hold int4 {row, seg,
 // begin, end} (far-entry offsets within the block).
+constexpr int kSolveChunks = 4;
 constexpr int kSeg = 512;
 constexpr int kMaxSeg = 4;
 __host__ __device__ inline int far_segments(int nfar) {
@@ -123,7 +124,13 @@ struct FactorSet {
   DevBuf litems, uitems;                   // int32 (row << 3 | seg)
   DevBuf udiag, urdiag;                    // fp64[total_rows]
   DevBuf perm;                             // int32[total_rows] (local), if has_perm
-  DevBuf order;                            // int32[nblocks] solve launch order (LPT)
+  DevBuf order;                            // int32[nblocks] solve launch order
+  // The blocks are cut into kSolveChunks contiguous chunks (block index
+  // ranges h_chunk[c] .. h_chunk[c+1]); `order` lists each chunk's blocks
+  // longest first (LPT) at the same positions, so a chunk can be solved on
+  // its own (host-buffer applies overlap the copies of one chunk with the
+  // solve of another).
+  std::vector<int> h_chunk;
   int64_t nnz_l() const;
   int64_t nnz_u() const;
   int64_t far_l() const { return h_loff.empty() ? 0 : h_loff.back(); }
@@ -154,7 +161,8 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
 // x_b = U_b^-1 L_b^-1 P_b rhs_b for every block b, launched as one kernel
 // (one CTA per block).  out = x, or out = sub - x when sub != nullptr.
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out,
-                    const double* sub, cudaStream_t s, long long* trace = nullptr);
+                    const double* sub, cudaStream_t s, long long* trace = nullptr,
+                    int chunk = -1);
 
 // A shard owns the interior blocks [b0, b1) (rows [row_lo, row_hi)) of a
 // preconditioner split across ranks.  Its D holds only those
@@ -181,6 +189,12 @@ struct Precond {
   Shard shard;
   DevBuf z1, t, w;  // scratch (apply is stream-ordered on ctx->stream)
   void apply(const double* y_dev, double* x_dev, cudaStream_t s, cudaEvent_t* ev = nullptr);
+  // x = B^-1 y with y, x in page-locked host memory: the interior rows move
+  // in kSolveChunks pieces on side streams so that each piece's copy overlaps
+  // the solve of the others.  d_y, d_x: device scratch of n doubles.
+  void apply_host(const double* y_host, double* x_host, double* d_y, double* d_x,
+                  cudaStream_t s);
+  ~Precond();
   void apply_shard_begin(const double* y_dev, double* tpart_dev, cudaStream_t s);
   void apply_shard_end(const double* y_dev, const double* tsum_dev, double* x_dev,
                        cudaStream_t s);
@@ -188,6 +202,10 @@ struct Precond {
   // interface rows of C x are the sum of y2part over ranks.
   void spmv_shard(const double* x_dev, double* y_dev, double* y2part_dev, bool with_g,
                   cudaStream_t s);
+
+ private:
+  cudaStream_t side[kSolveChunks] = {};
+  cudaEvent_t ev_in[kSolveChunks] = {}, ev_out[kSolveChunks] = {}, ev_mid = nullptr;
 };
 
 // Build the whole preconditioner (block_begin = 0, block_end = -1) or the

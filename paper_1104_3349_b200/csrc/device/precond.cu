@@ -200,6 +200,81 @@ void Precond::spmv_shard(const double* x, double* y, double* y2part, bool with_g
   }
 }
 
+Precond::~Precond() {
+  for (int c = 0; c < kSolveChunks; ++c) {
+    if (side[c]) cudaStreamDestroy(side[c]);
+    if (ev_in[c]) cudaEventDestroy(ev_in[c]);
+    if (ev_out[c]) cudaEventDestroy(ev_out[c]);
+  }
+  if (ev_mid) cudaEventDestroy(ev_mid);
+}
+
+void Precond::apply_host(const double* y_h, double* x_h, double* d_y, double* d_x,
+                         cudaStream_t s) {
+  if (shard.on) throw Error(1, "MscPreconditioner::apply: this is a shard (use apply_shard_*)");
+  if (!side[0]) {
+    for (int c = 0; c < kSolveChunks; ++c) {
+      MSCG_CUDA(cudaStreamCreateWithFlags(&side[c], cudaStreamNonBlocking));
+      MSCG_CUDA(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
+      MSCG_CUDA(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
+    }
+    MSCG_CUDA(cudaEventCreateWithFlags(&ev_mid, cudaEventDisableTiming));
+  }
+  double* z1 = this->z1.as<double>();
+  double* t = this->t.as<double>();
+  double* w = this->w.as<double>();
+  const int ng = n - p;
+  auto rows = [&](int c, int& lo, int& hi) {
+    const int b0 = D->h_chunk[c], b1 = D->h_chunk[c + 1];
+    lo = b0 < D->nblocks ? D->h_row0[b0] : p;
+    hi = b1 < D->nblocks ? D->h_row0[b1] : p;
+  };
+  // order the side streams after earlier work on s (scratch reuse)
+  MSCG_CUDA(cudaEventRecord(ev_mid, s));
+  // 1. per chunk: y rows in, z1 = D^-1 y1 on those blocks
+  for (int c = 0; c < kSolveChunks; ++c) {
+    int lo, hi;
+    rows(c, lo, hi);
+    MSCG_CUDA(cudaStreamWaitEvent(side[c], ev_mid, 0));
+    if (hi > lo)
+      MSCG_CUDA(cudaMemcpyAsync(d_y + lo, y_h + lo, sizeof(double) * (hi - lo),
+                                cudaMemcpyHostToDevice, side[c]));
+    block_trisolve(*D, d_y, z1, nullptr, side[c], nullptr, c);
+    ctx->launches++;
+    MSCG_CUDA(cudaEventRecord(ev_in[c], side[c]));
+  }
+  if (ng > 0)
+    MSCG_CUDA(cudaMemcpyAsync(d_y + p, y_h + p, sizeof(double) * ng, cudaMemcpyHostToDevice, s));
+  for (int c = 0; c < kSolveChunks; ++c) MSCG_CUDA(cudaStreamWaitEvent(s, ev_in[c], 0));
+  // 2. interface (whole vector, on s)
+  if (S) {
+    spmv(*F, z1, t, d_y + p, 1, s);
+    block_trisolve(*S, t, d_x + p, nullptr, s);
+    ctx->launches++;
+    MSCG_CUDA(cudaMemcpyAsync(x_h + p, d_x + p, sizeof(double) * ng, cudaMemcpyDeviceToHost, s));
+    spmv(*E, d_x + p, w, nullptr, 0, s);
+  }
+  MSCG_CUDA(cudaEventRecord(ev_mid, s));
+  // 3. per chunk: x1 = z1 - D^-1 w on those blocks, rows out
+  for (int c = 0; c < kSolveChunks; ++c) {
+    int lo, hi;
+    rows(c, lo, hi);
+    MSCG_CUDA(cudaStreamWaitEvent(side[c], ev_mid, 0));
+    if (S) {
+      block_trisolve(*D, w, d_x, z1, side[c], nullptr, c);
+      ctx->launches++;
+    } else if (hi > lo) {
+      MSCG_CUDA(cudaMemcpyAsync(d_x + lo, z1 + lo, sizeof(double) * (hi - lo),
+                                cudaMemcpyDeviceToDevice, side[c]));
+    }
+    if (hi > lo)
+      MSCG_CUDA(cudaMemcpyAsync(x_h + lo, d_x + lo, sizeof(double) * (hi - lo),
+                                cudaMemcpyDeviceToHost, side[c]));
+    MSCG_CUDA(cudaEventRecord(ev_out[c], side[c]));
+  }
+  for (int c = 0; c < kSolveChunks; ++c) MSCG_CUDA(cudaStreamWaitEvent(s, ev_out[c], 0));
+}
+
 void Precond::apply(const double* y, double* x, cudaStream_t s, cudaEvent_t* ev) {
   if (shard.on) throw Error(1, "MscPreconditioner::apply: this is a shard (use apply_shard_*)");
   // ev (optional): 6 events bracketing the 5 stages (ev[0] before stage 0,

@@ -69,10 +69,12 @@ struct TriArgs {
   const int4* uitems;
   const int* perm;  // nullable (Schur blocks)
   const int* order; // launch order of the blocks
+  int pos0;          // first launch-order position of this launch
   int dim_max;
   long long* trace;  // debug: clock64 stamps for block 0, or null
   unsigned sleep_ns; // worker back-off while polling
-  int pf_items;      // far-data L2 prefetch distance in work items (0 = off)
+  int pf_items;      // far-data L2 prefetch distance in rounds of items, L pass (0 = off)
+  int pf_u;          // same, U pass
   int hint;          // L2 policy: 0 normal, 1 demand evict-first, 2 + prefetch evict-last
   int near_pf;       // L2 prefetch of the near tile after next (measured: no gain)
   int skip0;         // keep workers off the solver's SM sub-partition
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   __shared__ int done_l, done_u;
   __shared__ int cnt[kPartRing];  // far items published per ring tile
 
-  const int b = a.order[blockIdx.x];  // heaviest blocks first (LPT)
+  const int b = a.order[a.pos0 + blockIdx.x];  // heaviest blocks first (LPT)
   const int n = a.dim[b], r0 = a.row0[b];
   const int nt = (n + kTile - 1) / kTile;
   const double* lt = a.ltile + a.toff[b] * kTileElems;
@@ -519,15 +521,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (w < 0) w = nitems;
     const long long lit = a.lioff[b + 1] - a.lioff[b];
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
-    if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
+    if (lane < a.pf_u && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
       prefetch_far(fv, fc, d.z, d.w, ppol);
     }
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
-      if (lane == 0 && a.pf_items && it + kWorkers * a.pf_items < nitems) {
-        const int4 f = items[it + kWorkers * a.pf_items];
+      if (lane == 0 && a.pf_u && it + kWorkers * a.pf_u < nitems) {
+        const int4 f = items[it + kWorkers * a.pf_u];
         prefetch_far(fv, fc, f.z, f.w, ppol);
       }
       const int i = d.x, k = d.y & 0xff;
@@ -560,8 +562,11 @@ size_t trisolve_smem_bytes(int dim_max) {
 }
 
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const double* sub,
-                    cudaStream_t s, long long* trace) {
+                    cudaStream_t s, long long* trace, int chunk) {
   if (fs.nblocks == 0) return;
+  const int pos0 = chunk < 0 ? 0 : fs.h_chunk[chunk];
+  const int npos = chunk < 0 ? fs.nblocks : fs.h_chunk[chunk + 1] - pos0;
+  if (npos <= 0) return;
   TriArgs a;
   a.row0 = fs.row0.as<int>();
   a.dim = fs.dim.as<int>();
@@ -582,6 +587,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.uitems = fs.uitems.as<int4>();
   a.perm = fs.has_perm ? fs.perm.as<int>() : nullptr;
   a.order = fs.order.as<int>();
+  a.pos0 = pos0;
   a.dim_max = fs.max_dim;
   a.trace = trace;
   static const unsigned sleep_ns = [] {
@@ -594,6 +600,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? atoi(e) : 1;
   }();
   a.pf_items = pf_items;
+  static const int pf_u = [] {
+    const char* e = getenv("MSCG_TRI_PFU");
+    return e ? atoi(e) : 1;
+  }();
+  a.pf_u = pf_u;
   static const int hint = [] {
     const char* e = getenv("MSCG_TRI_HINT");
     return e ? atoi(e) : 0;
@@ -621,7 +632,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     if (smem > 48 * 1024)
       MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    kern<<<fs.nblocks, warps * 32, smem, s>>>(a, rhs, out, sub);
+    kern<<<npos, warps * 32, smem, s>>>(a, rhs, out, sub);
   };
   switch (variant) {
     case 1: launch(trisolve_kernel<16, 8, 2>, 16); break;   // 2 CTAs/SM, deeper loads
