@@ -72,7 +72,8 @@ struct TriArgs {
   int pos0;          // first launch-order position of this launch
   int dim_max;
   long long* trace;  // debug: clock64 stamps for block 0, or null
-  unsigned sleep_ns; // worker back-off while polling
+  unsigned sleep_ns; // worker back-off while polling: first sleep
+  unsigned sleep_max;  // and cap of the doubling
   int pf_items;      // far-data L2 prefetch distance in rounds of items, L pass (0 = off)
   int pf_u;          // same, U pass
   int hint;          // L2 policy: 0 normal, 1 demand evict-first, 2 + prefetch evict-last
@@ -192,7 +193,8 @@ template <int kUnroll>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
-                                          const int* done, int need, uint64_t pol) {
+                                          const int* done, int need, uint64_t pol,
+                                          unsigned ns_max) {
   double acc = 0.0, acc2 = 0.0;
   for (int base = s; base < e; base += 32 * kUnroll) {
     double v[kUnroll];
@@ -212,7 +214,9 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
       // every lane polls the same word: the loop exit is warp-uniform, so
       // the warp stays converged (divergent spins cost the shuffles below
       // their fast path)
-      while (vload(done) < need) __nanosleep(ns);
+      // exponential back-off: the solver finishes a tile every few
+      // microseconds and short polls would steal its issue slots
+      for (unsigned s = ns; vload(done) < need; s = min(2 * s, ns_max)) __nanosleep(s);
     }
     // Gather operands (independent shared loads); poll only if one is still
     // pending (the counter is a hint, the sentinel is the guarantee).
@@ -445,11 +449,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int t = i / kTile;
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l, d.y >> 8, dpol);
+      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l, d.y >> 8, dpol, a.sleep_max);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
         // ring slot of tile t is free once tile t - kPartRing was consumed
-        while (vload(&done_l) < t - (kPartRing - 1)) __nanosleep(a.sleep_ns);
+        for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPartRing - 1);
+             sl = min(2 * sl, a.sleep_max))
+          __nanosleep(sl);
         *reinterpret_cast<volatile double*>(part + (t % kPartRing) * kPartTile +
                                             (i % kTile) * kMaxSeg + k) = acc;
         atomicAdd(&cnt[t % kPartRing], 1);
@@ -537,10 +543,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int pos = nt - 1 - t;
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, x, lane, a.sleep_ns, &done_u, d.y >> 8, dpol);
+      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, x, lane, a.sleep_ns, &done_u, d.y >> 8, dpol, a.sleep_max);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
-        while (vload(&done_u) < pos - (kPartRing - 1)) __nanosleep(a.sleep_ns);
+        for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPartRing - 1);
+             sl = min(2 * sl, a.sleep_max))
+          __nanosleep(sl);
         *reinterpret_cast<volatile double*>(part + (t % kPartRing) * kPartTile +
                                             (i % kTile) * kMaxSeg + k) = acc;
         atomicAdd(&cnt[t % kPartRing], 1);
@@ -595,6 +603,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? static_cast<unsigned>(atoi(e)) : 32u;
   }();
   a.sleep_ns = sleep_ns;
+  static const unsigned sleep_max = [] {
+    const char* e = getenv("MSCG_TRI_SLEEP_MAX");
+    return e ? static_cast<unsigned>(atoi(e)) : 512u;
+  }();
+  a.sleep_max = sleep_max < sleep_ns ? sleep_ns : sleep_max;
   static const int pf_items = [] {
     const char* e = getenv("MSCG_TRI_PF");
     return e ? atoi(e) : 1;
