@@ -42,11 +42,10 @@ namespace mscg {
 
 namespace {
 
-constexpr int kRing = 2;               // TMA ring depth (near tiles + scalars)
-constexpr int kPartRing = 8;           // far-sum ring depth (tiles)
+constexpr int kRing = 2;               // TMA ring depth (near tiles + rhs slice)
 constexpr int kPartTile = kTile * kMaxSeg;
-constexpr int kVecElems = 40;          // rhs / subtrahend slice: 32 + alignment slack
-constexpr int kSlotElems = kTileElems + 2 * kVecElems;
+constexpr int kVecElems = 40;          // rhs slice: 32 + alignment slack
+constexpr int kSlotElems = kTileElems + kVecElems;
 constexpr unsigned kTileBytes = kTileElems * sizeof(double);
 
 struct TriArgs {
@@ -57,8 +56,6 @@ struct TriArgs {
   const long long* toff;
   const long long* lioff;
   const long long* uioff;
-  const int* lrp;
-  const int* urp;
   const double* lval;
   const uint16_t* lcol;
   const double* uval;
@@ -76,9 +73,6 @@ struct TriArgs {
   unsigned sleep_max;  // and cap of the doubling
   int pf_items;      // far-data L2 prefetch distance in rounds of items, L pass (0 = off)
   int pf_u;          // same, U pass
-  int hint;          // L2 policy: 0 normal, 1 demand evict-first, 2 + prefetch evict-last
-  int near_pf;       // L2 prefetch of the near tile after next (measured: no gain)
-  int skip0;         // keep workers off the solver's SM sub-partition
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -116,49 +110,15 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// L2 eviction policies (createpolicy) for the far-entry stream: demand loads
-// mark consumed lines evict-first so that lines prefetched for upcoming items
-// survive until they are read.
-__device__ __forceinline__ uint64_t make_policy(int kind) {
-  uint64_t p;
-  if (kind == 2)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  else if (kind == 1)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double ld_far(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int ld_col(const uint16_t* p, uint64_t pol) {
-  unsigned short v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
-               : "=h"(v)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void l2_prefetch_hint(const void* p, unsigned bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p),
-               "r"(bytes), "l"(pol)
-               : "memory");
-}
-
 // L2 prefetch of far entries [s, e) (values + columns), widened to 16 B.
-__device__ __forceinline__ void prefetch_far(const double* v, const uint16_t* c, int s, int e,
-                                             uint64_t pol) {
+__device__ __forceinline__ void prefetch_far(const double* v, const uint16_t* c, int s, int e) {
   if (e <= s) return;
   const unsigned long long v0 = reinterpret_cast<unsigned long long>(v + s) & ~15ull;
   const unsigned long long v1 = (reinterpret_cast<unsigned long long>(v + e) + 15) & ~15ull;
   const unsigned long long c0 = reinterpret_cast<unsigned long long>(c + s) & ~15ull;
   const unsigned long long c1 = (reinterpret_cast<unsigned long long>(c + e) + 15) & ~15ull;
-  l2_prefetch_hint(reinterpret_cast<const void*>(v0), static_cast<unsigned>(v1 - v0), pol);
-  l2_prefetch_hint(reinterpret_cast<const void*>(c0), static_cast<unsigned>(c1 - c0), pol);
+  l2_prefetch(reinterpret_cast<const void*>(v0), static_cast<unsigned>(v1 - v0));
+  l2_prefetch(reinterpret_cast<const void*>(c0), static_cast<unsigned>(c1 - c0));
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -168,6 +128,20 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+// Pass counter read: acquire when the solution is overwritten in place (the
+// U pass reuses z's slots, so a value's presence cannot mark readiness).
+template <bool kAcquire>
+__device__ __forceinline__ int poll(const int* p) {
+  return kAcquire ? ld_acquire(p) : vload(p);
+}
 
 // A vector slice [p, p + 32) copied by TMA needs 16-byte aligned ends:
 // copy the enclosing aligned range and remember the offset (0 or 1).
@@ -189,12 +163,11 @@ __device__ __forceinline__ Slice aligned_slice(const double* p, int len) {
 // instead of per-lane loop bounds) so the final reduction runs converged.
 // The first round's loads are issued before the readiness wait (one poll
 // per warp on the tile counter).
-template <int kUnroll>
+template <int kUnroll, bool kInPlace>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
-                                          const int* done, int need, uint64_t pol,
-                                          unsigned ns_max) {
+                                          const int* done, int need, unsigned ns_max) {
   double acc = 0.0, acc2 = 0.0;
   for (int base = s; base < e; base += 32 * kUnroll) {
     double v[kUnroll];
@@ -203,8 +176,8 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
     for (int u = 0; u < kUnroll; ++u) {
       const int k = base + lane + 32 * u;
       if (k < e) {
-        v[u] = ld_far(vals + k, pol);
-        c[u] = ld_col(cols + k, pol);
+        v[u] = __ldg(vals + k);
+        c[u] = __ldg(cols + k);
       } else {
         v[u] = 0.0;
         c[u] = -1;
@@ -216,7 +189,7 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
       // their fast path)
       // exponential back-off: the solver finishes a tile every few
       // microseconds and short polls would steal its issue slots
-      for (unsigned s = ns; vload(done) < need; s = min(2 * s, ns_max)) __nanosleep(s);
+      for (unsigned s = ns; poll<kInPlace>(done) < need; s = min(2 * s, ns_max)) __nanosleep(s);
     }
     // Gather operands (independent shared loads); poll only if one is still
     // pending (the counter is a hint, the sentinel is the guarantee).
@@ -228,7 +201,7 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
       xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
       pending |= is_pending(xv[u]);
     }
-    while (__any_sync(0xffffffffu, pending)) {
+    while (!kInPlace && __any_sync(0xffffffffu, pending)) {
       __nanosleep(ns);
       pending = false;
 #pragma unroll
@@ -302,22 +275,24 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
   return static_cast<int>(__double_as_longlong(T[idx]));
 }
 
-template <int kWarps, int kUnroll, int kMinBlocks>
+// kPR: depth (tiles) of the far-sum ring.  kInPlace: x overwrites z slot by
+// slot (one solution vector in shared memory instead of two).  kProducer:
+// warp 1 issues the near-tile copies (the solver's issue of a bulk copy costs
+// ~400 cycles of its chain per tile) and warps 2.. are the workers.
+template <int kWarps, int kUnroll, int kMinBlocks, int kPR, bool kInPlace, bool kProducer>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
-  // Workers: warps 1..kWarps-1, or (skip0) only warps off the solver's SM
-  // sub-partition (warp % 4 != 0) so the chain does not share issue slots.
-  const bool skip0 = a.skip0 != 0;
-  const int kWorkers = skip0 ? kWarps - 1 - (kWarps - 1) / 4 : kWarps - 1;
+  constexpr int kFirstWorker = kProducer ? 2 : 1;
+  constexpr int kWorkers = kWarps - kFirstWorker;
   extern __shared__ __align__(128) double sm[];
-  double* ring = sm;                          // kRing slots: tile | meta | rhs | sub
-  double* part = ring + kRing * kSlotElems;   // [kPartRing][32 rows][kMaxSeg]
-  double* z = part + kPartRing * kPartTile;   // dim_max (L output)
-  double* x = z + ((a.dim_max + kTile - 1) & ~(kTile - 1));  // U output
+  double* ring = sm;                        // kRing slots: tile | meta | rhs slice
+  double* part = ring + kRing * kSlotElems; // [kPR][32 rows][kMaxSeg]
+  double* z = part + kPR * kPartTile;       // L output
+  double* x = kInPlace ? z : z + ((a.dim_max + kTile - 1) & ~(kTile - 1));  // U output
   __shared__ __align__(8) uint64_t bars[kRing];
   __shared__ int done_l, done_u;
-  __shared__ int cnt[kPartRing];  // far items published per ring tile
+  __shared__ int cnt[kPR];    // far items published per ring tile
 
   const int b = a.order[a.pos0 + blockIdx.x];  // heaviest blocks first (LPT)
   const int n = a.dim[b], r0 = a.row0[b];
@@ -326,26 +301,24 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const double* ut = a.utile + a.toff[b] * kTileElems;
   const double pend = pending_value();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t dpol = make_policy(a.hint >= 1 ? 1 : 0);
-  const uint64_t ppol = make_policy(a.hint >= 2 ? 2 : 0);
 
   for (int i = threadIdx.x; i < nt * kTile; i += blockDim.x) {
     // rows past the block's end read as zero by the neighbour products
     z[i] = i < n ? pend : 0.0;
-    x[i] = i < n ? pend : 0.0;
+    if (!kInPlace) x[i] = i < n ? pend : 0.0;
   }
-  for (int i = threadIdx.x; i < kPartRing * kPartTile; i += blockDim.x) part[i] = pend;
+  for (int i = threadIdx.x; i < kPR * kPartTile; i += blockDim.x) part[i] = pend;
   if (threadIdx.x == 0) {
     done_l = 0;
     done_u = 0;
-    for (int r = 0; r < kPartRing; ++r) cnt[r] = 0;
+    for (int r = 0; r < kPR; ++r) cnt[r] = 0;
     for (int r = 0; r < kRing; ++r) mbar_init(&bars[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  // Stream item q: q < nt -> L tile q (+ rhs slice), else U tile 2nt-1-q
-  // (+ subtrahend slice).  Item q lives in slot q % kRing, phase (q/kRing)&1.
+  // Near item q: q < nt -> L tile q (+ rhs slice), else U tile 2nt-1-q.
+  // Item q lives in slot q % kRing, phase (q / kRing) & 1.
   const int* pm = a.perm ? a.perm + r0 : nullptr;
   auto issue = [&](int q) {  // solver lane 0
     const int slot = q % kRing;
@@ -353,26 +326,32 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const bool lpass = q < nt;
     const int t = lpass ? q : 2 * nt - 1 - q;
     const double* tile = (lpass ? lt : ut) + static_cast<long long>(t) * kTileElems;
-    unsigned bytes = kTileBytes;
     Slice sr{nullptr, 0, 0};
-    const int len = min(kTile, n - t * kTile);
-    if (lpass && !pm) sr = aligned_slice(rhs + r0 + t * kTile, len);
-    if (!lpass && sub) sr = aligned_slice(sub + r0 + t * kTile, len);
-    bytes += sr.bytes;
-    mbar_expect_tx(&bars[slot], bytes);
+    if (lpass && !pm) sr = aligned_slice(rhs + r0 + t * kTile, min(kTile, n - t * kTile));
+    mbar_expect_tx(&bars[slot], kTileBytes + sr.bytes);
     bulk_load(dst, tile, kTileBytes, &bars[slot]);
     if (sr.bytes) bulk_load(dst + kTileElems, sr.src, sr.bytes, &bars[slot]);
-    return sr.off;
   };
-  // Slice offsets of the items in flight (written by solver lane 0).
-  __shared__ int soff[kRing];
+  // Producer: issue near items [q0, q1) as their slots free up (item q
+  // reuses the slot of item q - kRing, consumed once the solver published
+  // the matching pass counter).
+  auto produce = [&](int q0, int q1) {
+    for (int q = q0; q < q1; ++q) {
+      const int prev = q - kRing;  // item whose slot q reuses
+      const int* ctr = prev < nt ? &done_l : &done_u;
+      const int need = prev < nt ? prev + 1 : prev - nt + 1;
+      for (unsigned sl = 16; vload(ctr) < need; sl = min(2 * sl, 256u)) __nanosleep(sl);
+      if (lane == 0) issue(q);
+      __syncwarp();
+    }
+  };
   long long* tr = (a.trace && b == 0) ? a.trace : nullptr;
   const int j = lane;
 
   // ================================================================ L pass
   if (warp == 0) {
     if (lane == 0) {
-      for (int q = 0; q < kRing && q < 2 * nt; ++q) soff[q] = issue(q);
+      for (int q = 0; q < kRing && q < 2 * nt; ++q) issue(q);
       // the block's work-item lists go to L2 once
       l2_prefetch(reinterpret_cast<const void*>(reinterpret_cast<unsigned long long>(
                       a.litems + a.lioff[b]) & ~15ull),
@@ -383,21 +362,20 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int i = t * kTile + j;
       const bool valid = i < n;
       const int slot = t % kRing;
-      const int off = *reinterpret_cast<volatile int*>(&soff[slot]);
       // Schur blocks (row_perm): gather the right-hand side directly.
       double bperm = 0.0;
       if (pm && valid) bperm = rhs[r0 + pm[i]];
       mbar_wait(&bars[slot], (t / kRing) & 1);
       if (tr && lane == 0) tr[4 * t + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
+      const int off = static_cast<int>((reinterpret_cast<unsigned long long>(rhs + r0 + t * kTile) & 15) >> 3);
       const double bi = valid ? (pm ? bperm : T[kTileElems + off + j]) : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       double nb = 0.0;
       if (t > 1) nb += neighbour(T, 0, j, z + (t - 2) * kTile);
       if (t > 0) nb += neighbour(T, kTile, j, z + (t - 1) * kTile);
-      double far = 0.0;
-      wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
-      far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
+      wait_items(&cnt[t % kPR], __reduce_add_sync(0xffffffffu, nseg), lane);
+      const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 1] = clock64();
       // acc = b_i - (known sums); z_k = acc_k once step k is reached
@@ -415,50 +393,47 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&done_l) = t + 1;
         if (tr) tr[4 * t + 2] = clock64();
-        if (t + kRing < 2 * nt) soff[slot] = issue(t + kRing);
-        if (a.near_pf && t + kRing + 1 < 2 * nt) {
-          const int q = t + kRing + 1;
-          const int tt = q < nt ? q : 2 * nt - 1 - q;
-          l2_prefetch((q < nt ? lt : ut) + static_cast<long long>(tt) * kTileElems, kTileBytes);
-        }
+        if (!kProducer && t + kRing < 2 * nt) issue(t + kRing);
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 3] = clock64();
     }
+  } else if (kProducer && warp == 1) {
+    produce(kRing, min(nt + kRing, 2 * nt));
   } else {
     // workers: far items of L rows, rows ascending
-    int w = skip0 ? ((warp & 3) ? warp - 1 - (warp >> 2) : -1) : warp - 1;
+    const int w = warp - kFirstWorker;
     const double* fv = a.lval + a.loff[b];
     const uint16_t* fc = a.lcol + a.loff[b];
     const int4* items = a.litems + a.lioff[b];
     const int nitems = static_cast<int>(a.lioff[b + 1] - a.lioff[b]);
-    if (w < 0) w = nitems;  // idle warp on the solver's sub-partition
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
-      prefetch_far(fv, fc, d.z, d.w, ppol);
+      prefetch_far(fv, fc, d.z, d.w);
     }
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
       if (lane == 0 && a.pf_items && it + kWorkers * a.pf_items < nitems) {
         const int4 f = items[it + kWorkers * a.pf_items];
-        prefetch_far(fv, fc, f.z, f.w, ppol);
+        prefetch_far(fv, fc, f.z, f.w);
       }
       const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l, d.y >> 8, dpol, a.sleep_max);
+      const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l,
+                                                 d.y >> 8, a.sleep_max);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
-        // ring slot of tile t is free once tile t - kPartRing was consumed
-        for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPartRing - 1);
+        // ring slot of tile t is free once tile t - kPR was consumed
+        for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPR - 1);
              sl = min(2 * sl, a.sleep_max))
           __nanosleep(sl);
-        *reinterpret_cast<volatile double*>(part + (t % kPartRing) * kPartTile +
+        *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
                                             (i % kTile) * kMaxSeg + k) = acc;
-        atomicAdd(&cnt[t % kPartRing], 1);
+        atomicAdd(&cnt[t % kPR], 1);
         if (rt) {
           rt[2] = clock64();
           rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | k;
@@ -476,20 +451,17 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int i = t * kTile + j;
       const bool valid = i < n;
       const int slot = q % kRing;
-      const int off = *reinterpret_cast<volatile int*>(&soff[slot]);
       const double zi = valid ? z[i] : 0.0;
       mbar_wait(&bars[slot], (q / kRing) & 1);
       if (tr && lane == 0) tr[4 * q + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
       const double rd = valid ? T[kMetaDiag + j] : 0.0;
-      const double si = (valid && sub) ? T[kTileElems + off + j] : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       double nb = 0.0;
       if (tt > 0) nb += neighbour(T, 0, j, x + (t + 1) * kTile);
       if (tt > 1) nb += neighbour(T, kTile, j, x + (t + 2) * kTile);
-      double far = 0.0;
-      wait_items(&cnt[t % kPartRing], __reduce_add_sync(0xffffffffu, nseg), lane);
-      far = take_far(part + (t % kPartRing) * kPartTile + j * kMaxSeg, nseg, pend);
+      wait_items(&cnt[t % kPR], __reduce_add_sync(0xffffffffu, nseg), lane);
+      const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 1] = clock64();
       double acc = zi - (nb + far);
@@ -501,57 +473,56 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         if (j < k) acc = fma(-T[kTriOff + tri_u(j, k)], xk, acc);
       }
       if (!valid) xj = 0.0;
-      if (valid) {
-        *reinterpret_cast<volatile double*>(x + i) = xj;
-        out[r0 + i] = sub ? si - xj : xj;
-      }
+      if (valid) *reinterpret_cast<volatile double*>(x + i) = xj;
       __syncwarp();
       if (lane == 0) {
-        *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
+        if (kInPlace)
+          st_release(&done_u, tt + 1);
+        else
+          *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
         if (tr) tr[4 * q + 2] = clock64();
-        if (q + kRing < 2 * nt) soff[slot] = issue(q + kRing);
-        if (a.near_pf && q + kRing + 1 < 2 * nt)
-          l2_prefetch(ut + static_cast<long long>(2 * nt - 1 - (q + kRing + 1)) * kTileElems,
-                      kTileBytes);
+        if (!kProducer && q + kRing < 2 * nt) issue(q + kRing);
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 3] = clock64();
     }
+  } else if (kProducer && warp == 1) {
+    produce(nt + kRing, 2 * nt);
   } else {
     // workers: far items of U rows, rows descending
-    int w = skip0 ? ((warp & 3) ? warp - 1 - (warp >> 2) : -1) : warp - 1;
+    const int w = warp - kFirstWorker;
     const double* fv = a.uval + a.uoff[b];
     const uint16_t* fc = a.ucol + a.uoff[b];
     const int4* items = a.uitems + a.uioff[b];
     const int nitems = static_cast<int>(a.uioff[b + 1] - a.uioff[b]);
-    if (w < 0) w = nitems;
     const long long lit = a.lioff[b + 1] - a.lioff[b];
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_u && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
-      prefetch_far(fv, fc, d.z, d.w, ppol);
+      prefetch_far(fv, fc, d.z, d.w);
     }
     for (int it = w; it < nitems; it += kWorkers) {
       const int4 d = nxt;
       if (it + kWorkers < nitems) nxt = items[it + kWorkers];
       if (lane == 0 && a.pf_u && it + kWorkers * a.pf_u < nitems) {
         const int4 f = items[it + kWorkers * a.pf_u];
-        prefetch_far(fv, fc, f.z, f.w, ppol);
+        prefetch_far(fv, fc, f.z, f.w);
       }
       const int i = d.x, k = d.y & 0xff;
       const int t = i / kTile;
       const int pos = nt - 1 - t;
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll>(fv, fc, d.z, d.w, x, lane, a.sleep_ns, &done_u, d.y >> 8, dpol, a.sleep_max);
+      const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, x, lane, a.sleep_ns,
+                                                    &done_u, d.y >> 8, a.sleep_max);
       if (rt) rt[1] = clock64();
       if (lane == 0) {
-        for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPartRing - 1);
+        for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPR - 1);
              sl = min(2 * sl, a.sleep_max))
           __nanosleep(sl);
-        *reinterpret_cast<volatile double*>(part + (t % kPartRing) * kPartTile +
+        *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
                                             (i % kTile) * kMaxSeg + k) = acc;
-        atomicAdd(&cnt[t % kPartRing], 1);
+        atomicAdd(&cnt[t % kPR], 1);
         if (rt) {
           rt[2] = clock64();
           rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | k;
@@ -559,15 +530,20 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       }
     }
   }
+  __syncthreads();
+  // epilogue: the block's solution leaves in one coalesced sweep
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    out[r0 + i] = sub ? sub[r0 + i] - x[i] : x[i];
+}
+
+template <int kPR, bool kInPlace>
+size_t smem_bytes(int dim_max) {
+  const size_t dpad = (static_cast<size_t>(dim_max) + kTile - 1) & ~static_cast<size_t>(kTile - 1);
+  return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
+                           static_cast<size_t>(kPR) * kPartTile + (kInPlace ? 1 : 2) * dpad);
 }
 
 }  // namespace
-
-size_t trisolve_smem_bytes(int dim_max) {
-  return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
-                           static_cast<size_t>(kPartRing) * kPartTile +
-                           2 * static_cast<size_t>((dim_max + kTile - 1) & ~(kTile - 1)));
-}
 
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const double* sub,
                     cudaStream_t s, long long* trace, int chunk) {
@@ -583,8 +559,6 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.toff = fs.toff.as<long long>();
   a.lioff = fs.lioff.as<long long>();
   a.uioff = fs.uioff.as<long long>();
-  a.lrp = fs.lrp.as<int>();
-  a.urp = fs.urp.as<int>();
   a.lval = fs.lval.as<double>();
   a.lcol = fs.lcol.as<uint16_t>();
   a.uval = fs.uval.as<double>();
@@ -618,39 +592,33 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? atoi(e) : 1;
   }();
   a.pf_u = pf_u;
-  static const int hint = [] {
-    const char* e = getenv("MSCG_TRI_HINT");
-    return e ? atoi(e) : 0;
-  }();
-  a.hint = hint;
-  static const int near_pf = [] {
-    const char* e = getenv("MSCG_TRI_NEARPF");
-    return e ? atoi(e) : 0;
-  }();
-  a.near_pf = near_pf;
-  static const int skip0 = [] {
-    const char* e = getenv("MSCG_TRI_SKIP0");
-    return e ? atoi(e) : 0;
-  }();
-  a.skip0 = skip0;
-  const size_t smem = trisolve_smem_bytes(fs.max_dim);
-  if (smem > 227 * 1024)
-    throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
-                       " rows exceeds the shared-memory solution vectors");
   static const int variant = [] {
     const char* e = getenv("MSCG_TRI_VARIANT");
     return e ? atoi(e) : 0;
   }();
-  auto launch = [&](auto kern, int warps) {
+  auto launch = [&](auto kern, int warps, size_t smem) {
+    if (smem > 227 * 1024)
+      throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
+                         " rows exceeds the shared-memory solution vector");
     if (smem > 48 * 1024)
       MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
     kern<<<npos, warps * 32, smem, s>>>(a, rhs, out, sub);
   };
+  const int d = fs.max_dim;
   switch (variant) {
-    case 1: launch(trisolve_kernel<16, 8, 2>, 16); break;   // 2 CTAs/SM, deeper loads
-    case 2: launch(trisolve_kernel<16, 16, 1>, 16); break;  // 1 CTA/SM, 128 registers
-    default: launch(trisolve_kernel<16, 4, 2>, 16); break;  // 2 CTAs/SM (64 registers)
+    case 1:  // 3 CTAs/SM: 12 warps, 4-tile sum ring (cfg4 3.19 ms, cfg5 9.30 ms)
+      launch(trisolve_kernel<12, 4, 3, 4, true, false>, 12, smem_bytes<4, true>(d));
+      break;
+    case 2:  // producer warp issues the near tiles, 14 workers (cfg4 2.93, cfg5 9.54)
+      launch(trisolve_kernel<16, 4, 2, 8, true, true>, 16, smem_bytes<8, true>(d));
+      break;
+    case 3:  // separate z and x vectors (cfg4 2.78, cfg5 9.35)
+      launch(trisolve_kernel<16, 4, 2, 8, false, false>, 16, smem_bytes<8, false>(d));
+      break;
+    default:  // 2 CTAs/SM (64 registers), x overwrites z in place (cfg4 2.68, cfg5 9.25)
+      launch(trisolve_kernel<16, 4, 2, 8, true, false>, 16, smem_bytes<8, true>(d));
+      break;
   }
   MSCG_CUDA(cudaGetLastError());
 }
