@@ -13,13 +13,13 @@
 //    needs — the near window (the two neighbour tiles dense, 32 x 64 fp64
 //    column-major, and the strictly triangular part of the diagonal tile
 //    packed by column), the per-row metadata (1/U_jj, number of far work
-//    items) and the tile's slice of the right-hand side / subtrahend —
+//    items) and, in the L pass, the tile's slice of the right-hand side —
 //    arrives in shared memory by TMA bulk copies (cp.async.bulk + mbarrier,
-//    double-buffered).  The solver therefore issues no global loads at all:
-//    measured, a solver load queued behind the workers' streaming requests
-//    stalled the chain for ~30K cycles per tile.  Lane j owns row j,
-//    neighbour tiles are applied from registers through shuffles, and the
-//    32-step diagonal chain costs one shuffle + one FMA per row;
+//    double-buffered).  The solver issues no global loads: a load queued
+//    behind the workers' streaming requests stalled the chain for ~30K
+//    cycles per tile.  Lane j owns row j; the neighbour tiles are applied
+//    with broadcast shared loads of their solution, then the 32-step
+//    diagonal chain costs one shuffle + one FMA per row;
 //  * workers (warps 1-15) stream the far entries (L: columns < 32(t-2), U:
 //    columns >= 32(t+3)) from HBM.  Each row's far entries are cut into work
 //    items of kSeg = 512 entries, listed per block at setup in the order the
@@ -27,10 +27,15 @@
 //    published first; a worker issues an item's loads, sleeps until its
 //    inputs are final, and publishes one partial sum per item into a
 //    shared-memory ring that the solver sums in a fixed order (deterministic);
-//  * z (L output) and x (U output) live in shared memory.  Readiness is the
-//    value itself: slots start as a signalling-NaN pattern no arithmetic
-//    produces and an aligned 8-byte shared store is single-copy atomic, so
-//    neither flags nor fences sit on the chain.
+//  * the solution lives in shared memory, x overwriting z slot by slot (the
+//    U pass reads z of a tile just before writing its x; workers read x only
+//    of tiles already solved).  In the L pass readiness is the value itself:
+//    slots start as a signalling-NaN pattern no arithmetic produces and an
+//    aligned 8-byte shared store is single-copy atomic; the U pass counter
+//    is published with release/acquire.  Every wait is warp-uniform (all
+//    lanes poll the same word): a divergent spin sends the next shuffles to
+//    their slow collective path.  The result leaves in one coalesced
+//    epilogue.
 // Rounding differs from the reference's sequential row sums by ~1e-16
 // relative, far inside the 1e-10 apply bar.
 #include <cstdlib>
