@@ -507,33 +507,66 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
     double* __restrict__ lval, uint16_t* __restrict__ lcol, double* __restrict__ uval,
     uint16_t* __restrict__ ucol, double* __restrict__ ltile, double* __restrict__ utile,
     double* __restrict__ urdiag, const long long* __restrict__ lioff,
-    const long long* __restrict__ uioff, int4* __restrict__ litems, int4* __restrict__ uitems) {
+    const long long* __restrict__ uioff, int4* __restrict__ litems, int4* __restrict__ uitems,
+    int* __restrict__ lnum, int* __restrict__ unum) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   int* lr = lrp + r0 + b;
   int* ur = urp + r0 + b;
   if (threadIdx.x == 0) {
     int sl = 0, su = 0;
-    // Work items {row, segment, begin, end} (entry offsets within the block).
-    auto emit = [](int4*& out, int i, int s, int cnt) {
-      const int ns = far_segments(cnt);
-      for (int k = 0; k < ns; ++k) {
-        const int b0 = s + k * kSeg;
-        *out++ = make_int4(i, k, b0, k == ns - 1 ? s + cnt : b0 + kSeg);
-      }
-    };
-    int4* li = litems + lioff[b];
     for (int i = 0; i < n; ++i) {
       lr[i] = sl;
       ur[i] = su;
-      emit(li, i, sl, lcnt[r0 + i]);
       sl += lcnt[r0 + i];
       su += ucnt[r0 + i];
     }
     lr[n] = sl;
     ur[n] = su;
-    int4* ui = uitems + uioff[b];
-    for (int i = n - 1; i >= 0; --i) emit(ui, i, ur[i], ucnt[r0 + i]);
+    // Work items in solve order (entry offsets within the block).  Long rows:
+    // {row, segment, begin, end}, kSeg entries per segment.  Runs of short
+    // rows of one tile: one multi-row item (see kShortRow).
+    auto build = [&](int4* out, const int* rp, const int* cnt, bool asc) {
+      int4* o = out;
+      int g0 = -1, g1 = -1, gent = 0;  // open group: rows [g0, g1], entries
+      auto close = [&]() {
+        if (g0 < 0) return;
+        if (g0 == g1)
+          *o++ = make_int4(g0, 0, rp[g0], rp[g0 + 1]);
+        else
+          *o++ = make_int4(g0, kMultiFlag | (g1 - g0), rp[g0], rp[g1 + 1]);
+        g0 = g1 = -1;
+        gent = 0;
+      };
+      for (int k = 0; k < n; ++k) {
+        const int i = asc ? k : n - 1 - k;
+        const int c = cnt[r0 + i];
+        if (c == 0) continue;
+        if (c <= kShortRow) {
+          const int lo = g0 < 0 ? i : min(g0, i), hi = g0 < 0 ? i : max(g1, i);
+          if (g0 >= 0 && ((i >> 5) != (g0 >> 5) || gent + c > kGroupEntries || hi - lo >= 32))
+            close();
+          if (g0 < 0) {
+            g0 = g1 = i;
+          } else {
+            g0 = min(g0, i);
+            g1 = max(g1, i);
+          }
+          gent += c;
+          continue;
+        }
+        close();
+        const int ns = far_segments(c);
+        for (int q = 0; q < ns; ++q) {
+          const int b0 = rp[i] + q * kSeg;
+          *o++ = make_int4(i, q, b0, q == ns - 1 ? rp[i] + c : b0 + kSeg);
+        }
+      }
+      close();
+      return static_cast<int>(o - out);
+    };
+    lnum[b] = build(litems + lioff[b], lr, lcnt, true);
+    unum[b] = build(uitems + uioff[b], ur, ucnt, false);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -603,15 +636,21 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   // are all final.  L: highest column's tile + 1; U: tiles above the lowest.
   __syncthreads();
   const int nt = (n + kTile - 1) / kTile;
-  for (long long q = lioff[b] + threadIdx.x; q < lioff[b + 1]; q += blockDim.x) {
+  for (long long q = lioff[b] + threadIdx.x; q < lioff[b] + lnum[b]; q += blockDim.x) {
     int4 d = litems[q];
-    const int c = lcol[lb + d.w - 1];
+    int c = lcol[lb + d.w - 1];
+    if (d.y & kMultiFlag)  // highest column over the group's rows
+      for (int i = d.x; i <= d.x + (d.y & 0x7f); ++i)
+        if (lr[i + 1] > lr[i]) c = max(c, static_cast<int>(lcol[lb + lr[i + 1] - 1]));
     d.y = (d.y & 0xff) | (((c >> 5) + 1) << 8);
     litems[q] = d;
   }
-  for (long long q = uioff[b] + threadIdx.x; q < uioff[b + 1]; q += blockDim.x) {
+  for (long long q = uioff[b] + threadIdx.x; q < uioff[b] + unum[b]; q += blockDim.x) {
     int4 d = uitems[q];
-    const int c = ucol[ub + d.z];
+    int c = ucol[ub + d.z];
+    if (d.y & kMultiFlag)  // lowest column over the group's rows
+      for (int i = d.x; i <= d.x + (d.y & 0x7f); ++i)
+        if (ur[i + 1] > ur[i]) c = min(c, static_cast<int>(ucol[ub + ur[i]]));
     d.y = (d.y & 0xff) | ((nt - (c >> 5)) << 8);
     uitems[q] = d;
   }
@@ -863,6 +902,8 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   }
   fs->litems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_lioff[nb]));
   fs->uitems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_uioff[nb]));
+  fs->lnum = DevBuf(sizeof(int) * std::max(1, nb));
+  fs->unum = DevBuf(sizeof(int) * std::max(1, nb));
   fs->lrp = DevBuf(sizeof(int) * (total + nb));
   fs->urp = DevBuf(sizeof(int) * (total + nb));
   fs->lval = DevBuf(sizeof(double) * std::max<long long>(1, fs->far_l()));
@@ -881,7 +922,8 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
       fs->lrp.as<int>(), fs->urp.as<int>(), fs->lval.as<double>(), fs->lcol.as<uint16_t>(),
       fs->uval.as<double>(), fs->ucol.as<uint16_t>(), fs->ltile.as<double>(),
       fs->utile.as<double>(), fs->urdiag.as<double>(), fs->lioff.as<long long>(),
-      fs->uioff.as<long long>(), fs->litems.as<int4>(), fs->uitems.as<int4>());
+      fs->uioff.as<long long>(), fs->litems.as<int4>(), fs->uitems.as<int4>(),
+      fs->lnum.as<int>(), fs->unum.as<int>());
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
   MSCG_CUDA(cudaStreamSynchronize(s));

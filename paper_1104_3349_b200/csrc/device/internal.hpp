@@ -96,6 +96,14 @@ constexpr int kTileElems = kNearElems + 2 * kTile;
 // and pass (L: rows ascending, U: rows descending) hold int4 {row, seg,
 // begin, end} (far-entry offsets within the block).
 constexpr int kSolveChunks = 4;
+// Rows of one tile whose far lists are short (<= kShortRow entries) are
+// grouped into one work item of at most kGroupEntries entries: a warp loads
+// them in one round and sums each row in shared memory (one memory round trip
+// for the group instead of one per row).  Item encoding: y = need << 8 |
+// kMultiFlag | (rows - 1), x = first row (ascending), [z, w) = entries.
+constexpr int kShortRow = 96;
+constexpr int kGroupEntries = 128;
+constexpr int kMultiFlag = 0x80;
 constexpr int kSeg = 512;
 constexpr int kMaxSeg = 4;
 __host__ __device__ inline int far_segments(int nfar) {
@@ -120,7 +128,8 @@ struct FactorSet {
   DevBuf lcol, ucol;                       // uint16
   DevBuf ltile, utile;                     // fp64 [tiles][kTileElems]
   std::vector<int64_t> h_lioff, h_uioff;   // per block far work-item offsets (+1)
-  DevBuf lioff, uioff;                     // int64[nblocks+1]
+  DevBuf lioff, uioff;                     // int64[nblocks+1] (capacity)
+  DevBuf lnum, unum;                       // int32[nblocks] items in use
   DevBuf litems, uitems;                   // int32 (row << 3 | seg)
   DevBuf udiag, urdiag;                    // fp64[total_rows]
   DevBuf perm;                             // int32[total_rows] (local), if has_perm

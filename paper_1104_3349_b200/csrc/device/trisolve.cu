@@ -69,6 +69,10 @@ struct TriArgs {
   const double* utile;
   const int4* litems;  // {row, segment | need << 8, begin, end}
   const int4* uitems;
+  const int* lnum;     // items per block
+  const int* unum;
+  const int* lrp;      // far-entry row offsets, row0[b] + b + i
+  const int* urp;
   const int* perm;  // nullable (Schur blocks)
   const int* order; // launch order of the blocks
   int pos0;          // first launch-order position of this launch
@@ -224,6 +228,56 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
   return warp_sum(acc + acc2);
 }
 
+// A multi-row item: rows [row0, row0 + span) of one tile, entries [s, e)
+// (at most 32 * kUnroll).  One round of loads for all rows; each product goes
+// to the warp's shared scratch and lane r sums row r's run in entry order.
+// Returns lane r's row sum (and whether row r has entries).
+template <int kUnroll, bool kInPlace>
+__device__ __noinline__ double group_dot(const double* __restrict__ vals,
+                                            const uint16_t* __restrict__ cols, int s, int e,
+                                            const int* rp, int row0, int span,
+                                            const double* sol, double* scratch, int lane,
+                                            unsigned ns, const int* done, int need,
+                                            unsigned ns_max, bool& has) {
+  double v[kUnroll];
+  int c[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const int k = s + lane + 32 * u;
+    v[u] = k < e ? __ldg(vals + k) : 0.0;
+    c[u] = k < e ? __ldg(cols + k) : -1;
+  }
+  const bool mine = lane < span;
+  const int rb = mine ? __ldg(rp + row0 + lane) : 0;
+  const int re = mine ? __ldg(rp + row0 + lane + 1) : 0;
+  for (unsigned sl = ns; poll<kInPlace>(done) < need; sl = min(2 * sl, ns_max)) __nanosleep(sl);
+  const volatile double* vs = sol;
+  double xv[kUnroll];
+  bool pending = false;
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
+    pending |= is_pending(xv[u]);
+  }
+  while (!kInPlace && __any_sync(0xffffffffu, pending)) {
+    __nanosleep(ns);
+    pending = false;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (c[u] >= 0 && is_pending(xv[u])) xv[u] = vs[c[u]];
+      pending |= is_pending(xv[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) scratch[lane + 32 * u] = v[u] * xv[u];
+  __syncwarp();
+  double acc = 0.0;
+  for (int k = rb; k < re; ++k) acc += scratch[k - s];
+  __syncwarp();  // scratch is reused by the warp's next item
+  has = re > rb;
+  return acc;
+}
+
 // sum_k T[(c0 + k) * 32 + j] * v[k] over one 32-column neighbour tile; v is
 // the neighbour tile's solution in shared memory, read as broadcast 16-byte
 // loads (measured: a shuffle costs 3x the issue slots of a broadcast load, and
@@ -294,7 +348,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   double* ring = sm;                        // kRing slots: tile | meta | rhs slice
   double* part = ring + kRing * kSlotElems; // [kPR][32 rows][kMaxSeg]
   double* z = part + kPR * kPartTile;       // L output
-  double* x = kInPlace ? z : z + ((a.dim_max + kTile - 1) & ~(kTile - 1));  // U output
+  const int dpad = (a.dim_max + kTile - 1) & ~(kTile - 1);
+  double* x = kInPlace ? z : z + dpad;      // U output
+  double* scratch = x + dpad;               // [workers][kGroupEntries]
+  static_assert(32 * kUnroll >= kGroupEntries, "a multi-row item is one round of loads");
   __shared__ __align__(8) uint64_t bars[kRing];
   __shared__ int done_l, done_u;
   __shared__ int cnt[kPR];    // far items published per ring tile
@@ -411,7 +468,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const double* fv = a.lval + a.loff[b];
     const uint16_t* fc = a.lcol + a.loff[b];
     const int4* items = a.litems + a.lioff[b];
-    const int nitems = static_cast<int>(a.lioff[b + 1] - a.lioff[b]);
+    const int nitems = a.lnum[b];
+    const int* rp = a.lrp + r0 + b;
+    double* scr = scratch + w * kGroupEntries;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
@@ -428,21 +487,37 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int t = i / kTile;
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, z, lane, a.sleep_ns, &done_l,
-                                                 d.y >> 8, a.sleep_max);
-      if (rt) rt[1] = clock64();
-      if (lane == 0) {
-        // ring slot of tile t is free once tile t - kPR was consumed
+      if (k & kMultiFlag) {
+        bool has;
+        const double acc =
+            group_dot<kUnroll, false>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, z, scr, lane,
+                                      a.sleep_ns, &done_l, d.y >> 8, a.sleep_max, has);
+        if (rt) rt[1] = clock64();
         for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPR - 1);
              sl = min(2 * sl, a.sleep_max))
           __nanosleep(sl);
-        *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
-                                            (i % kTile) * kMaxSeg + k) = acc;
-        atomicAdd(&cnt[t % kPR], 1);
-        if (rt) {
-          rt[2] = clock64();
-          rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | k;
+        if (has)
+          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
+                                              ((i + lane) % kTile) * kMaxSeg) = acc;
+        const int np = __popc(__ballot_sync(0xffffffffu, has));
+        if (lane == 0) atomicAdd(&cnt[t % kPR], np);
+      } else {
+        const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, z, lane, a.sleep_ns,
+                                                   &done_l, d.y >> 8, a.sleep_max);
+        if (rt) rt[1] = clock64();
+        if (lane == 0) {
+          // ring slot of tile t is free once tile t - kPR was consumed
+          for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPR - 1);
+               sl = min(2 * sl, a.sleep_max))
+            __nanosleep(sl);
+          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
+                                              (i % kTile) * kMaxSeg + k) = acc;
+          atomicAdd(&cnt[t % kPR], 1);
         }
+      }
+      if (rt) {
+        rt[2] = clock64();
+        rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | (k & 7);
       }
     }
   }
@@ -499,8 +574,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const double* fv = a.uval + a.uoff[b];
     const uint16_t* fc = a.ucol + a.uoff[b];
     const int4* items = a.uitems + a.uioff[b];
-    const int nitems = static_cast<int>(a.uioff[b + 1] - a.uioff[b]);
-    const long long lit = a.lioff[b + 1] - a.lioff[b];
+    const int nitems = a.unum[b];
+    const long long lit = a.lnum[b];
+    const int* rp = a.urp + r0 + b;
+    double* scr = scratch + w * kGroupEntries;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_u && w + kWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kWorkers * lane];
@@ -518,20 +595,36 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int pos = nt - 1 - t;
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
-      const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, x, lane, a.sleep_ns,
-                                                    &done_u, d.y >> 8, a.sleep_max);
-      if (rt) rt[1] = clock64();
-      if (lane == 0) {
+      if (k & kMultiFlag) {
+        bool has;
+        const double acc =
+            group_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, x, scr, lane,
+                                         a.sleep_ns, &done_u, d.y >> 8, a.sleep_max, has);
+        if (rt) rt[1] = clock64();
         for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPR - 1);
              sl = min(2 * sl, a.sleep_max))
           __nanosleep(sl);
-        *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
-                                            (i % kTile) * kMaxSeg + k) = acc;
-        atomicAdd(&cnt[t % kPR], 1);
-        if (rt) {
-          rt[2] = clock64();
-          rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | k;
+        if (has)
+          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
+                                              ((i + lane) % kTile) * kMaxSeg) = acc;
+        const int np = __popc(__ballot_sync(0xffffffffu, has));
+        if (lane == 0) atomicAdd(&cnt[t % kPR], np);
+      } else {
+        const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, x, lane, a.sleep_ns,
+                                                      &done_u, d.y >> 8, a.sleep_max);
+        if (rt) rt[1] = clock64();
+        if (lane == 0) {
+          for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPR - 1);
+               sl = min(2 * sl, a.sleep_max))
+            __nanosleep(sl);
+          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
+                                              (i % kTile) * kMaxSeg + k) = acc;
+          atomicAdd(&cnt[t % kPR], 1);
         }
+      }
+      if (rt) {
+        rt[2] = clock64();
+        rt[3] = (static_cast<long long>(d.y >> 8) << 32) | (i << 3) | (k & 7);
       }
     }
   }
@@ -542,10 +635,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 }
 
 template <int kPR, bool kInPlace>
-size_t smem_bytes(int dim_max) {
+size_t smem_bytes(int dim_max, int workers) {
   const size_t dpad = (static_cast<size_t>(dim_max) + kTile - 1) & ~static_cast<size_t>(kTile - 1);
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
-                           static_cast<size_t>(kPR) * kPartTile + (kInPlace ? 1 : 2) * dpad);
+                           static_cast<size_t>(kPR) * kPartTile + (kInPlace ? 1 : 2) * dpad +
+                           static_cast<size_t>(workers) * kGroupEntries);
 }
 
 }  // namespace
@@ -572,6 +666,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.utile = fs.utile.as<double>();
   a.litems = fs.litems.as<int4>();
   a.uitems = fs.uitems.as<int4>();
+  a.lnum = fs.lnum.as<int>();
+  a.unum = fs.unum.as<int>();
+  a.lrp = fs.lrp.as<int>();
+  a.urp = fs.urp.as<int>();
   a.perm = fs.has_perm ? fs.perm.as<int>() : nullptr;
   a.order = fs.order.as<int>();
   a.pos0 = pos0;
@@ -613,16 +711,19 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   const int d = fs.max_dim;
   switch (variant) {
     case 1:  // 3 CTAs/SM: 12 warps, 4-tile sum ring (cfg4 3.19 ms, cfg5 9.30 ms)
-      launch(trisolve_kernel<12, 4, 3, 4, true, false>, 12, smem_bytes<4, true>(d));
+      launch(trisolve_kernel<12, 4, 3, 4, true, false>, 12, smem_bytes<4, true>(d, 11));
       break;
     case 2:  // producer warp issues the near tiles, 14 workers (cfg4 2.93, cfg5 9.54)
-      launch(trisolve_kernel<16, 4, 2, 8, true, true>, 16, smem_bytes<8, true>(d));
+      launch(trisolve_kernel<16, 4, 2, 8, true, true>, 16, smem_bytes<8, true>(d, 14));
+      break;
+    case 4:  // 8 far entries in flight per lane
+      launch(trisolve_kernel<16, 8, 2, 8, true, false>, 16, smem_bytes<8, true>(d, 15));
       break;
     case 3:  // separate z and x vectors (cfg4 2.78, cfg5 9.35)
-      launch(trisolve_kernel<16, 4, 2, 8, false, false>, 16, smem_bytes<8, false>(d));
+      launch(trisolve_kernel<16, 4, 2, 8, false, false>, 16, smem_bytes<8, false>(d, 15));
       break;
     default:  // 2 CTAs/SM (64 registers), x overwrites z in place (cfg4 2.68, cfg5 9.25)
-      launch(trisolve_kernel<16, 4, 2, 8, true, false>, 16, smem_bytes<8, true>(d));
+      launch(trisolve_kernel<16, 4, 2, 8, true, false>, 16, smem_bytes<8, true>(d, 15));
       break;
   }
   MSCG_CUDA(cudaGetLastError());

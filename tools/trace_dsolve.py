@@ -45,16 +45,42 @@ def main():
                                                  C.byref(st))
     assert rc == n, (rc, st.message)
     out = a.out or os.path.join(ROOT, "gpurun_out", f"trace_{a.config}.npz")
-    # far work items of block 0 (kSeg = 512 entries, at most 4 per row): the
-    # trace holds 4 stamps per item, then 3 per far chunk
+    # far work items of block 0, as factor.cu's pack kernel builds them: long
+    # rows in kSeg = 512 pieces (at most 4), runs of short rows (<= 96
+    # entries) of one tile grouped up to 128 entries.  The trace holds 4
+    # stamps per item.
     def nitems(m, lower):
         rp, ci = m.row_offsets, m.col_indices
-        tot = 0
+        cnt = []
         for i in range(n):
             c = ci[rp[i]:rp[i + 1]]
             t = i // 32
-            nf = int((c < 32 * (t - 2)).sum()) if lower else int((c >= 32 * (t + 3)).sum())
-            tot += min(4, (nf + 511) // 512)
+            cnt.append(int((c < 32 * (t - 2)).sum()) if lower else int((c >= 32 * (t + 3)).sum()))
+        order = range(n) if lower else range(n - 1, -1, -1)
+        tot, g0, g1, gent = 0, -1, -1, 0
+        for i in order:
+            c = cnt[i]
+            if c == 0:
+                continue
+            if c <= 96:
+                if g0 >= 0:
+                    lo, hi = min(g0, i), max(g1, i)
+                    if i // 32 != g0 // 32 or gent + c > 128 or hi - lo >= 32:
+                        tot += 1
+                        g0 = -1
+                if g0 < 0:
+                    g0 = g1 = i
+                    gent = 0
+                else:
+                    g0, g1 = min(g0, i), max(g1, i)
+                gent += c
+                continue
+            if g0 >= 0:
+                tot += 1
+                g0 = -1
+            tot += min(4, (c + 511) // 512)
+        if g0 >= 0:
+            tot += 1
         return tot
     np.savez_compressed(out, trace=buf, lnnz=np.diff(f.lower.row_offsets),
                         unnz=np.diff(f.upper.row_offsets),
