@@ -173,7 +173,7 @@ __device__ __forceinline__ Slice aligned_slice(const double* p, int len) {
 // The first round's loads are issued before the readiness wait (one poll
 // per warp on the tile counter).
 template <int kUnroll, bool kInPlace>
-__device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
+__device__ __noinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
                                           const int* done, int need, unsigned ns_max) {
@@ -351,7 +351,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int dpad = (a.dim_max + kTile - 1) & ~(kTile - 1);
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
-  static_assert(32 * kUnroll >= kGroupEntries, "a multi-row item is one round of loads");
   __shared__ __align__(8) uint64_t bars[kRing];
   __shared__ int done_l, done_u;
   __shared__ int cnt[kPR];    // far items published per ring tile
@@ -490,7 +489,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (k & kMultiFlag) {
         bool has;
         const double acc =
-            group_dot<kUnroll, false>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, z, scr, lane,
+            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, z, scr, lane,
                                       a.sleep_ns, &done_l, d.y >> 8, a.sleep_max, has);
         if (rt) rt[1] = clock64();
         for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPR - 1);
@@ -598,7 +597,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (k & kMultiFlag) {
         bool has;
         const double acc =
-            group_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, x, scr, lane,
+            group_dot<kGroupEntries / 32, kInPlace>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, x, scr, lane,
                                          a.sleep_ns, &done_u, d.y >> 8, a.sleep_max, has);
         if (rt) rt[1] = clock64();
         for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPR - 1);
