@@ -80,18 +80,51 @@ __global__ void __launch_bounds__(kThreads) nrm2_kernel(int n, const double* __r
   if (last_block(red)) finish(red, 1, out, 1);
 }
 
-// h[i] = V_i . w for i < nv  (one pass over w and the nv basis vectors)
+// h[i] = V_i . w for i < nv: basis vectors in groups of kDotGroup, so w is
+// read once per group and each CTA reduces kDotGroup sums per pass.
+constexpr int kDotGroup = 8;
 __global__ void __launch_bounds__(kThreads) multidot_kernel(int n, int nv, const double* __restrict__ V,
                                                             size_t ld, const double* __restrict__ w,
                                                             Reducer red, double* h) {
-  __shared__ double sh[kThreads / 32];
-  for (int i = 0; i < nv; ++i) {
-    const double* vi = V + ld * i;
-    double acc = 0.0;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
-      acc = fma(vi[r], w[r], acc);
-    const double s = block_sum(acc, sh);
-    if (threadIdx.x == 0) red.partials[static_cast<size_t>(i) * red.nblk + blockIdx.x] = s;
+  __shared__ double sh[kThreads / 32][kDotGroup];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i0 = 0; i0 < nv; i0 += kDotGroup) {
+    const int ng = min(kDotGroup, nv - i0);
+    double acc[kDotGroup];
+#pragma unroll
+    for (int g = 0; g < kDotGroup; ++g) acc[g] = 0.0;
+    const int stride = gridDim.x * blockDim.x;
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; r + stride < n; r += 2 * stride) {  // two rows in flight per thread
+      const double wr = w[r], wr2 = w[r + stride];
+      double va[kDotGroup], vb[kDotGroup];
+#pragma unroll
+      for (int g = 0; g < kDotGroup; ++g) {
+        va[g] = g < ng ? __ldg(V + ld * (i0 + g) + r) : 0.0;
+        vb[g] = g < ng ? __ldg(V + ld * (i0 + g) + r + stride) : 0.0;
+      }
+#pragma unroll
+      for (int g = 0; g < kDotGroup; ++g) acc[g] = fma(vb[g], wr2, fma(va[g], wr, acc[g]));
+    }
+    if (r < n) {
+      const double wr = w[r];
+#pragma unroll
+      for (int g = 0; g < kDotGroup; ++g)
+        if (g < ng) acc[g] = fma(__ldg(V + ld * (i0 + g) + r), wr, acc[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < kDotGroup; ++g) {
+      double v = acc[g];
+      for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) sh[warp][g] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < ng) {
+      double t = 0.0;
+      for (int k = 0; k < kThreads / 32; ++k) t += sh[k][threadIdx.x];
+      red.partials[static_cast<size_t>(i0 + threadIdx.x) * red.nblk + blockIdx.x] = t;
+    }
+    __syncthreads();
   }
   if (last_block(red)) finish(red, nv, h, 0);
 }
