@@ -447,13 +447,16 @@ __device__ __forceinline__ bool l_far(int c, int i) {
 __device__ __forceinline__ bool u_far(int c, int i) {
   return c >= ((i >> 5) + kNearTiles) * kTile;
 }
+// Neighbour-window entries (the two tiles next to the diagonal tile).
+__device__ __forceinline__ bool l_nbr(int c, int i) { return !l_far(c, i) && c < (i >> 5) * kTile; }
+__device__ __forceinline__ bool u_nbr(int c, int i) { return !u_far(c, i) && c >= ((i >> 5) + 1) * kTile; }
 
 // Per row far counts (into lrp/urp scratch slots) and per block totals.
 __global__ void __launch_bounds__(256) count_far_kernel(
     const int* __restrict__ set_row0, const int* __restrict__ blk_dim, PoolView pool,
-    int* __restrict__ lcnt, int* __restrict__ ucnt, long long* __restrict__ far_l,
-    long long* __restrict__ far_u, long long* __restrict__ items_l,
-    long long* __restrict__ items_u) {
+    int* __restrict__ lcnt, int* __restrict__ ucnt, int* __restrict__ lnb,
+    int* __restrict__ unb, long long* __restrict__ far_l, long long* __restrict__ far_u,
+    long long* __restrict__ items_l, long long* __restrict__ items_u) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,14 +472,26 @@ __global__ void __launch_bounds__(256) count_far_kernel(
   for (int i = warp; i < n; i += blockDim.x / 32) {
     const uint32_t ls = pool.lstart[r0 + i], us = pool.ustart[r0 + i];
     const int ll = pool.llen[r0 + i], ul = pool.ulen[r0 + i];
-    int cl = 0, cu = 0;
-    for (int q = lane; q < ll; q += 32) cl += l_far(pool.lcol[ls + q], i);
-    for (int q = lane; q < ul; q += 32) cu += u_far(pool.ucol[us + q], i);
+    int cl = 0, cu = 0, nl = 0, nu = 0;
+    for (int q = lane; q < ll; q += 32) {
+      const int c = pool.lcol[ls + q];
+      cl += l_far(c, i);
+      nl += l_nbr(c, i);
+    }
+    for (int q = lane; q < ul; q += 32) {
+      const int c = pool.ucol[us + q];
+      cu += u_far(c, i);
+      nu += u_nbr(c, i);
+    }
     cl = __reduce_add_sync(0xffffffffu, cl);
     cu = __reduce_add_sync(0xffffffffu, cu);
+    nl = __reduce_add_sync(0xffffffffu, nl);
+    nu = __reduce_add_sync(0xffffffffu, nu);
     if (lane == 0) {
       lcnt[r0 + i] = cl;
       ucnt[r0 + i] = cu;
+      lnb[r0 + i] = nl;
+      unb[r0 + i] = nu;
       tl += cl;
       tu += cu;
       jl += far_segments(cl);
@@ -508,7 +523,8 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
     uint16_t* __restrict__ ucol, double* __restrict__ ltile, double* __restrict__ utile,
     double* __restrict__ urdiag, const long long* __restrict__ lioff,
     const long long* __restrict__ uioff, int4* __restrict__ litems, int4* __restrict__ uitems,
-    int* __restrict__ lnum, int* __restrict__ unum) {
+    int* __restrict__ lnum, int* __restrict__ unum, const int* __restrict__ lnb,
+    const int* __restrict__ unb, int* __restrict__ lwidth, int* __restrict__ uwidth) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   int* lr = lrp + r0 + b;
@@ -572,62 +588,118 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned ltmask = (1u << lane) - 1u;
   const long long lb = loff[b], ub = uoff[b];
-  double* lt = ltile + toff[b] * kTileElems;
-  double* ut = utile + toff[b] * kTileElems;
-  for (int i = warp; i < n; i += blockDim.x / 32) {
+  const int nt = (n + kTile - 1) / kTile;
+  const long long tb = toff[b];
+  double* lt = ltile + tb * kTileElems;
+  double* ut = utile + tb * kTileElems;
+  // Neighbour-window format per tile: ELL width (widest row) or dense.
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    int ml = 0, mu = 0;
+    for (int i = t * kTile; i < min(n, (t + 1) * kTile); ++i) {
+      ml = max(ml, lnb[r0 + i]);
+      mu = max(mu, unb[r0 + i]);
+    }
+    lwidth[tb + t] = ell_width(ml);
+    uwidth[tb + t] = ell_width(mu);
+  }
+  __syncthreads();
+  // Headers: the solver issues near items q = 0 .. 2nt-1 (L tiles ascending,
+  // then U tiles descending); item q carries the copy size of item q + kRing.
+  auto item_w = [&](int q) { return q < nt ? lwidth[tb + q] : uwidth[tb + 2 * nt - 1 - q]; };
+  for (int q = threadIdx.x; q < 2 * nt; q += blockDim.x) {
+    double* T = q < nt ? lt + static_cast<long long>(q) * kTileElems
+                       : ut + static_cast<long long>(2 * nt - 1 - q) * kTileElems;
+    T[kHdr] = __longlong_as_double(item_w(q));
+    T[kHdr + 1] = __longlong_as_double(
+        q + kRing < 2 * nt ? 8LL * tile_elems(item_w(q + kRing)) : 0LL);
+  }
+  for (int i = warp; i < nt * kTile; i += blockDim.x / 32) {
     const int t = i >> 5, j = i & 31;
-    if (lane == 0) {
+    const bool row = i < n;
+    double* ltt = lt + static_cast<long long>(t) * kTileElems;
+    double* utt = ut + static_cast<long long>(t) * kTileElems;
+    const int wl = lwidth[tb + t], wu = uwidth[tb + t];
+    if (lane == 0 && row) {
       const double rd = 1.0 / pool.udiag[r0 + i];
       urdiag[r0 + i] = rd;
       // tile metadata for the solver (see kMetaDiag / kMetaSeg)
-      double* ltm = lt + static_cast<long long>(t) * kTileElems;
-      double* utm = ut + static_cast<long long>(t) * kTileElems;
-      utm[kMetaDiag + j] = rd;
-      ltm[kMetaSeg + j] = __longlong_as_double(far_segments(lcnt[r0 + i]));
-      utm[kMetaSeg + j] = __longlong_as_double(far_segments(ucnt[r0 + i]));
+      utt[kMetaDiag + j] = rd;
+      ltt[kMetaSeg + j] = __longlong_as_double(far_segments(lcnt[r0 + i]));
+      utt[kMetaSeg + j] = __longlong_as_double(far_segments(ucnt[r0 + i]));
     }
+    // window padding: every ELL slot past the row's entries reads a solved slot
+    if (wl != kDenseNbr)
+      for (int e = (row ? lnb[r0 + i] : 0) + lane; e < wl; e += 32)
+        reinterpret_cast<unsigned char*>(ltt)[ell_colbyte(j, e)] = kPadColL;
+    if (wu != kDenseNbr)
+      for (int e = (row ? unb[r0 + i] : 0) + lane; e < wu; e += 32)
+        reinterpret_cast<unsigned char*>(utt)[ell_colbyte(j, e)] = kPadColU;
+    if (!row) continue;
     {
       const uint32_t ls = pool.lstart[r0 + i];
       const int ll = pool.llen[r0 + i];
       long long w = lb + lr[i];
+      int e0 = 0;  // neighbour entries of the row so far
       for (int q0 = 0; q0 < ll; q0 += 32) {
         const int q = q0 + lane;
         const bool in = q < ll;
         const int c = in ? pool.lcol[ls + q] : 0;
         const double v = in ? pool.lval[ls + q] : 0.0;
         const bool far = in && l_far(c, i);
+        const bool nbr = in && l_nbr(c, i);
         const unsigned bf = __ballot_sync(0xffffffffu, far);
+        const unsigned bn = __ballot_sync(0xffffffffu, nbr);
+        const int k = c - (t - (kNearTiles - 1)) * kTile;  // window column 0..95
         if (far) {
           lval[w + __popc(bf & ltmask)] = v;
           lcol[w + __popc(bf & ltmask)] = static_cast<uint16_t>(c);
+        } else if (nbr) {
+          const int e = e0 + __popc(bn & ltmask);
+          if (wl == kDenseNbr) {
+            ltt[kNbrOff + k * kTile + j] = v;
+          } else {
+            ltt[ell_val(wl, j, e)] = v;
+            reinterpret_cast<unsigned char*>(ltt)[ell_colbyte(j, e)] = static_cast<unsigned char>(k);
+          }
         } else if (in) {
-          const int k = c - (t - (kNearTiles - 1)) * kTile;  // 0..95
-          lt[static_cast<long long>(t) * kTileElems +
-             (k < 2 * kTile ? k * kTile + j : kTriOff + tri_l(j, k - 2 * kTile))] = v;
+          ltt[kTriOff + tri_l(j, k - 2 * kTile)] = v;
         }
         w += __popc(bf);
+        e0 += __popc(bn);
       }
     }
     {
       const uint32_t us = pool.ustart[r0 + i];
       const int ul = pool.ulen[r0 + i];
       long long w = ub + ur[i];
+      int e0 = 0;
       for (int q0 = 0; q0 < ul; q0 += 32) {
         const int q = q0 + lane;
         const bool in = q < ul;
         const int c = in ? pool.ucol[us + q] : 0;
         const double v = in ? pool.uval[us + q] : 0.0;
         const bool far = in && u_far(c, i);
+        const bool nbr = in && u_nbr(c, i);
         const unsigned bf = __ballot_sync(0xffffffffu, far);
+        const unsigned bn = __ballot_sync(0xffffffffu, nbr);
+        const int k = c - t * kTile;  // 0..95
         if (far) {
           uval[w + __popc(bf & ltmask)] = v;
           ucol[w + __popc(bf & ltmask)] = static_cast<uint16_t>(c);
+        } else if (nbr) {
+          const int e = e0 + __popc(bn & ltmask);
+          if (wu == kDenseNbr) {
+            utt[kNbrOff + (k - kTile) * kTile + j] = v;
+          } else {
+            utt[ell_val(wu, j, e)] = v;
+            reinterpret_cast<unsigned char*>(utt)[ell_colbyte(j, e)] =
+                static_cast<unsigned char>(k - kTile);
+          }
         } else if (in) {
-          const int k = c - t * kTile;  // 0..95
-          ut[static_cast<long long>(t) * kTileElems +
-             (k < kTile ? kTriOff + tri_u(j, k) : (k - kTile) * kTile + j)] = v;
+          utt[kTriOff + tri_u(j, k)] = v;
         }
         w += __popc(bf);
+        e0 += __popc(bn);
       }
     }
   }
@@ -635,7 +707,6 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   // must have published `need` tiles of its pass before the item's columns
   // are all final.  L: highest column's tile + 1; U: tiles above the lowest.
   __syncthreads();
-  const int nt = (n + kTile - 1) / kTile;
   for (long long q = lioff[b] + threadIdx.x; q < lioff[b] + lnum[b]; q += blockDim.x) {
     int4 d = litems[q];
     int c = lcol[lb + d.w - 1];
@@ -854,10 +925,12 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   pv.ulen = ulen.as<int>();
   pv.udiag = fs->udiag.as<double>();
   DevBuf lcnt(sizeof(int) * total), ucnt(sizeof(int) * total);
+  DevBuf lnb(sizeof(int) * total), unb(sizeof(int) * total);
   DevBuf farl(sizeof(long long) * nb), faru(sizeof(long long) * nb);
   DevBuf itl(sizeof(long long) * nb), itu(sizeof(long long) * nb);
   count_far_kernel<<<nb, 256, 0, s>>>(fs->row0.as<int>(), fs->dim.as<int>(), pv, lcnt.as<int>(),
-                                      ucnt.as<int>(), farl.as<long long>(), faru.as<long long>(),
+                                      ucnt.as<int>(), lnb.as<int>(), unb.as<int>(),
+                                      farl.as<long long>(), faru.as<long long>(),
                                       itl.as<long long>(), itu.as<long long>());
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
@@ -884,22 +957,6 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   fs->toff = upload_vec(fs->h_toff, s);
   fs->lioff = upload_vec(fs->h_lioff, s);
   fs->uioff = upload_vec(fs->h_uioff, s);
-  {
-    // Launch order for the solve: longest blocks first, so the last wave of
-    // CTAs holds the shortest blocks (LPT).  Cost ~ far entries + near tiles.
-    std::vector<int> ord(nb);
-    std::iota(ord.begin(), ord.end(), 0);
-    auto cost = [&](int b) {
-      return hl[b] + hu[b] + 2LL * kTileElems * (fs->h_toff[b + 1] - fs->h_toff[b]);
-    };
-    fs->h_chunk.assign(kSolveChunks + 1, 0);
-    for (int c = 0; c <= kSolveChunks; ++c)
-      fs->h_chunk[c] = static_cast<int>(static_cast<long long>(nb) * c / kSolveChunks);
-    for (int c = 0; c < kSolveChunks; ++c)
-      std::stable_sort(ord.begin() + fs->h_chunk[c], ord.begin() + fs->h_chunk[c + 1],
-                       [&](int x, int y) { return cost(x) > cost(y); });
-    fs->order = upload_vec(ord, s);
-  }
   fs->litems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_lioff[nb]));
   fs->uitems = DevBuf(sizeof(int4) * std::max<long long>(1, fs->h_uioff[nb]));
   fs->lnum = DevBuf(sizeof(int) * std::max(1, nb));
@@ -914,6 +971,8 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   fs->ltile = DevBuf(tile_bytes);
   fs->utile = DevBuf(tile_bytes);
   fs->urdiag = DevBuf(sizeof(double) * total);
+  fs->lwidth = DevBuf(sizeof(int) * std::max<long long>(1, fs->tiles()));
+  fs->uwidth = DevBuf(sizeof(int) * std::max<long long>(1, fs->tiles()));
   MSCG_CUDA(cudaMemsetAsync(fs->ltile.p, 0, tile_bytes, s));
   MSCG_CUDA(cudaMemsetAsync(fs->utile.p, 0, tile_bytes, s));
   pack_tiled_kernel<<<nb, 256, 0, s>>>(
@@ -923,10 +982,37 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
       fs->uval.as<double>(), fs->ucol.as<uint16_t>(), fs->ltile.as<double>(),
       fs->utile.as<double>(), fs->urdiag.as<double>(), fs->lioff.as<long long>(),
       fs->uioff.as<long long>(), fs->litems.as<int4>(), fs->uitems.as<int4>(),
-      fs->lnum.as<int>(), fs->unum.as<int>());
+      fs->lnum.as<int>(), fs->unum.as<int>(), lnb.as<int>(), unb.as<int>(),
+      fs->lwidth.as<int>(), fs->uwidth.as<int>());
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
+  fs->h_lwidth.resize(fs->tiles());
+  fs->h_uwidth.resize(fs->tiles());
+  if (fs->tiles()) {
+    MSCG_CUDA(cudaMemcpyAsync(fs->h_lwidth.data(), fs->lwidth.p, sizeof(int) * fs->tiles(), cudaMemcpyDeviceToHost, s));
+    MSCG_CUDA(cudaMemcpyAsync(fs->h_uwidth.data(), fs->uwidth.p, sizeof(int) * fs->tiles(), cudaMemcpyDeviceToHost, s));
+  }
   MSCG_CUDA(cudaStreamSynchronize(s));
+  {
+    // Launch order for the solve: longest blocks first, so the last wave of
+    // CTAs holds the shortest blocks (LPT).  Cost ~ bytes: far entries plus
+    // the copied near tiles.
+    std::vector<int> ord(nb);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::vector<long long> tile_cost(nb, 0);
+    for (int b = 0; b < nb; ++b)
+      for (long long t = fs->h_toff[b]; t < fs->h_toff[b + 1]; ++t)
+        tile_cost[b] += tile_elems(fs->h_lwidth[t]) + tile_elems(fs->h_uwidth[t]);
+    auto cost = [&](int b) { return 10 * (hl[b] + hu[b]) + 8 * tile_cost[b]; };
+    fs->h_chunk.assign(kSolveChunks + 1, 0);
+    for (int c = 0; c <= kSolveChunks; ++c)
+      fs->h_chunk[c] = static_cast<int>(static_cast<long long>(nb) * c / kSolveChunks);
+    for (int c = 0; c < kSolveChunks; ++c)
+      std::stable_sort(ord.begin() + fs->h_chunk[c], ord.begin() + fs->h_chunk[c + 1],
+                       [&](int x, int y) { return cost(x) > cost(y); });
+    fs->order = upload_vec(ord, s);
+  }
+
   if (times) times->pack_s += std::chrono::duration<double>(clk::now() - t3).count();
   return fs;
 }
@@ -988,28 +1074,49 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
       lci.push_back(hlc[k]);
       lv.push_back(hlv[k]);
     }
-    for (int k = 0; k < kNearTiles * kTile; ++k) {
+    // near window in ascending column order: neighbour tiles, then the
+    // diagonal tile (absent entries are zeros; stored values never are)
+    auto nbr_entries = [&](const double* T, int w, int j, auto&& emit) {
+      if (w == kDenseNbr) {
+        for (int k = 0; k < 2 * kTile; ++k) emit(k, T[kNbrOff + k * kTile + j]);
+      } else {
+        const unsigned char* cb = reinterpret_cast<const unsigned char*>(T);
+        for (int e = 0; e < w; ++e) emit(cb[ell_colbyte(j, e)], T[ell_val(w, j, e)]);
+      }
+    };
+    const double* LT = &hlt[t * tsz];
+    const double* UT = &hut[t * tsz];
+    nbr_entries(LT, fs.h_lwidth[t0 + t], j, [&](int k, double v) {
       const int c = (t - (kNearTiles - 1)) * kTile + k;
-      const int kd = k - 2 * kTile;
-      if (kd >= j) continue;  // diagonal tile: strictly lower part only
-      const double v = hlt[t * tsz + (kd < 0 ? k * kTile + j : kTriOff + tri_l(j, kd))];
-      if (c >= 0 && c < i && v != 0.0) {
+      if (c >= 0 && v != 0.0) {
         lci.push_back(c);
+        lv.push_back(v);
+      }
+    });
+    for (int k = 0; k < j; ++k) {
+      const double v = LT[kTriOff + tri_l(j, k)];
+      if (v != 0.0) {
+        lci.push_back(t * kTile + k);
         lv.push_back(v);
       }
     }
     lrp[i + 1] = static_cast<int>(lci.size());
     uci.push_back(i);
     uv.push_back(hd[i]);
-    for (int k = 0; k < kNearTiles * kTile; ++k) {
-      const int c = t * kTile + k;
-      if (k < kTile && k <= j) continue;  // diagonal tile: strictly upper part only
-      const double v = hut[t * tsz + (k < kTile ? kTriOff + tri_u(j, k) : (k - kTile) * kTile + j)];
-      if (c > i && c < n && v != 0.0) {
-        uci.push_back(c);
+    for (int k = j + 1; k < kTile; ++k) {
+      const double v = UT[kTriOff + tri_u(j, k)];
+      if (t * kTile + k < n && v != 0.0) {
+        uci.push_back(t * kTile + k);
         uv.push_back(v);
       }
     }
+    nbr_entries(UT, fs.h_uwidth[t0 + t], j, [&](int k, double v) {
+      const int c = (t + 1) * kTile + k;
+      if (c < n && v != 0.0) {
+        uci.push_back(c);
+        uv.push_back(v);
+      }
+    });
     for (int k = hur[i]; k < hur[i + 1]; ++k) {
       uci.push_back(huc[k]);
       uv.push_back(huv[k]);

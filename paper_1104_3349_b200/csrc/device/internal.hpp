@@ -75,22 +75,56 @@ void spmv(const DevCsr& a, const double* x, double* y, const double* base, int m
 // never zero), so the reference CSR is recoverable exactly.
 constexpr int kTile = 32;
 constexpr int kNearTiles = 3;
-// Stored near tile: the two neighbour tiles dense (L: t-2, t-1; U: t+1, t+2;
-// 32 x 64 column-major, entry [k*32 + j]), then the strictly triangular part
-// of the diagonal tile packed by column (tri_l / tri_u), then per-row
-// metadata the chain needs, so that one TMA copy brings everything and the
-// solver warp issues no global loads: [kMetaDiag + j] = 1 / U_jj (U tiles),
-// [kMetaSeg + j] = far work items of row j (int in the low 32 bits).
-constexpr int kNbrElems = 2 * kTile * kTile;
-constexpr int kTriOff = kNbrElems;
+// Stored near tile (one TMA copy brings everything the chain needs, so the
+// solver warp issues no global loads), in this order:
+//  * per-row metadata: [kMetaDiag + j] = 1 / U_jj (U tiles), [kMetaSeg + j]
+//    = far work items of row j (int in the low 32 bits);
+//  * header: [kHdr] = ELL width W of this tile (or kDenseNbr), [kHdr + 1] =
+//    bytes of the near item the solver issues kRing items later (the tile
+//    stream carries its own copy sizes);
+//  * the strictly triangular part of the diagonal tile packed by column
+//    (tri_l / tri_u);
+//  * the two neighbour tiles (L: t-2, t-1; U: t+1, t+2), as a 64-column
+//    window, either
+//      - ELL (W entries per row, W a multiple of 4, rows padded with zero
+//        values): window columns as bytes, word [(e/4)*32 + j] holding
+//        entries 4(e/4)..+3 of row j, then values as double2 pairs
+//        [(e/2)*32 + j] — 36 W doubles; or
+//      - dense (kDenseNbr, when ELL would not be smaller): 32 x 64
+//        column-major, entry [k*32 + j].
+// Only the used prefix of a tile is copied (kNbrOff + 36 W doubles for ELL).
+constexpr int kMetaDiag = 0;
+constexpr int kMetaSeg = kTile;
+constexpr int kHdr = 2 * kTile;
+constexpr int kTriOff = kHdr + 4;
 constexpr int kTriElems = kTile * (kTile - 1) / 2;
 // L: column k holds rows k+1..31; U: column k holds rows 0..k-1.
 __host__ __device__ constexpr int tri_l(int j, int k) { return k * (2 * kTile - 1 - k) / 2 + j - k - 1; }
 __host__ __device__ constexpr int tri_u(int j, int k) { return k * (k - 1) / 2 + j; }
-constexpr int kNearElems = kNbrElems + kTriElems;
-constexpr int kMetaDiag = kNearElems;
-constexpr int kMetaSeg = kNearElems + kTile;
-constexpr int kTileElems = kNearElems + 2 * kTile;
+constexpr int kNbrOff = kTriOff + kTriElems;
+constexpr int kNbrElems = 2 * kTile * kTile;
+constexpr int kTileElems = kNbrOff + kNbrElems;
+constexpr int kDenseNbr = -1;
+constexpr int kEllMax = ((kNbrElems / 36) / 4) * 4;  // widest ELL smaller than dense (56)
+__host__ __device__ constexpr int ell_width(int maxrow) {
+  return (maxrow + 3) / 4 * 4 > kEllMax ? kDenseNbr : (maxrow + 3) / 4 * 4;
+}
+__host__ __device__ constexpr int tile_elems(int w) {
+  return w == kDenseNbr ? kTileElems : kNbrOff + 36 * w;
+}
+// ELL entry e of row j: value index and column byte index within the tile.
+__host__ __device__ constexpr int ell_val(int w, int j, int e) {
+  return kNbrOff + 4 * w + ((e >> 1) * kTile + j) * 2 + (e & 1);
+}
+__host__ __device__ constexpr int ell_colbyte(int j, int e) {
+  return kNbrOff * 8 + ((e >> 2) * kTile + j) * 4 + (e & 3);
+}
+// Window padding column (a slot that is always solved before use): L: the
+// last row of tile t-1; U: the first row of tile t+1.
+constexpr int kPadColL = 2 * kTile - 1;
+constexpr int kPadColU = 0;
+// Near items in flight per solver (TMA ring depth).
+constexpr int kRing = 2;
 // Far entries of a row are cut into work items of kSeg entries (at most
 // kMaxSeg per row; the last item takes the remainder).  Item lists per block
 // and pass (L: rows ascending, U: rows descending) hold int4 {row, seg,
@@ -126,7 +160,9 @@ struct FactorSet {
   DevBuf lrp, urp;                         // int32[total_rows + nblocks]
   DevBuf lval, uval;                       // fp64 (far entries)
   DevBuf lcol, ucol;                       // uint16
-  DevBuf ltile, utile;                     // fp64 [tiles][kTileElems]
+  DevBuf ltile, utile;                     // fp64 [tiles][kTileElems] (used prefix varies)
+  DevBuf lwidth, uwidth;                   // int32[tiles]: ELL width or kDenseNbr
+  std::vector<int> h_lwidth, h_uwidth;
   std::vector<int64_t> h_lioff, h_uioff;   // per block far work-item offsets (+1)
   DevBuf lioff, uioff;                     // int64[nblocks+1] (capacity)
   DevBuf lnum, unum;                       // int32[nblocks] items in use

@@ -47,11 +47,9 @@ namespace mscg {
 
 namespace {
 
-constexpr int kRing = 2;               // TMA ring depth (near tiles + rhs slice)
 constexpr int kPartTile = kTile * kMaxSeg;
 constexpr int kVecElems = 40;          // rhs slice: 32 + alignment slack
 constexpr int kSlotElems = kTileElems + kVecElems;
-constexpr unsigned kTileBytes = kTileElems * sizeof(double);
 
 struct TriArgs {
   const int* row0;
@@ -67,6 +65,8 @@ struct TriArgs {
   const uint16_t* ucol;
   const double* ltile;
   const double* utile;
+  const int* lwidth;   // per tile: ELL width of the neighbour window or kDenseNbr
+  const int* uwidth;
   const int4* litems;  // {row, segment | need << 8, begin, end}
   const int4* uitems;
   const int* lnum;     // items per block
@@ -296,6 +296,25 @@ __device__ __forceinline__ double neighbour(const double* T, int c0, int j, cons
   return (a0 + a1) + (a2 + a3);
 }
 
+// Same over the ELL neighbour window (see internal.hpp): W entries per row,
+// window columns as bytes (4 per word), values as double2 pairs; win = the
+// solution of the two neighbour tiles (64 slots).
+__device__ __forceinline__ double ell_neighbours(const double* T, int w, int j,
+                                                 const double* win) {
+  const uint32_t* cw = reinterpret_cast<const uint32_t*>(T + kNbrOff);
+  const double2* vv = reinterpret_cast<const double2*>(T + kNbrOff + 4 * w);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int e4 = 0; e4 < (w >> 2); ++e4) {
+    const uint32_t c = cw[e4 * kTile + j];
+    const double2 p = vv[(2 * e4) * kTile + j], q = vv[(2 * e4 + 1) * kTile + j];
+    a0 = fma(p.x, win[c & 0xff], a0);
+    a1 = fma(p.y, win[(c >> 8) & 0xff], a1);
+    a2 = fma(q.x, win[(c >> 16) & 0xff], a2);
+    a3 = fma(q.y, win[c >> 24], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
 // Solver: wait until `expected` far items of the tile were published, then
 // reset the counter for the ring tile's next use.  All lanes poll the same
 // word, so the exit is warp-uniform and the chain that follows keeps the
@@ -381,7 +400,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   // Near item q: q < nt -> L tile q (+ rhs slice), else U tile 2nt-1-q.
   // Item q lives in slot q % kRing, phase (q / kRing) & 1.
   const int* pm = a.perm ? a.perm + r0 : nullptr;
-  auto issue = [&](int q) {  // solver lane 0
+  // `bytes`: the item's used prefix (its predecessor kRing items earlier
+  // carries it in its header; the first kRing come from the width tables).
+  auto issue = [&](int q, unsigned bytes) {  // solver lane 0
     const int slot = q % kRing;
     double* dst = ring + slot * kSlotElems;
     const bool lpass = q < nt;
@@ -389,9 +410,18 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const double* tile = (lpass ? lt : ut) + static_cast<long long>(t) * kTileElems;
     Slice sr{nullptr, 0, 0};
     if (lpass && !pm) sr = aligned_slice(rhs + r0 + t * kTile, min(kTile, n - t * kTile));
-    mbar_expect_tx(&bars[slot], kTileBytes + sr.bytes);
-    bulk_load(dst, tile, kTileBytes, &bars[slot]);
+    mbar_expect_tx(&bars[slot], bytes + sr.bytes);
+    bulk_load(dst, tile, bytes, &bars[slot]);
     if (sr.bytes) bulk_load(dst + kTileElems, sr.src, sr.bytes, &bars[slot]);
+  };
+  auto first_bytes = [&](int q) {
+    const long long tb = a.toff[b];
+    const int w = q < nt ? a.lwidth[tb + q] : a.uwidth[tb + 2 * nt - 1 - q];
+    return static_cast<unsigned>(8 * tile_elems(w));
+  };
+  // copy size of item q + kRing, from item q's header (slot still intact)
+  auto next_bytes = [&](int q) {
+    return static_cast<unsigned>(meta_int(ring + (q % kRing) * kSlotElems, kHdr + 1));
   };
   // Producer: issue near items [q0, q1) as their slots free up (item q
   // reuses the slot of item q - kRing, consumed once the solver published
@@ -402,7 +432,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int* ctr = prev < nt ? &done_l : &done_u;
       const int need = prev < nt ? prev + 1 : prev - nt + 1;
       for (unsigned sl = 16; vload(ctr) < need; sl = min(2 * sl, 256u)) __nanosleep(sl);
-      if (lane == 0) issue(q);
+      if (lane == 0) issue(q, next_bytes(prev));
       __syncwarp();
     }
   };
@@ -412,7 +442,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   // ================================================================ L pass
   if (warp == 0) {
     if (lane == 0) {
-      for (int q = 0; q < kRing && q < 2 * nt; ++q) issue(q);
+      for (int q = 0; q < kRing && q < 2 * nt; ++q) issue(q, first_bytes(q));
       // the block's work-item lists go to L2 once
       l2_prefetch(reinterpret_cast<const void*>(reinterpret_cast<unsigned long long>(
                       a.litems + a.lioff[b]) & ~15ull),
@@ -432,9 +462,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int off = static_cast<int>((reinterpret_cast<unsigned long long>(rhs + r0 + t * kTile) & 15) >> 3);
       const double bi = valid ? (pm ? bperm : T[kTileElems + off + j]) : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
+      const int wn = meta_int(T, kHdr);
       double nb = 0.0;
-      if (t > 1) nb += neighbour(T, 0, j, z + (t - 2) * kTile);
-      if (t > 0) nb += neighbour(T, kTile, j, z + (t - 1) * kTile);
+      if (wn == kDenseNbr) {
+        if (t > 1) nb += neighbour(T + kNbrOff, 0, j, z + (t - 2) * kTile);
+        if (t > 0) nb += neighbour(T + kNbrOff, kTile, j, z + (t - 1) * kTile);
+      } else {
+        nb = ell_neighbours(T, wn, j, z + (t - 2) * kTile);
+      }
       wait_items(&cnt[t % kPR], __reduce_add_sync(0xffffffffu, nseg), lane);
       const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
@@ -454,7 +489,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&done_l) = t + 1;
         if (tr) tr[4 * t + 2] = clock64();
-        if (!kProducer && t + kRing < 2 * nt) issue(t + kRing);
+        if (!kProducer && t + kRing < 2 * nt) issue(t + kRing, next_bytes(t));
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 3] = clock64();
@@ -536,9 +571,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double* T = ring + slot * kSlotElems;
       const double rd = valid ? T[kMetaDiag + j] : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
+      const int wn = meta_int(T, kHdr);
       double nb = 0.0;
-      if (tt > 0) nb += neighbour(T, 0, j, x + (t + 1) * kTile);
-      if (tt > 1) nb += neighbour(T, kTile, j, x + (t + 2) * kTile);
+      if (wn == kDenseNbr) {
+        if (tt > 0) nb += neighbour(T + kNbrOff, 0, j, x + (t + 1) * kTile);
+        if (tt > 1) nb += neighbour(T + kNbrOff, kTile, j, x + (t + 2) * kTile);
+      } else {
+        nb = ell_neighbours(T, wn, j, x + (t + 1) * kTile);
+      }
       wait_items(&cnt[t % kPR], __reduce_add_sync(0xffffffffu, nseg), lane);
       const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
@@ -560,7 +600,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         else
           *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
         if (tr) tr[4 * q + 2] = clock64();
-        if (!kProducer && q + kRing < 2 * nt) issue(q + kRing);
+        if (!kProducer && q + kRing < 2 * nt) issue(q + kRing, next_bytes(q));
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 3] = clock64();
@@ -663,6 +703,8 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.ucol = fs.ucol.as<uint16_t>();
   a.ltile = fs.ltile.as<double>();
   a.utile = fs.utile.as<double>();
+  a.lwidth = fs.lwidth.as<int>();
+  a.uwidth = fs.uwidth.as<int>();
   a.litems = fs.litems.as<int4>();
   a.uitems = fs.uitems.as<int4>();
   a.lnum = fs.lnum.as<int>();
