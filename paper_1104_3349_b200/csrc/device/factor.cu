@@ -64,22 +64,145 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
 // ---- ILUT ------------------------------------------------------------------
 
+// Finished-row record read by later pivots: {U_kk bits, ustart | ulen << 32}.
+__device__ __forceinline__ longlong2 load_rec(const longlong2* recs, int g) {
+  return recs[g];
+}
+
+constexpr int kIlutBatch = 4;  // U-row entries per lane in flight per round
+constexpr int kNone = 0x7fffffff;
+constexpr int kPfCands = 16;   // cached candidates whose U rows are L2-prefetched at refill
+
+// Fire-and-forget L2 prefetch of a finished U row (values + columns): the
+// pivots' U rows are re-read from HBM (a block's U outgrows its share of
+// L2), so the rows of the upcoming pivots are requested well ahead.
+__device__ __forceinline__ void prefetch_urow(const PoolView& pool, long long ry) {
+  const uint32_t s0 = static_cast<uint32_t>(ry);
+  const int len = static_cast<int>(static_cast<unsigned long long>(ry) >> 32);
+  if (len <= 0) return;
+  const unsigned long long v0 = reinterpret_cast<unsigned long long>(pool.uval + s0) & ~15ull;
+  const unsigned long long v1 = (reinterpret_cast<unsigned long long>(pool.uval + s0 + len) + 15) & ~15ull;
+  const unsigned long long c0 = reinterpret_cast<unsigned long long>(pool.ucol + s0) & ~15ull;
+  const unsigned long long c1 = (reinterpret_cast<unsigned long long>(pool.ucol + s0 + len) + 15) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v0), "r"(static_cast<unsigned>(v1 - v0)) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c0), "r"(static_cast<unsigned>(c1 - c0)) : "memory");
+}
+
+// Candidate cache: lane L holds one pending column (cand, kNone if empty) and
+// its row record (rec, loaded asynchronously).  Invariant: the cache holds
+// every pending column in (kk, hi) — refill() scans the bitmap from `from`,
+// caches the first (up to) 32 set bits below `end` and returns hi.
+__device__ __forceinline__ int refill(const uint32_t* bits, int from, int end, unsigned lane,
+                                      int* slot, const longlong2* brec, int& cand,
+                                      longlong2& rec, bool& pf) {
+  cand = kNone;
+  pf = false;
+  for (int wb = from >> 5; (wb << 5) < end; wb += 32) {
+    const int w = wb + static_cast<int>(lane);
+    unsigned word = 0;
+    if ((w << 5) < end) {
+      word = bits[w];
+      if (w == (from >> 5)) word &= ~0u << (from & 31);
+      if (((w + 1) << 5) > end) word &= (1u << (end & 31)) - 1u;
+    }
+    const int c = __popc(word);
+    int pre = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (static_cast<int>(lane) >= o) pre += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    if (total == 0) continue;
+    for (int r = pre - c; word && r < 32; ++r) {
+      slot[r] = (w << 5) + __ffs(word) - 1;
+      word &= word - 1;
+    }
+    __syncwarp();
+    if (static_cast<int>(lane) < min(total, 32)) {
+      cand = slot[lane];
+      rec = load_rec(brec, cand);
+      pf = static_cast<int>(lane) < kPfCands;
+    }
+    const int hi = total > 32 ? slot[31] + 1 : min(end, (wb + 32) << 5);
+    __syncwarp();  // slot is rewritten by the next refill
+    return hi;
+  }
+  return end;
+}
+
+// Insert a new pending column f (kk < f < hi) into the cache.
+__device__ __forceinline__ void cache_insert(int f, unsigned lane, const longlong2* brec,
+                                             int& cand, longlong2& rec, int& hi, bool& pf) {
+  if (f >= hi) return;
+  const unsigned freem = __ballot_sync(0xffffffffu, cand == kNone);
+  if (freem) {
+    if (static_cast<int>(lane) == __ffs(freem) - 1) {
+      cand = f;
+      rec = load_rec(brec, f);
+      pf = true;
+    }
+    return;
+  }
+  const int mx = __reduce_max_sync(0xffffffffu, cand);
+  if (mx > f) {  // full: the largest candidate leaves, hi drops to it
+    hi = mx;
+    if (cand == mx) {
+      cand = f;
+      rec = load_rec(brec, f);
+      pf = true;
+    }
+  } else {
+    hi = f;
+  }
+}
+
+// Slots of a round that hold entries (warp-uniform).
+__device__ __forceinline__ int batch_slots(int len, int base) {
+  return min(kIlutBatch, (len - base + 31) >> 5);
+}
+__device__ __forceinline__ void load_batch(const PoolView& pool, uint32_t s0, int len, int base,
+                                           unsigned lane, int (&jj)[kIlutBatch],
+                                           double (&uu)[kIlutBatch]) {
+  const int nr = batch_slots(len, base);
+#pragma unroll
+  for (int r = 0; r < kIlutBatch; ++r) {
+    const int q = base + static_cast<int>(lane) + 32 * r;
+    jj[r] = -1;
+    if (r < nr && q < len) {
+      jj[r] = pool.ucol[s0 + q];
+      uu[r] = pool.uval[s0 + q];
+    }
+  }
+}
+
+// Absent entries of the working row hold a NaN pattern no arithmetic
+// produces, so the update's own load tells whether an entry is new (the
+// reference's `present` flag, factorization.cpp:84-88) without an atomic
+// round trip; the bitmap (ascending scans) is kept exact by setting a bit
+// only when an entry appears.
+constexpr long long kAbsent = 0x7ff4a85a5e5a0001LL;
+__device__ __forceinline__ double absent_value() { return __longlong_as_double(kAbsent); }
+__device__ __forceinline__ bool is_absent(double v) { return __double_as_longlong(v) == kAbsent; }
+
 __global__ void __launch_bounds__(32) ilut_kernel(
     int nblocks, const int* __restrict__ blk_row0, const int* __restrict__ blk_dim,
     const int* __restrict__ blk_col0, const int* __restrict__ set_row0,
     const int* __restrict__ blk_ids, const int* __restrict__ a_rp,
     const int* __restrict__ a_ci, const double* __restrict__ a_v, double tol,
-    PoolView pool, int* block_counter, int dim_max) {
+    PoolView pool, longlong2* recs, int* block_counter, int dim_max) {
+  // The warp's shared memory is only the working row (dense fp64), its
+  // presence bitmap and a 32-entry scratch, so that 8 warps fit per SM;
+  // finished rows are read back through their 16-byte records and the pools
+  // (L1/L2), the records of upcoming pivots cached one per lane.
   extern __shared__ __align__(16) unsigned char smem[];
   double* work = reinterpret_cast<double*>(smem);
-  double* udg = work + dim_max;
-  uint32_t* ust = reinterpret_cast<uint32_t*>(udg + dim_max);
-  uint32_t* bits = ust + dim_max;
-  uint16_t* uln = reinterpret_cast<uint16_t*>(bits + ((dim_max + 31) / 32 + 1));
+  uint32_t* bits = reinterpret_cast<uint32_t*>(work + dim_max);
+  int* slot = reinterpret_cast<int*>(bits + ((dim_max + 31) / 32 + 1));
   const unsigned lane = lane_id();
   const unsigned ltmask = (1u << lane) - 1u;
 
-  for (int i = lane; i < dim_max; i += 32) work[i] = 0.0;
+  for (int i = lane; i < dim_max; i += 32) work[i] = absent_value();
   for (int i = lane; i < (dim_max + 31) / 32 + 1; i += 32) bits[i] = 0u;
   unsigned long long lcur = 0, lend = 0, ucur = 0, uend = 0;
   __syncwarp();
@@ -92,6 +215,7 @@ __global__ void __launch_bounds__(32) ilut_kernel(
     const int b = blk_ids[t];
     const int row0 = blk_row0[b], dim = blk_dim[b], col0 = blk_col0[b];
     const int srow0 = set_row0[b];
+    const longlong2* brec = recs + srow0;
     long long tot_l = 0, tot_u = 0;
     bool failed = false;
 
@@ -119,46 +243,107 @@ __global__ void __launch_bounds__(32) ilut_kernel(
       }
       __syncwarp();
 
-      // Pivot loop: ascending pending columns k < i.
-      int k = -1;
-      const int last_word = (i - 1) >> 5;
-      while (i > 0) {
-        const int start = k + 1;
-        if (start >= i) break;
-        int kk = -1;
-        for (int wb = start >> 5; wb <= last_word; wb += 32) {
-          const int w = wb + lane;
-          unsigned word = 0;
-          if (w <= last_word) {
-            word = bits[w];
-            if (w == (start >> 5)) word &= ~0u << (start & 31);
-            if (w == last_word && (i & 31)) word &= (1u << (i & 31)) - 1u;
-          }
-          const unsigned any = __ballot_sync(0xffffffffu, word != 0u);
-          if (any) {
-            const int f = __ffs(any) - 1;
-            const unsigned wf = __shfl_sync(0xffffffffu, word, f);
-            kk = ((wb + f) << 5) + (__ffs(wf) - 1);
-            break;
-          }
+      // Pivot loop over the pending columns k < i in ascending order: the
+      // next pivot is the smallest cached candidate (fills of each update
+      // are inserted), and the U row of the one after it is in flight while
+      // the current pivot's update runs.
+      int cand = kNone;
+      longlong2 rec = make_longlong2(0, 0);
+      bool pf = false;  // this lane's candidate row still to be prefetched
+      int hi = refill(bits, 0, i, lane, slot, brec, cand, rec, pf);
+      int kk = __reduce_min_sync(0xffffffffu, cand);
+      int jj[kIlutBatch], pj[kIlutBatch];
+      double uu[kIlutBatch], pu[kIlutBatch];
+      bool have = false;
+      while (kk != kNone) {
+        const int own = __ffs(__ballot_sync(0xffffffffu, cand == kk)) - 1;
+        const long long rx = __shfl_sync(0xffffffffu, rec.x, own);
+        const long long ry = __shfl_sync(0xffffffffu, rec.y, own);
+        if (static_cast<int>(lane) == own) {
+          cand = kNone;
+          pf = false;
         }
-        if (kk < 0) break;
-        const double m = __ddiv_rn(work[kk], udg[kk]);
+        const double ukk = __longlong_as_double(rx);
+        const uint32_t s0 = static_cast<uint32_t>(ry);
+        const int len = static_cast<int>(static_cast<unsigned long long>(ry) >> 32);
+        if (!have) load_batch(pool, s0, len, 0, lane, jj, uu);
+        // the next candidate's U row goes in flight now
+        const int k2 = __reduce_min_sync(0xffffffffu, cand);
+        if (k2 != kNone) {
+          const int own2 = __ffs(__ballot_sync(0xffffffffu, cand == k2)) - 1;
+          const long long ry2 = __shfl_sync(0xffffffffu, rec.y, own2);
+          load_batch(pool, static_cast<uint32_t>(ry2),
+                     static_cast<int>(static_cast<unsigned long long>(ry2) >> 32), 0, lane, pj, pu);
+        }
+        if (pf) {
+          prefetch_urow(pool, rec.y);
+          pf = false;
+        }
+        const double m = __ddiv_rn(work[kk], ukk);
         if (fabs(m) < tau || m == 0.0) {
           if (lane == 0) work[kk] = 0.0;
         } else {
           if (lane == 0) work[kk] = m;
-          const uint32_t s0 = ust[kk];
-          const int len = uln[kk];
-          for (int q = lane; q < len; q += 32) {
-            const int j = pool.ucol[s0 + q];
-            const double u = pool.uval[s0 + q];
-            work[j] = __dsub_rn(work[j], __dmul_rn(m, u));
-            atomicOr(&bits[j >> 5], 1u << (j & 31));
+          for (int base = 0;;) {
+            // next round's loads before this round's updates
+            const int nr = batch_slots(len, base);
+            const int nbase = base + 32 * kIlutBatch;
+            int nj[kIlutBatch];
+            double nu[kIlutBatch];
+            if (nbase < len) load_batch(pool, s0, len, nbase, lane, nj, nu);
+            double wv[kIlutBatch];
+#pragma unroll
+            for (int r = 0; r < kIlutBatch; ++r)
+              if (r < nr && jj[r] >= 0) wv[r] = work[jj[r]];
+            unsigned fills = 0;  // slots whose entry is new and a pending pivot below hi
+#pragma unroll
+            for (int r = 0; r < kIlutBatch; ++r) {
+              if (r < nr && jj[r] >= 0) {
+                const int j = jj[r];
+                const bool fresh = is_absent(wv[r]);
+                // a new entry starts at 0.0 (reference: work[j] = 0, then -=)
+                work[j] = __dsub_rn(fresh ? 0.0 : wv[r], __dmul_rn(m, uu[r]));
+                if (fresh) {
+                  atomicOr(&bits[j >> 5], 1u << (j & 31));
+                  if (j > kk && j < hi) fills |= 1u << r;
+                }
+              }
+            }
+            if (__any_sync(0xffffffffu, fills != 0)) {
+#pragma unroll
+              for (int r = 0; r < kIlutBatch; ++r) {
+                unsigned fm = __ballot_sync(0xffffffffu, (fills >> r) & 1u);
+                while (fm) {
+                  const int src = __ffs(fm) - 1;
+                  fm &= fm - 1;
+                  cache_insert(__shfl_sync(0xffffffffu, jj[r], src), lane, brec, cand, rec, hi, pf);
+                }
+              }
+            }
+            if (nbase >= len) break;
+            base = nbase;
+#pragma unroll
+            for (int r = 0; r < kIlutBatch; ++r) {
+              jj[r] = nj[r];
+              uu[r] = nu[r];
+            }
           }
         }
         __syncwarp();
-        k = kk;
+        int nxt = __reduce_min_sync(0xffffffffu, cand);
+        if (nxt == kNone && hi < i) {
+          hi = refill(bits, hi, i, lane, slot, brec, cand, rec, pf);
+          nxt = __reduce_min_sync(0xffffffffu, cand);
+        }
+        have = nxt == k2 && k2 != kNone;
+        if (have) {
+#pragma unroll
+          for (int r = 0; r < kIlutBatch; ++r) {
+            jj[r] = pj[r];
+            uu[r] = pu[r];
+          }
+        }
+        kk = nxt;
       }
 
       // Reserve pool space for the worst case of this row.
@@ -215,11 +400,10 @@ __global__ void __launch_bounds__(32) ilut_kernel(
           if (bd) diag = __shfl_sync(0xffffffffu, v, __ffs(bd) - 1);
           lpos += __popc(bl);
           upos += __popc(bu);
-          if (present) work[j] = 0.0;
+          if (present) work[j] = absent_value();
         }
         if (w < nwords) bits[w] = 0u;
       }
-      __syncwarp();
       const int nl = static_cast<int>(lpos - l0), nu = static_cast<int>(upos - u0);
       if (lane == 0) {
         lcur = lpos;
@@ -230,9 +414,9 @@ __global__ void __launch_bounds__(32) ilut_kernel(
         pool.ustart[g] = static_cast<uint32_t>(u0);
         pool.ulen[g] = nu;
         pool.udiag[g] = diag;
-        ust[i] = static_cast<uint32_t>(u0);
-        uln[i] = static_cast<uint16_t>(nu);
-        udg[i] = diag;
+        recs[g] = make_longlong2(__double_as_longlong(diag),
+                                 static_cast<long long>((static_cast<unsigned long long>(nu) << 32) |
+                                                        static_cast<uint32_t>(u0)));
       }
       tot_l += nl;
       tot_u += nu;
@@ -246,7 +430,7 @@ __global__ void __launch_bounds__(32) ilut_kernel(
     }
     if (failed) {
       // leave the shared work row clean for the next block
-      for (int i = lane; i < dim_max; i += 32) work[i] = 0.0;
+      for (int i = lane; i < dim_max; i += 32) work[i] = absent_value();
       for (int i = lane; i < (dim_max + 31) / 32 + 1; i += 32) bits[i] = 0u;
       __syncwarp();
     }
@@ -590,8 +774,8 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   const long long lb = loff[b], ub = uoff[b];
   const int nt = (n + kTile - 1) / kTile;
   const long long tb = toff[b];
-  double* lt = ltile + tb * kTileElems;
-  double* ut = utile + tb * kTileElems;
+  double* lt = ltile + tb * kTileStride;
+  double* ut = utile + tb * kTileStride;
   // Neighbour-window format per tile: ELL width (widest row) or dense.
   for (int t = threadIdx.x; t < nt; t += blockDim.x) {
     int ml = 0, mu = 0;
@@ -607,8 +791,8 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   // then U tiles descending); item q carries the copy size of item q + kRing.
   auto item_w = [&](int q) { return q < nt ? lwidth[tb + q] : uwidth[tb + 2 * nt - 1 - q]; };
   for (int q = threadIdx.x; q < 2 * nt; q += blockDim.x) {
-    double* T = q < nt ? lt + static_cast<long long>(q) * kTileElems
-                       : ut + static_cast<long long>(2 * nt - 1 - q) * kTileElems;
+    double* T = q < nt ? lt + static_cast<long long>(q) * kTileStride
+                       : ut + static_cast<long long>(2 * nt - 1 - q) * kTileStride;
     T[kHdr] = __longlong_as_double(item_w(q));
     T[kHdr + 1] = __longlong_as_double(
         q + kRing < 2 * nt ? 8LL * tile_elems(item_w(q + kRing)) : 0LL);
@@ -616,8 +800,8 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   for (int i = warp; i < nt * kTile; i += blockDim.x / 32) {
     const int t = i >> 5, j = i & 31;
     const bool row = i < n;
-    double* ltt = lt + static_cast<long long>(t) * kTileElems;
-    double* utt = ut + static_cast<long long>(t) * kTileElems;
+    double* ltt = lt + static_cast<long long>(t) * kTileStride;
+    double* utt = ut + static_cast<long long>(t) * kTileStride;
     const int wl = lwidth[tb + t], wu = uwidth[tb + t];
     if (lane == 0 && row) {
       const double rd = 1.0 / pool.udiag[r0 + i];
@@ -662,7 +846,7 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
             reinterpret_cast<unsigned char*>(ltt)[ell_colbyte(j, e)] = static_cast<unsigned char>(k);
           }
         } else if (in) {
-          ltt[kTriOff + tri_l(j, k - 2 * kTile)] = v;
+          ltt[kOrigOff + tri_l(j, k - 2 * kTile)] = v;
         }
         w += __popc(bf);
         e0 += __popc(bn);
@@ -696,10 +880,60 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
                 static_cast<unsigned char>(k - kTile);
           }
         } else if (in) {
-          utt[kTriOff + tri_u(j, k)] = v;
+          utt[kOrigOff + tri_u(j, k)] = v;
         }
         w += __popc(bf);
         e0 += __popc(bn);
+      }
+    }
+  }
+  // Inverses of the diagonal tiles (lane k builds column k by substitution
+  // on the tile's own triangle; rows past the block end have U_jj^-1 = 0).
+  __syncthreads();
+  for (int t = warp; t < nt; t += blockDim.x / 32) {
+    // (written by other threads of this CTA above: read through L2)
+    const double* lo = lt + static_cast<long long>(t) * kTileStride + kOrigOff;
+    const double* uo = ut + static_cast<long long>(t) * kTileStride + kOrigOff;
+    double* li = lt + static_cast<long long>(t) * kTileStride + kTriOff;
+    double* ui = ut + static_cast<long long>(t) * kTileStride + kTriOff;
+    const double* rdg = ut + static_cast<long long>(t) * kTileStride + kMetaDiag;
+    const int k = lane;
+    {  // column k of L_tt^-1: x_k = 1, x_j = -sum_{k<=m<j} L_jm x_m
+      double x[kTile];
+#pragma unroll
+      for (int q = 0; q < kTile; ++q) x[q] = 0.0;
+#pragma unroll
+      for (int jr = 0; jr < kTile; ++jr) {
+        if (jr < k) continue;
+        if (jr == k) {
+          x[jr] = 1.0;
+          continue;
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < kTile; ++m)
+          if (m >= k && m < jr) acc = fma(-__ldcg(lo + tri_l(jr, m)), x[m], acc);
+        x[jr] = acc;
+        li[tri_l(jr, k)] = acc;
+      }
+    }
+    {  // column k of U_tt^-1: x_k = 1/U_kk, x_j = -(sum_{j<m<=k} U_jm x_m) / U_jj
+      double x[kTile];
+#pragma unroll
+      for (int q = 0; q < kTile; ++q) x[q] = 0.0;
+#pragma unroll
+      for (int jr = kTile - 1; jr >= 0; --jr) {
+        if (jr > k) continue;
+        if (jr == k) {
+          x[jr] = __ldcg(rdg + k);
+          continue;
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < kTile; ++m)
+          if (m > jr && m <= k) acc = fma(-__ldcg(uo + tri_u(jr, m)), x[m], acc);
+        x[jr] = acc * __ldcg(rdg + jr);
+        ui[tri_u(jr, k)] = x[jr];
       }
     }
   }
@@ -775,12 +1009,16 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   fs->dim = upload_vec(fs->h_dim, s);
   std::vector<int> ilut_ids, lu_ids;
   for (int b = 0; b < nb; ++b) (exact[b] ? lu_ids : ilut_ids).push_back(b);
+  // largest blocks first, so the last wave holds the smallest (LPT)
+  std::stable_sort(ilut_ids.begin(), ilut_ids.end(),
+                   [&](int x, int y) { return blocks[x].dim > blocks[y].dim; });
   DevBuf d_ilut_ids = upload_vec(ilut_ids, s), d_lu_ids = upload_vec(lu_ids, s);
 
   // Per-row pool metadata and per-block totals.
   DevBuf lstart(sizeof(uint32_t) * total), llen(sizeof(int) * total);
   DevBuf ustart(sizeof(uint32_t) * total), ulen(sizeof(int) * total);
   fs->udiag = DevBuf(sizeof(double) * total);
+  DevBuf recs(sizeof(longlong2) * total);
   DevBuf nnzl(sizeof(long long) * nb), nnzu(sizeof(long long) * nb);
   DevBuf counters(64);
   if (fs->has_perm) {
@@ -810,7 +1048,7 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   int ilut_smem = 0;
   {
     const int words = (dmax + 31) / 32 + 1;
-    ilut_smem = dmax * 8 * 2 + dmax * 4 + words * 4 + dmax * 2 + 16;
+    ilut_smem = dmax * 8 + words * 4 + 32 * 4 + 16;
     ilut_smem = (ilut_smem + 15) & ~15;
   }
   int ilut_grid = 0;
@@ -869,7 +1107,7 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
       ilut_kernel<<<ilut_grid, 32, ilut_smem, s>>>(
           static_cast<int>(ilut_ids.size()), d_row0.as<int>(), fs->dim.as<int>(),
           d_col0.as<int>(), fs->row0.as<int>(), d_ilut_ids.as<int>(), a_rp, a_ci, a_v, tol,
-          pv, block_counter, dmax);
+          pv, recs.as<longlong2>(), block_counter, dmax);
       MSCG_CUDA(cudaGetLastError());
       ctx->launches++;
     }
@@ -967,7 +1205,7 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   fs->lcol = DevBuf(sizeof(uint16_t) * std::max<long long>(1, fs->far_l()));
   fs->uval = DevBuf(sizeof(double) * std::max<long long>(1, fs->far_u()));
   fs->ucol = DevBuf(sizeof(uint16_t) * std::max<long long>(1, fs->far_u()));
-  const size_t tile_bytes = sizeof(double) * kTileElems * std::max<long long>(1, fs->tiles());
+  const size_t tile_bytes = sizeof(double) * kTileStride * std::max<long long>(1, fs->tiles());
   fs->ltile = DevBuf(tile_bytes);
   fs->utile = DevBuf(tile_bytes);
   fs->urdiag = DevBuf(sizeof(double) * total);
@@ -1039,7 +1277,7 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
   const long long lb = fs.h_loff[idx], le = fs.h_loff[idx + 1];
   const long long ub = fs.h_uoff[idx], ue = fs.h_uoff[idx + 1];
   const long long t0 = fs.h_toff[idx], nt = fs.h_toff[idx + 1] - t0;
-  const size_t tsz = kTileElems;
+  const size_t tsz = kTileStride;
   std::vector<int> hlr(n + 1), hur(n + 1);
   std::vector<uint16_t> hlc(le - lb), huc(ue - ub);
   std::vector<double> hlv(le - lb), huv(ue - ub), hd(n), hlt(tsz * nt), hut(tsz * nt);
@@ -1094,7 +1332,7 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
       }
     });
     for (int k = 0; k < j; ++k) {
-      const double v = LT[kTriOff + tri_l(j, k)];
+      const double v = LT[kOrigOff + tri_l(j, k)];
       if (v != 0.0) {
         lci.push_back(t * kTile + k);
         lv.push_back(v);
@@ -1104,7 +1342,7 @@ void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
     uci.push_back(i);
     uv.push_back(hd[i]);
     for (int k = j + 1; k < kTile; ++k) {
-      const double v = UT[kTriOff + tri_u(j, k)];
+      const double v = UT[kOrigOff + tri_u(j, k)];
       if (t * kTile + k < n && v != 0.0) {
         uci.push_back(t * kTile + k);
         uv.push_back(v);

@@ -82,8 +82,10 @@ constexpr int kNearTiles = 3;
 //  * header: [kHdr] = ELL width W of this tile (or kDenseNbr), [kHdr + 1] =
 //    bytes of the near item the solver issues kRing items later (the tile
 //    stream carries its own copy sizes);
-//  * the strictly triangular part of the diagonal tile packed by column
-//    (tri_l / tri_u);
+//  * the strictly triangular part of the INVERSE of the diagonal tile packed
+//    by column (tri_l / tri_u): L_tt^-1 is unit lower triangular, U_tt^-1
+//    upper triangular with diagonal 1 / U_jj (the metadata), so the tile's
+//    32-step substitution chain becomes one 32-term dot product per row;
 //  * the two neighbour tiles (L: t-2, t-1; U: t+1, t+2), as a 64-column
 //    window, either
 //      - ELL (W entries per row, W a multiple of 4, rows padded with zero
@@ -93,6 +95,9 @@ constexpr int kNearTiles = 3;
 //      - dense (kDenseNbr, when ELL would not be smaller): 32 x 64
 //        column-major, entry [k*32 + j].
 // Only the used prefix of a tile is copied (kNbrOff + 36 W doubles for ELL).
+// Past the largest copy (kTileElems) each slot keeps the diagonal tile's own
+// strictly triangular part (kOrigOff, same packing), never read by the solve,
+// from which the reference factors are recovered exactly.
 constexpr int kMetaDiag = 0;
 constexpr int kMetaSeg = kTile;
 constexpr int kHdr = 2 * kTile;
@@ -104,6 +109,8 @@ __host__ __device__ constexpr int tri_u(int j, int k) { return k * (k - 1) / 2 +
 constexpr int kNbrOff = kTriOff + kTriElems;
 constexpr int kNbrElems = 2 * kTile * kTile;
 constexpr int kTileElems = kNbrOff + kNbrElems;
+constexpr int kOrigOff = kTileElems;
+constexpr int kTileStride = kOrigOff + kTriElems;
 constexpr int kDenseNbr = -1;
 constexpr int kEllMax = ((kNbrElems / 36) / 4) * 4;  // widest ELL smaller than dense (56)
 __host__ __device__ constexpr int ell_width(int maxrow) {
@@ -160,7 +167,7 @@ struct FactorSet {
   DevBuf lrp, urp;                         // int32[total_rows + nblocks]
   DevBuf lval, uval;                       // fp64 (far entries)
   DevBuf lcol, ucol;                       // uint16
-  DevBuf ltile, utile;                     // fp64 [tiles][kTileElems] (used prefix varies)
+  DevBuf ltile, utile;                     // fp64 [tiles][kTileStride] (copied prefix varies)
   DevBuf lwidth, uwidth;                   // int32[tiles]: ELL width or kDenseNbr
   std::vector<int> h_lwidth, h_uwidth;
   std::vector<int64_t> h_lioff, h_uioff;   // per block far work-item offsets (+1)

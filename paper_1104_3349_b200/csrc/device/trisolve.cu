@@ -304,6 +304,8 @@ __device__ __forceinline__ double ell_neighbours(const double* T, int w, int j,
   const uint32_t* cw = reinterpret_cast<const uint32_t*>(T + kNbrOff);
   const double2* vv = reinterpret_cast<const double2*>(T + kNbrOff + 4 * w);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  // unrolled so that several rounds of shared loads are in flight
+#pragma unroll 4
   for (int e4 = 0; e4 < (w >> 2); ++e4) {
     const uint32_t c = cw[e4 * kTile + j];
     const double2 p = vv[(2 * e4) * kTile + j], q = vv[(2 * e4 + 1) * kTile + j];
@@ -311,6 +313,31 @@ __device__ __forceinline__ double ell_neighbours(const double* T, int w, int j,
     a1 = fma(p.y, win[(c >> 8) & 0xff], a1);
     a2 = fma(q.x, win[(c >> 16) & 0xff], a2);
     a3 = fma(q.y, win[c >> 24], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// Row j of the diagonal tile's inverse times the tile's residuals r (shared,
+// read as broadcast 16-byte loads): L: z_j = r_j + sum_{k<j} Linv_jk r_k;
+// U: x_j = r_j / U_jj + sum_{k>j} Uinv_jk r_k.  Four partial sums in a fixed
+// order (deterministic).
+template <bool kLower>
+__device__ __forceinline__ double tile_inverse_dot(const double* T, const double* r, int j) {
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  double a0 = kLower ? r[j] : r[j] * T[kMetaDiag + j], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int k = 0; k < kTile; k += 4) {
+    const double2 p = r2[k / 2], q = r2[k / 2 + 1];
+    const bool i0 = kLower ? k < j : k > j, i1 = kLower ? k + 1 < j : k + 1 > j;
+    const bool i2 = kLower ? k + 2 < j : k + 2 > j, i3 = kLower ? k + 3 < j : k + 3 > j;
+    const double c0 = i0 ? T[kTriOff + (kLower ? tri_l(j, k) : tri_u(j, k))] : 0.0;
+    const double c1 = i1 ? T[kTriOff + (kLower ? tri_l(j, k + 1) : tri_u(j, k + 1))] : 0.0;
+    const double c2 = i2 ? T[kTriOff + (kLower ? tri_l(j, k + 2) : tri_u(j, k + 2))] : 0.0;
+    const double c3 = i3 ? T[kTriOff + (kLower ? tri_l(j, k + 3) : tri_u(j, k + 3))] : 0.0;
+    a0 = fma(c0, p.x, a0);
+    a1 = fma(c1, p.y, a1);
+    a2 = fma(c2, q.x, a2);
+    a3 = fma(c3, q.y, a3);
   }
   return (a0 + a1) + (a2 + a3);
 }
@@ -370,6 +397,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int dpad = (a.dim_max + kTile - 1) & ~(kTile - 1);
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
+  double* rbuf = scratch + kWorkers * kGroupEntries;  // solver: the tile's residuals
   __shared__ __align__(8) uint64_t bars[kRing];
   __shared__ int done_l, done_u;
   __shared__ int cnt[kPR];    // far items published per ring tile
@@ -377,8 +405,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int b = a.order[a.pos0 + blockIdx.x];  // heaviest blocks first (LPT)
   const int n = a.dim[b], r0 = a.row0[b];
   const int nt = (n + kTile - 1) / kTile;
-  const double* lt = a.ltile + a.toff[b] * kTileElems;
-  const double* ut = a.utile + a.toff[b] * kTileElems;
+  const double* lt = a.ltile + a.toff[b] * kTileStride;
+  const double* ut = a.utile + a.toff[b] * kTileStride;
   const double pend = pending_value();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -407,7 +435,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     double* dst = ring + slot * kSlotElems;
     const bool lpass = q < nt;
     const int t = lpass ? q : 2 * nt - 1 - q;
-    const double* tile = (lpass ? lt : ut) + static_cast<long long>(t) * kTileElems;
+    const double* tile = (lpass ? lt : ut) + static_cast<long long>(t) * kTileStride;
     Slice sr{nullptr, 0, 0};
     if (lpass && !pm) sr = aligned_slice(rhs + r0 + t * kTile, min(kTile, n - t * kTile));
     mbar_expect_tx(&bars[slot], bytes + sr.bytes);
@@ -474,16 +502,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 1] = clock64();
-      // acc = b_i - (known sums); z_k = acc_k once step k is reached
-      double acc = bi - (nb + far);
-      double zj = 0.0;
-#pragma unroll
-      for (int k = 0; k < kTile; ++k) {
-        const double zk = __shfl_sync(0xffffffffu, acc, k);
-        if (j == k) zj = zk;
-        if (j > k) acc = fma(-T[kTriOff + tri_l(j, k)], zk, acc);
-      }
-      if (!valid) zj = 0.0;
+      // z_t = L_tt^-1 r with r = b - (known sums): one dot product per row
+      // over the tile's residuals instead of a 32-step substitution chain
+      rbuf[j] = bi - (nb + far);
+      __syncwarp();
+      double zj = valid ? tile_inverse_dot<true>(T, rbuf, j) : 0.0;
+      __syncwarp();  // rbuf is rewritten by the next tile
       if (valid) *reinterpret_cast<volatile double*>(z + i) = zj;
       __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
@@ -569,7 +593,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       mbar_wait(&bars[slot], (q / kRing) & 1);
       if (tr && lane == 0) tr[4 * q + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
-      const double rd = valid ? T[kMetaDiag + j] : 0.0;
       const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
       const int wn = meta_int(T, kHdr);
       double nb = 0.0;
@@ -583,15 +606,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 1] = clock64();
-      double acc = zi - (nb + far);
-      double xj = 0.0;
-#pragma unroll
-      for (int k = kTile - 1; k >= 0; --k) {
-        const double xk = __shfl_sync(0xffffffffu, acc * rd, k);
-        if (j == k) xj = xk;
-        if (j < k) acc = fma(-T[kTriOff + tri_u(j, k)], xk, acc);
-      }
-      if (!valid) xj = 0.0;
+      // x_t = U_tt^-1 r with r = z - (known sums)
+      rbuf[j] = zi - (nb + far);
+      __syncwarp();
+      double xj = valid ? tile_inverse_dot<false>(T, rbuf, j) : 0.0;
+      __syncwarp();
       if (valid) *reinterpret_cast<volatile double*>(x + i) = xj;
       __syncwarp();
       if (lane == 0) {
@@ -678,7 +697,7 @@ size_t smem_bytes(int dim_max, int workers) {
   const size_t dpad = (static_cast<size_t>(dim_max) + kTile - 1) & ~static_cast<size_t>(kTile - 1);
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
                            static_cast<size_t>(kPR) * kPartTile + (kInPlace ? 1 : 2) * dpad +
-                           static_cast<size_t>(workers) * kGroupEntries);
+                           static_cast<size_t>(workers) * kGroupEntries + kTile);
 }
 
 }  // namespace
