@@ -708,33 +708,43 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
     double* __restrict__ urdiag, const long long* __restrict__ lioff,
     const long long* __restrict__ uioff, int4* __restrict__ litems, int4* __restrict__ uitems,
     int* __restrict__ lnum, int* __restrict__ unum, const int* __restrict__ lnb,
-    const int* __restrict__ unb, int* __restrict__ lwidth, int* __restrict__ uwidth) {
+    const int* __restrict__ unb, int* __restrict__ lwidth, int* __restrict__ uwidth,
+    int* __restrict__ lslot, int* __restrict__ uslot, int* __restrict__ nslots,
+    int4* __restrict__ ltmp, int4* __restrict__ utmp) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   int* lr = lrp + r0 + b;
   int* ur = urp + r0 + b;
   if (threadIdx.x == 0) {
-    int sl = 0, su = 0;
+    int sl = 0, su = 0, ql = 0, qu = 0;
     for (int i = 0; i < n; ++i) {
       lr[i] = sl;
       ur[i] = su;
       sl += lcnt[r0 + i];
       su += ucnt[r0 + i];
+      // far-sum slots of the row's work items (one per segment)
+      lslot[r0 + i] = ql;
+      uslot[r0 + i] = qu;
+      ql += far_segments(lcnt[r0 + i]);
+      qu += far_segments(ucnt[r0 + i]);
     }
     lr[n] = sl;
     ur[n] = su;
+    nslots[b] = max(ql, qu);
     // Work items in solve order (entry offsets within the block).  Long rows:
     // {row, segment, begin, end}, kSeg entries per segment.  Runs of short
     // rows of one tile: one multi-row item (see kShortRow).
-    auto build = [&](int4* out, const int* rp, const int* cnt, bool asc) {
+    // x = row | first far-sum slot << 16.
+    auto build = [&](int4* out, const int* rp, const int* cnt, const int* slot, bool asc) {
       int4* o = out;
       int g0 = -1, g1 = -1, gent = 0;  // open group: rows [g0, g1], entries
       auto close = [&]() {
         if (g0 < 0) return;
+        const int x = g0 | (slot[r0 + g0] << 16);
         if (g0 == g1)
-          *o++ = make_int4(g0, 0, rp[g0], rp[g0 + 1]);
+          *o++ = make_int4(x, 0, rp[g0], rp[g0 + 1]);
         else
-          *o++ = make_int4(g0, kMultiFlag | (g1 - g0), rp[g0], rp[g1 + 1]);
+          *o++ = make_int4(x, kMultiFlag | (g1 - g0), rp[g0], rp[g1 + 1]);
         g0 = g1 = -1;
         gent = 0;
       };
@@ -759,14 +769,15 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
         const int ns = far_segments(c);
         for (int q = 0; q < ns; ++q) {
           const int b0 = rp[i] + q * kSeg;
-          *o++ = make_int4(i, q, b0, q == ns - 1 ? rp[i] + c : b0 + kSeg);
+          *o++ = make_int4(i | ((slot[r0 + i] + q) << 16), q, b0,
+                           q == ns - 1 ? rp[i] + c : b0 + kSeg);
         }
       }
       close();
       return static_cast<int>(o - out);
     };
-    lnum[b] = build(litems + lioff[b], lr, lcnt, true);
-    unum[b] = build(uitems + uioff[b], ur, ucnt, false);
+    lnum[b] = build(litems + lioff[b], lr, lcnt, lslot, true);
+    unum[b] = build(uitems + uioff[b], ur, ucnt, uslot, false);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -808,8 +819,10 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
       urdiag[r0 + i] = rd;
       // tile metadata for the solver (see kMetaDiag / kMetaSeg)
       utt[kMetaDiag + j] = rd;
-      ltt[kMetaSeg + j] = __longlong_as_double(far_segments(lcnt[r0 + i]));
-      utt[kMetaSeg + j] = __longlong_as_double(far_segments(ucnt[r0 + i]));
+      ltt[kMetaSeg + j] =
+          __longlong_as_double(far_segments(lcnt[r0 + i]) | (static_cast<long long>(lslot[r0 + i]) << 8));
+      utt[kMetaSeg + j] =
+          __longlong_as_double(far_segments(ucnt[r0 + i]) | (static_cast<long long>(uslot[r0 + i]) << 8));
     }
     // window padding: every ELL slot past the row's entries reads a solved slot
     if (wl != kDenseNbr)
@@ -943,22 +956,47 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   __syncthreads();
   for (long long q = lioff[b] + threadIdx.x; q < lioff[b] + lnum[b]; q += blockDim.x) {
     int4 d = litems[q];
+    const int r = d.x & 0xffff;
     int c = lcol[lb + d.w - 1];
     if (d.y & kMultiFlag)  // highest column over the group's rows
-      for (int i = d.x; i <= d.x + (d.y & 0x7f); ++i)
+      for (int i = r; i <= r + (d.y & 0x7f); ++i)
         if (lr[i + 1] > lr[i]) c = max(c, static_cast<int>(lcol[lb + lr[i + 1] - 1]));
     d.y = (d.y & 0xff) | (((c >> 5) + 1) << 8);
     litems[q] = d;
   }
   for (long long q = uioff[b] + threadIdx.x; q < uioff[b] + unum[b]; q += blockDim.x) {
     int4 d = uitems[q];
+    const int r = d.x & 0xffff;
     int c = ucol[ub + d.z];
     if (d.y & kMultiFlag)  // lowest column over the group's rows
-      for (int i = d.x; i <= d.x + (d.y & 0x7f); ++i)
+      for (int i = r; i <= r + (d.y & 0x7f); ++i)
         if (ur[i + 1] > ur[i]) c = min(c, static_cast<int>(ucol[ub + ur[i]]));
     d.y = (d.y & 0xff) | ((nt - (c >> 5)) << 8);
     uitems[q] = d;
   }
+  // Workers take items in order of readiness (stable counting sort by need):
+  // an item whose inputs are final never waits behind one whose are not, so
+  // the far entries of late rows stream while the chain is still early.
+  // Each item writes its own far-sum slot, so the sums stay deterministic.
+  __syncthreads();
+  __shared__ int hist[2][kMaxNeed + 2];
+  auto sort_items = [&](int4* items, int4* tmp, int cnt, int* h) {
+    for (int k = threadIdx.x; k < kMaxNeed + 2; k += blockDim.x) h[k] = 0;
+    __syncthreads();
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+      tmp[q] = items[q];
+      atomicAdd(&h[(items[q].y >> 8) + 1], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 1; k < kMaxNeed + 2; ++k) h[k] += h[k - 1];
+    __syncthreads();
+    if (threadIdx.x == 0)  // stable scatter
+      for (int q = 0; q < cnt; ++q) items[h[tmp[q].y >> 8]++] = tmp[q];
+    __syncthreads();
+  };
+  sort_items(litems + lioff[b], ltmp + lioff[b], lnum[b], hist[0]);
+  sort_items(uitems + uioff[b], utmp + uioff[b], unum[b], hist[1]);
 }
 
 template <class T>
@@ -1211,6 +1249,11 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   fs->urdiag = DevBuf(sizeof(double) * total);
   fs->lwidth = DevBuf(sizeof(int) * std::max<long long>(1, fs->tiles()));
   fs->uwidth = DevBuf(sizeof(int) * std::max<long long>(1, fs->tiles()));
+  fs->lslot = DevBuf(sizeof(int) * std::max(1, total));
+  fs->uslot = DevBuf(sizeof(int) * std::max(1, total));
+  DevBuf nslots(sizeof(int) * std::max(1, nb));
+  DevBuf ltmp(sizeof(int4) * std::max<long long>(1, fs->h_lioff[nb]));
+  DevBuf utmp(sizeof(int4) * std::max<long long>(1, fs->h_uioff[nb]));
   MSCG_CUDA(cudaMemsetAsync(fs->ltile.p, 0, tile_bytes, s));
   MSCG_CUDA(cudaMemsetAsync(fs->utile.p, 0, tile_bytes, s));
   pack_tiled_kernel<<<nb, 256, 0, s>>>(
@@ -1221,9 +1264,16 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
       fs->utile.as<double>(), fs->urdiag.as<double>(), fs->lioff.as<long long>(),
       fs->uioff.as<long long>(), fs->litems.as<int4>(), fs->uitems.as<int4>(),
       fs->lnum.as<int>(), fs->unum.as<int>(), lnb.as<int>(), unb.as<int>(),
-      fs->lwidth.as<int>(), fs->uwidth.as<int>());
+      fs->lwidth.as<int>(), fs->uwidth.as<int>(), fs->lslot.as<int>(), fs->uslot.as<int>(),
+      nslots.as<int>(), ltmp.as<int4>(), utmp.as<int4>());
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
+  {
+    std::vector<int> hs(std::max(1, nb));
+    MSCG_CUDA(cudaMemcpyAsync(hs.data(), nslots.p, sizeof(int) * hs.size(), cudaMemcpyDeviceToHost, s));
+    MSCG_CUDA(cudaStreamSynchronize(s));
+    fs->max_slots = nb ? *std::max_element(hs.begin(), hs.end()) : 0;
+  }
   fs->h_lwidth.resize(fs->tiles());
   fs->h_uwidth.resize(fs->tiles());
   if (fs->tiles()) {

@@ -147,6 +147,7 @@ constexpr int kGroupEntries = 128;
 constexpr int kMultiFlag = 0x80;
 constexpr int kSeg = 512;
 constexpr int kMaxSeg = 4;
+constexpr int kMaxNeed = 65536 / kTile;  // readiness counts are tiles of a block
 __host__ __device__ inline int far_segments(int nfar) {
   const int s = (nfar + kSeg - 1) / kSeg;
   return s < kMaxSeg ? s : kMaxSeg;
@@ -169,6 +170,10 @@ struct FactorSet {
   DevBuf lcol, ucol;                       // uint16
   DevBuf ltile, utile;                     // fp64 [tiles][kTileStride] (copied prefix varies)
   DevBuf lwidth, uwidth;                   // int32[tiles]: ELL width or kDenseNbr
+  // Far sums: every work item writes its own slot (per block and pass; a
+  // row's slots are consecutive from lslot/uslot[row]), max_slots per block.
+  DevBuf lslot, uslot;                     // int32[total_rows]
+  int max_slots = 0;
   std::vector<int> h_lwidth, h_uwidth;
   std::vector<int64_t> h_lioff, h_uioff;   // per block far work-item offsets (+1)
   DevBuf lioff, uioff;                     // int64[nblocks+1] (capacity)

@@ -38,6 +38,7 @@
 //    epilogue.
 // Rounding differs from the reference's sequential row sums by ~1e-16
 // relative, far inside the 1e-10 apply bar.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -47,7 +48,6 @@ namespace mscg {
 
 namespace {
 
-constexpr int kPartTile = kTile * kMaxSeg;
 constexpr int kVecElems = 40;          // rhs slice: 32 + alignment slack
 constexpr int kSlotElems = kTileElems + kVecElems;
 
@@ -73,6 +73,9 @@ struct TriArgs {
   const int* unum;
   const int* lrp;      // far-entry row offsets, row0[b] + b + i
   const int* urp;
+  const int* lslot;    // first far-sum slot of each row, row0[b] + i
+  const int* uslot;
+  int max_slots;       // far-sum slots per block (shared memory)
   const int* perm;  // nullable (Schur blocks)
   const int* order; // launch order of the blocks
   int pos0;          // first launch-order position of this launch
@@ -342,21 +345,6 @@ __device__ __forceinline__ double tile_inverse_dot(const double* T, const double
   return (a0 + a1) + (a2 + a3);
 }
 
-// Solver: wait until `expected` far items of the tile were published, then
-// reset the counter for the ring tile's next use.  All lanes poll the same
-// word, so the exit is warp-uniform and the chain that follows keeps the
-// shuffles' converged fast path.
-__device__ __forceinline__ void wait_items(int* counter, int expected, int lane) {
-  if (expected > 0) {
-    int spins = 0;
-    while (vload(counter) < expected)
-      if (++spins > 8) __nanosleep(20);
-    __syncwarp();
-    if (lane == 0) *reinterpret_cast<volatile int*>(counter) = 0;
-  }
-  __syncwarp();
-}
-
 // Sum of the published far partial sums of one row, in item order, resetting
 // the slots.  Warp-uniform trip count (max over the lanes' item counts).
 __device__ __forceinline__ double take_far(double* slots, int nseg, double pend) {
@@ -380,11 +368,11 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
   return static_cast<int>(__double_as_longlong(T[idx]));
 }
 
-// kPR: depth (tiles) of the far-sum ring.  kInPlace: x overwrites z slot by
-// slot (one solution vector in shared memory instead of two).  kProducer:
+// kInPlace: x overwrites z slot by slot (one solution vector in shared memory
+// instead of two).  kProducer:
 // warp 1 issues the near-tile copies (the solver's issue of a bulk copy costs
 // ~400 cycles of its chain per tile) and warps 2.. are the workers.
-template <int kWarps, int kUnroll, int kMinBlocks, int kPR, bool kInPlace, bool kProducer>
+template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
@@ -392,15 +380,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   constexpr int kWorkers = kWarps - kFirstWorker;
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                        // kRing slots: tile | meta | rhs slice
-  double* part = ring + kRing * kSlotElems; // [kPR][32 rows][kMaxSeg]
-  double* z = part + kPR * kPartTile;       // L output
+  double* part = ring + kRing * kSlotElems; // far sums, one slot per work item
+  double* z = part + ((a.max_slots + 1) & ~1);  // L output
   const int dpad = (a.dim_max + kTile - 1) & ~(kTile - 1);
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
   double* rbuf = scratch + kWorkers * kGroupEntries;  // solver: the tile's residuals
   __shared__ __align__(8) uint64_t bars[kRing];
   __shared__ int done_l, done_u;
-  __shared__ int cnt[kPR];    // far items published per ring tile
 
   const int b = a.order[a.pos0 + blockIdx.x];  // heaviest blocks first (LPT)
   const int n = a.dim[b], r0 = a.row0[b];
@@ -415,11 +402,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     z[i] = i < n ? pend : 0.0;
     if (!kInPlace) x[i] = i < n ? pend : 0.0;
   }
-  for (int i = threadIdx.x; i < kPR * kPartTile; i += blockDim.x) part[i] = pend;
+  for (int i = threadIdx.x; i < a.max_slots; i += blockDim.x) part[i] = pend;
   if (threadIdx.x == 0) {
     done_l = 0;
     done_u = 0;
-    for (int r = 0; r < kPR; ++r) cnt[r] = 0;
     for (int r = 0; r < kRing; ++r) mbar_init(&bars[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -489,7 +475,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double* T = ring + slot * kSlotElems;
       const int off = static_cast<int>((reinterpret_cast<unsigned long long>(rhs + r0 + t * kTile) & 15) >> 3);
       const double bi = valid ? (pm ? bperm : T[kTileElems + off + j]) : 0.0;
-      const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
+      const int fm = valid ? meta_int(T, kMetaSeg + j) : 0;  // items | first slot << 8
       const int wn = meta_int(T, kHdr);
       double nb = 0.0;
       if (wn == kDenseNbr) {
@@ -498,8 +484,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       } else {
         nb = ell_neighbours(T, wn, j, z + (t - 2) * kTile);
       }
-      wait_items(&cnt[t % kPR], __reduce_add_sync(0xffffffffu, nseg), lane);
-      const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
+      const double far = take_far(part + (fm >> 8), fm & 0xff, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 1] = clock64();
       // z_t = L_tt^-1 r with r = b - (known sums): one dot product per row
@@ -541,37 +526,24 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int4 f = items[it + kWorkers * a.pf_items];
         prefetch_far(fv, fc, f.z, f.w);
       }
-      const int i = d.x, k = d.y & 0xff;
-      const int t = i / kTile;
+      const int i = d.x & 0xffff, k = d.y & 0xff;
+      const int slot = static_cast<int>(static_cast<unsigned>(d.x) >> 16);
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * it : nullptr;
       if (rt) rt[0] = clock64();
       if (k & kMultiFlag) {
+        const int span = (k & 0x7f) + 1;
+        const int my = lane < span ? a.lslot[r0 + i + lane] : 0;
         bool has;
         const double acc =
-            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, z, scr, lane,
-                                      a.sleep_ns, &done_l, d.y >> 8, a.sleep_max, has);
+            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, span, z, scr, lane,
+                                                 a.sleep_ns, &done_l, d.y >> 8, a.sleep_max, has);
         if (rt) rt[1] = clock64();
-        for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPR - 1);
-             sl = min(2 * sl, a.sleep_max))
-          __nanosleep(sl);
-        if (has)
-          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
-                                              ((i + lane) % kTile) * kMaxSeg) = acc;
-        const int np = __popc(__ballot_sync(0xffffffffu, has));
-        if (lane == 0) atomicAdd(&cnt[t % kPR], np);
+        if (has) *reinterpret_cast<volatile double*>(part + my) = acc;
       } else {
         const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, z, lane, a.sleep_ns,
                                                    &done_l, d.y >> 8, a.sleep_max);
         if (rt) rt[1] = clock64();
-        if (lane == 0) {
-          // ring slot of tile t is free once tile t - kPR was consumed
-          for (unsigned sl = a.sleep_ns; vload(&done_l) < t - (kPR - 1);
-               sl = min(2 * sl, a.sleep_max))
-            __nanosleep(sl);
-          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
-                                              (i % kTile) * kMaxSeg + k) = acc;
-          atomicAdd(&cnt[t % kPR], 1);
-        }
+        if (lane == 0) *reinterpret_cast<volatile double*>(part + slot) = acc;
       }
       if (rt) {
         rt[2] = clock64();
@@ -579,7 +551,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       }
     }
   }
-  __syncthreads();  // every L far sum consumed before U sums reuse the ring
+  __syncthreads();  // every L far sum consumed (slots pending again) before the U pass
 
   // ================================================================ U pass
   if (warp == 0) {
@@ -593,7 +565,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       mbar_wait(&bars[slot], (q / kRing) & 1);
       if (tr && lane == 0) tr[4 * q + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
-      const int nseg = valid ? meta_int(T, kMetaSeg + j) : 0;
+      const int fm = valid ? meta_int(T, kMetaSeg + j) : 0;
       const int wn = meta_int(T, kHdr);
       double nb = 0.0;
       if (wn == kDenseNbr) {
@@ -602,8 +574,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       } else {
         nb = ell_neighbours(T, wn, j, x + (t + 1) * kTile);
       }
-      wait_items(&cnt[t % kPR], __reduce_add_sync(0xffffffffu, nseg), lane);
-      const double far = take_far(part + (t % kPR) * kPartTile + j * kMaxSeg, nseg, pend);
+      const double far = take_far(part + (fm >> 8), fm & 0xff, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 1] = clock64();
       // x_t = U_tt^-1 r with r = z - (known sums)
@@ -648,37 +619,24 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int4 f = items[it + kWorkers * a.pf_u];
         prefetch_far(fv, fc, f.z, f.w);
       }
-      const int i = d.x, k = d.y & 0xff;
-      const int t = i / kTile;
-      const int pos = nt - 1 - t;
+      const int i = d.x & 0xffff, k = d.y & 0xff;
+      const int slot = static_cast<int>(static_cast<unsigned>(d.x) >> 16);
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * (lit + it) : nullptr;
       if (rt) rt[0] = clock64();
       if (k & kMultiFlag) {
+        const int span = (k & 0x7f) + 1;
+        const int my = lane < span ? a.uslot[r0 + i + lane] : 0;
         bool has;
         const double acc =
-            group_dot<kGroupEntries / 32, kInPlace>(fv, fc, d.z, d.w, rp, i, (k & 0x7f) + 1, x, scr, lane,
-                                         a.sleep_ns, &done_u, d.y >> 8, a.sleep_max, has);
+            group_dot<kGroupEntries / 32, kInPlace>(fv, fc, d.z, d.w, rp, i, span, x, scr, lane,
+                                                    a.sleep_ns, &done_u, d.y >> 8, a.sleep_max, has);
         if (rt) rt[1] = clock64();
-        for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPR - 1);
-             sl = min(2 * sl, a.sleep_max))
-          __nanosleep(sl);
-        if (has)
-          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
-                                              ((i + lane) % kTile) * kMaxSeg) = acc;
-        const int np = __popc(__ballot_sync(0xffffffffu, has));
-        if (lane == 0) atomicAdd(&cnt[t % kPR], np);
+        if (has) *reinterpret_cast<volatile double*>(part + my) = acc;
       } else {
         const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, x, lane, a.sleep_ns,
                                                       &done_u, d.y >> 8, a.sleep_max);
         if (rt) rt[1] = clock64();
-        if (lane == 0) {
-          for (unsigned sl = a.sleep_ns; vload(&done_u) < pos - (kPR - 1);
-               sl = min(2 * sl, a.sleep_max))
-            __nanosleep(sl);
-          *reinterpret_cast<volatile double*>(part + (t % kPR) * kPartTile +
-                                              (i % kTile) * kMaxSeg + k) = acc;
-          atomicAdd(&cnt[t % kPR], 1);
-        }
+        if (lane == 0) *reinterpret_cast<volatile double*>(part + slot) = acc;
       }
       if (rt) {
         rt[2] = clock64();
@@ -692,11 +650,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     out[r0 + i] = sub ? sub[r0 + i] - x[i] : x[i];
 }
 
-template <int kPR, bool kInPlace>
-size_t smem_bytes(int dim_max, int workers) {
+template <bool kInPlace>
+size_t smem_bytes(int dim_max, int workers, int slots) {
   const size_t dpad = (static_cast<size_t>(dim_max) + kTile - 1) & ~static_cast<size_t>(kTile - 1);
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
-                           static_cast<size_t>(kPR) * kPartTile + (kInPlace ? 1 : 2) * dpad +
+                           ((static_cast<size_t>(slots) + 1) & ~static_cast<size_t>(1)) +
+                           (kInPlace ? 1 : 2) * dpad +
                            static_cast<size_t>(workers) * kGroupEntries + kTile);
 }
 
@@ -730,6 +689,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.unum = fs.unum.as<int>();
   a.lrp = fs.lrp.as<int>();
   a.urp = fs.urp.as<int>();
+  a.lslot = fs.lslot.as<int>();
+  a.uslot = fs.uslot.as<int>();
+  a.max_slots = fs.max_slots;
   a.perm = fs.has_perm ? fs.perm.as<int>() : nullptr;
   a.order = fs.order.as<int>();
   a.pos0 = pos0;
@@ -766,24 +728,28 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     if (smem > 48 * 1024)
       MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
+    static const bool verbose = getenv("MSCG_VERBOSE") != nullptr;
+    if (verbose)
+      fprintf(stderr, "block_trisolve: %d blocks, dim_max %d, far-sum slots %d, smem %zu B\n",
+              npos, fs.max_dim, fs.max_slots, smem);
     kern<<<npos, warps * 32, smem, s>>>(a, rhs, out, sub);
   };
-  const int d = fs.max_dim;
+  const int d = fs.max_dim, ns = fs.max_slots;
   switch (variant) {
-    case 1:  // 3 CTAs/SM: 12 warps, 4-tile sum ring (cfg4 3.19 ms, cfg5 9.30 ms)
-      launch(trisolve_kernel<12, 4, 3, 4, true, false>, 12, smem_bytes<4, true>(d, 11));
+    case 1:  // 3 CTAs/SM: 12 warps
+      launch(trisolve_kernel<12, 4, 3, true, false>, 12, smem_bytes<true>(d, 11, ns));
       break;
-    case 2:  // producer warp issues the near tiles, 14 workers (cfg4 2.93, cfg5 9.54)
-      launch(trisolve_kernel<16, 4, 2, 8, true, true>, 16, smem_bytes<8, true>(d, 14));
+    case 2:  // producer warp issues the near tiles, 14 workers
+      launch(trisolve_kernel<16, 4, 2, true, true>, 16, smem_bytes<true>(d, 14, ns));
       break;
     case 4:  // 8 far entries in flight per lane
-      launch(trisolve_kernel<16, 8, 2, 8, true, false>, 16, smem_bytes<8, true>(d, 15));
+      launch(trisolve_kernel<16, 8, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
       break;
-    case 3:  // separate z and x vectors (cfg4 2.78, cfg5 9.35)
-      launch(trisolve_kernel<16, 4, 2, 8, false, false>, 16, smem_bytes<8, false>(d, 15));
+    case 3:  // separate z and x vectors
+      launch(trisolve_kernel<16, 4, 2, false, false>, 16, smem_bytes<false>(d, 15, ns));
       break;
-    default:  // 2 CTAs/SM (64 registers), x overwrites z in place (cfg4 2.68, cfg5 9.25)
-      launch(trisolve_kernel<16, 4, 2, 8, true, false>, 16, smem_bytes<8, true>(d, 15));
+    default:  // 2 CTAs/SM (64 registers), x overwrites z in place
+      launch(trisolve_kernel<16, 4, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
       break;
   }
   MSCG_CUDA(cudaGetLastError());
