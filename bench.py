@@ -590,6 +590,11 @@ def main():
                        "max_iters": args.max_iters, "orth": args.orth},
             "iterations": rep.iterations, "converged": rep.converged,
             "final_true_residual": rep.residual_history[-1],
+            # BASELINE cfg4 times setup + solve: problem generation and
+            # partition (host), MSC build, device factorisation, then GMRES
+            "setup_plus_solve_s": tts + sum(v for k, v in setup.items()
+                                            if k in ("generate_partition_s", "build_msc_s",
+                                                     "device_factorisation_s")),
             "setup": setup, "gpu_launches": ctx.launches - l0,
         }
     if rank == 0 and ws == 1 and args.mode == "apply" and not args.no_cpu_baseline:

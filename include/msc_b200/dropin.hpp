@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "msc/gmres.hpp"
+#include "msc/matrix_market.hpp"
 #include "msc/preconditioner.hpp"
 #include "msc/schur_approx.hpp"
 #include "mscg.h"
@@ -38,6 +39,7 @@ namespace msc_b200 {
   switch (st.code) {
     case MSCG_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case MSCG_ERR_SINGULAR: throw msc::SingularMatrixError(msg, st.pivot_index);
+    case MSCG_ERR_IO: throw msc::IoError(msg);  // message already carries "(line N)"
     default: throw std::runtime_error(msg);
   }
 }
@@ -208,6 +210,29 @@ inline std::pair<std::vector<double>, msc::SolveReport> gmres(
   r.residual_history.assign(hist.begin(), hist.begin() + rep.history_len);
   r.solve_seconds = rep.solve_seconds;
   return {std::move(x), std::move(r)};
+}
+
+// load_matrix_market / write_matrix_market (matrix_market.hpp:28-31) through
+// the library's parser and writer (same CSR, same file bytes, same IoError).
+inline msc::SparseMatrix load_matrix_market(const std::filesystem::path& path) {
+  mscg_status st{};
+  int nr = 0, nc = 0;
+  int64_t nnz = 0;
+  check(mscg_mm_read(path.c_str(), &nr, &nc, &nnz, nullptr, nullptr, nullptr, &st), st);
+  std::vector<int> rp(nr + 1), ci(nnz);
+  std::vector<double> v(nnz);
+  check(mscg_mm_read(path.c_str(), &nr, &nc, &nnz, rp.data(), ci.data(), v.data(), &st), st);
+  std::vector<msc::Triplet> t;
+  t.reserve(nnz);
+  for (int i = 0; i < nr; ++i)
+    for (int k = rp[i]; k < rp[i + 1]; ++k) t.push_back({i, ci[k], v[k]});
+  return msc::SparseMatrix::from_triplets(nr, nc, std::move(t));
+}
+inline void write_matrix_market(const std::filesystem::path& path, const msc::SparseMatrix& a) {
+  mscg_status st{};
+  check(mscg_mm_write(path.c_str(), a.rows(), a.cols(), a.row_offsets().data(),
+                      a.col_indices().data(), a.values().data(), &st),
+        st);
 }
 
 }  // namespace msc_b200

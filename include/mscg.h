@@ -40,7 +40,8 @@ typedef enum {
   MSCG_ERR_SINGULAR = 2,         /* SingularMatrixError */
   MSCG_ERR_CUDA = 3,             /* no device / CUDA runtime failure */
   MSCG_ERR_OUT_OF_MEMORY = 4,
-  MSCG_ERR_RUNTIME = 5           /* std::runtime_error */
+  MSCG_ERR_RUNTIME = 5,          /* std::runtime_error */
+  MSCG_ERR_IO = 6                /* msc::IoError (matrix_market.hpp:16-24) */
 } mscg_code;
 
 typedef enum { MSCG_MEM_HOST = 0, MSCG_MEM_DEVICE = 1 } mscg_mem;
@@ -235,6 +236,20 @@ int mscg_gmres(mscg_ctx *ctx, mscg_csr *a, mscg_precond *pc, const double *b,
 /* true_residual (gmres.cpp:26-33). */
 int mscg_true_residual(mscg_ctx *ctx, mscg_csr *a, const double *x,
                        const double *b, int mem, double *out, mscg_status *st);
+
+/* ---- Matrix Market coordinate I/O (host) -------------------------------
+ * Replaces load_matrix_market / write_matrix_market / load_vector_market /
+ * write_vector_market (proj/include/msc/matrix_market.hpp:26-36,
+ * proj/src/matrix_market.cpp:20-142).  mscg_mm_read with rp == NULL only
+ * reports the sizes; call again with rp[nrows+1], ci[nnz], v[nnz].  Failures
+ * return MSCG_ERR_IO with the reference's message ("... (line N)"). */
+int mscg_mm_read(const char *path, int *nrows, int *ncols, int64_t *nnz, int *rp,
+                 int *ci, double *v, mscg_status *st);
+int mscg_mm_write(const char *path, int nrows, int ncols, const int *rp, const int *ci,
+                  const double *v, mscg_status *st);
+/* n x 1 coordinate files; v == NULL only reports n */
+int mscg_mm_read_vector(const char *path, int *n, double *v, mscg_status *st);
+int mscg_mm_write_vector(const char *path, int n, const double *v, mscg_status *st);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,7 @@
 //   gmres                 proj/include/msc/gmres.hpp:44-47
 //   factor_ilut / solve   proj/include/msc/factorization.hpp:38-43
 //   matvec                proj/include/msc/sparse_matrix.hpp:87
+//   load/write_(matrix|vector)_market  proj/include/msc/matrix_market.hpp:26-36
 //   oracle::random_vector / random_saddle  proj/tests/oracles.hpp:92-142
 // The "anchored" interface re-ordering is the harness-level fix of
 // SURVEY.md §8(d) (public API only: permute + PartitionedMatrix::from_split +
@@ -35,6 +36,7 @@
 #include "msc/aggregates.hpp"
 #include "msc/factorization.hpp"
 #include "msc/gmres.hpp"
+#include "msc/matrix_market.hpp"
 #include "msc/oseen.hpp"
 #include "msc/parallel.hpp"
 #include "msc/partitioned_matrix.hpp"
@@ -462,6 +464,35 @@ double ref_time_block_solves(int nf, RefFactors** fs, const double* rhs,
 
 int ref_hardware_threads() {
   return static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+}
+
+// Matrix Market I/O through the reference (matrix_market.cpp:20-142).
+struct RefMat {
+  SparseMatrix a;
+};
+int ref_mm_read(const char* path, RefMat** out) {
+  return guarded([&] { *out = new RefMat{load_matrix_market(path)}; });
+}
+void ref_mat_dims(RefMat* m, int* nrows, int* ncols, int64_t* nnz) {
+  *nrows = m->a.rows();
+  *ncols = m->a.cols();
+  *nnz = m->a.nnz();
+}
+void ref_mat_get(RefMat* m, int* rp, int* ci, double* v) { copy_csr(m->a, rp, ci, v); }
+void ref_mat_free(RefMat* m) { delete m; }
+int ref_mm_write(const char* path, int nrows, int ncols, const int* rp, const int* ci,
+                 const double* v) {
+  return guarded([&] { write_matrix_market(path, csr_from_arrays(nrows, ncols, rp, ci, v)); });
+}
+int ref_mm_read_vector(const char* path, int* n, double* v) {
+  return guarded([&] {
+    std::vector<double> x = load_vector_market(path);
+    *n = static_cast<int>(x.size());
+    if (v) std::memcpy(v, x.data(), sizeof(double) * x.size());
+  });
+}
+int ref_mm_write_vector(const char* path, int n, const double* v) {
+  return guarded([&] { write_vector_market(path, std::span<const double>(v, n)); });
 }
 
 }  // extern "C"

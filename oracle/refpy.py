@@ -91,6 +91,14 @@ def lib():
         L.ref_time_block_solves.argtypes = [C.c_int, C.POINTER(vp), _f64p, _f64p,
                                             C.c_int, C.c_int]
         L.ref_hardware_threads.restype = C.c_int
+        L.ref_mm_read.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.ref_mat_dims.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int64)]
+        L.ref_mat_get.argtypes = [vp, vp, vp, vp]
+        L.ref_mat_free.argtypes = [vp]
+        L.ref_mm_write.argtypes = [C.c_char_p, C.c_int, C.c_int, vp, vp, vp]
+        L.ref_mm_read_vector.argtypes = [C.c_char_p, C.POINTER(C.c_int), vp]
+        L.ref_mm_write_vector.argtypes = [C.c_char_p, C.c_int, vp]
         _lib = L
     return _lib
 
@@ -316,3 +324,44 @@ def time_block_solves(factors, rhs, reps, workers):
 
 def hardware_threads():
     return lib().ref_hardware_threads()
+
+
+# ---- Matrix Market (reference load/write_(matrix|vector)_market) ----------
+
+def _vp(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def mm_read(path) -> Csr:
+    h = C.c_void_p()
+    _check(lib().ref_mm_read(os.fsencode(path), C.byref(h)))
+    try:
+        nr, nc, nnz = C.c_int(), C.c_int(), C.c_int64()
+        lib().ref_mat_dims(h, C.byref(nr), C.byref(nc), C.byref(nnz))
+        rp = np.empty(nr.value + 1, np.int32)
+        ci = np.empty(max(1, nnz.value), np.int32)
+        v = np.empty(max(1, nnz.value))
+        lib().ref_mat_get(h, _vp(rp), _vp(ci), _vp(v))
+        return Csr(nr.value, nc.value, rp, ci[:nnz.value].copy(), v[:nnz.value].copy())
+    finally:
+        lib().ref_mat_free(h)
+
+
+def mm_write(path, a: Csr) -> None:
+    rp = np.ascontiguousarray(a.rp, np.int32)
+    ci = np.ascontiguousarray(a.ci, np.int32)
+    v = np.ascontiguousarray(a.v, np.float64)
+    _check(lib().ref_mm_write(os.fsencode(path), a.nrows, a.ncols, _vp(rp), _vp(ci), _vp(v)))
+
+
+def mm_read_vector(path) -> np.ndarray:
+    n = C.c_int()
+    _check(lib().ref_mm_read_vector(os.fsencode(path), C.byref(n), None))
+    out = np.empty(n.value)
+    _check(lib().ref_mm_read_vector(os.fsencode(path), C.byref(n), _vp(out)))
+    return out
+
+
+def mm_write_vector(path, v) -> None:
+    v = np.ascontiguousarray(v, np.float64)
+    _check(lib().ref_mm_write_vector(os.fsencode(path), len(v), _vp(v)))

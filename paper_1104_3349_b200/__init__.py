@@ -5,6 +5,7 @@ from .msc import (  # noqa: F401
     Context,
     CudaError,
     DeviceMatrix,
+    IoError,
     MscError,
     MscPreconditioner,
     PreconditionerShard,
@@ -20,10 +21,14 @@ from .msc import (  # noqa: F401
     default_context,
     fill_factor,
     gmres,
+    load_matrix_market,
+    load_vector_market,
     matvec,
     oseen_problem,
     partitioned_problem,
     true_residual,
+    write_matrix_market,
+    write_vector_market,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

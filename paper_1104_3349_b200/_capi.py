@@ -15,6 +15,7 @@ MSCG_ERR_SINGULAR = 2
 MSCG_ERR_CUDA = 3
 MSCG_ERR_OUT_OF_MEMORY = 4
 MSCG_ERR_RUNTIME = 5
+MSCG_ERR_IO = 6
 MEM_HOST = 0
 MEM_DEVICE = 1
 
@@ -42,6 +43,11 @@ class GmresReport(C.Structure):
 
 _SIGS = {
     "mscg_abi_version": (C.c_int, []),
+    "mscg_mm_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                               C.POINTER(C.c_int64), vp, vp, vp, C.POINTER(Status)]),
+    "mscg_mm_write": (C.c_int, [C.c_char_p, C.c_int, C.c_int, vp, vp, vp, C.POINTER(Status)]),
+    "mscg_mm_read_vector": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), vp, C.POINTER(Status)]),
+    "mscg_mm_write_vector": (C.c_int, [C.c_char_p, C.c_int, vp, C.POINTER(Status)]),
     "mscg_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(Status)]),
     "mscg_ctx_destroy": (None, [vp]),
     "mscg_ctx_stream": (vp, [vp]),

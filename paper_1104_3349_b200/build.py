@@ -31,7 +31,7 @@ NVFLAGS = ARCH + ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-v"] + INC
 
 SOURCES = [
-    "host/oseen.cpp", "host/partition.cpp", "host/schur.cpp", "capi.cpp",
+    "host/oseen.cpp", "host/partition.cpp", "host/schur.cpp", "host/mmio.cpp", "capi.cpp",
     "device/runtime.cu", "device/spmv.cu", "device/factor.cu", "device/trisolve.cu",
     "device/precond.cu", "device/gmres.cu",
 ]

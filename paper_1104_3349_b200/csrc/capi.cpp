@@ -66,6 +66,9 @@ int guard(mscg_status* st, F&& f) {
   } catch (const std::invalid_argument& e) {
     set_status(st, MSCG_ERR_INVALID_ARGUMENT, e.what());
     return MSCG_ERR_INVALID_ARGUMENT;
+  } catch (const mscg::host::IoError& e) {
+    set_status(st, MSCG_ERR_IO, e.what());
+    return MSCG_ERR_IO;
   } catch (const std::bad_alloc& e) {
     set_status(st, MSCG_ERR_OUT_OF_MEMORY, "host out of memory");
     return MSCG_ERR_OUT_OF_MEMORY;
@@ -598,6 +601,55 @@ int mscg_true_residual(mscg_ctx* ctx, mscg_csr* a, const double* x, const double
     MSCG_CUDA(cudaMemcpy(dx.p, x, sizeof(double) * a->a->ncols, cudaMemcpyHostToDevice));
     MSCG_CUDA(cudaMemcpy(db.p, b, sizeof(double) * n, cudaMemcpyHostToDevice));
     *out = mscg::true_residual(&ctx->ctx, *a->a, dx.as<double>(), db.as<double>());
+  });
+}
+
+// ---- Matrix Market I/O ------------------------------------------------------
+
+int mscg_mm_read(const char* path, int* nrows, int* ncols, int64_t* nnz, int* rp, int* ci,
+                 double* v, mscg_status* st) {
+  return guard(st, [&] {
+    if (!path || !nrows || !ncols || !nnz) throw std::invalid_argument("mm_read: null argument");
+    const mscg::host::Csr a = mscg::host::load_matrix_market(path);
+    *nrows = a.nrows;
+    *ncols = a.ncols;
+    *nnz = a.nnz();
+    if (!rp) return;
+    if (!ci || !v) throw std::invalid_argument("mm_read: null output array");
+    std::memcpy(rp, a.rp.data(), sizeof(int) * a.rp.size());
+    if (a.nnz()) {
+      std::memcpy(ci, a.ci.data(), sizeof(int) * a.ci.size());
+      std::memcpy(v, a.v.data(), sizeof(double) * a.v.size());
+    }
+  });
+}
+
+int mscg_mm_write(const char* path, int nrows, int ncols, const int* rp, const int* ci,
+                  const double* v, mscg_status* st) {
+  return guard(st, [&] {
+    if (!path || nrows < 0 || ncols < 0 || !rp)
+      throw std::invalid_argument("mm_write: bad matrix");
+    mscg::host::Csr a(nrows, ncols);
+    a.rp.assign(rp, rp + nrows + 1);
+    a.ci.assign(ci, ci + rp[nrows]);
+    a.v.assign(v, v + rp[nrows]);
+    mscg::host::write_matrix_market(path, a);
+  });
+}
+
+int mscg_mm_read_vector(const char* path, int* n, double* v, mscg_status* st) {
+  return guard(st, [&] {
+    if (!path || !n) throw std::invalid_argument("mm_read_vector: null argument");
+    const std::vector<double> x = mscg::host::load_vector_market(path);
+    *n = static_cast<int>(x.size());
+    if (v && !x.empty()) std::memcpy(v, x.data(), sizeof(double) * x.size());
+  });
+}
+
+int mscg_mm_write_vector(const char* path, int n, const double* v, mscg_status* st) {
+  return guard(st, [&] {
+    if (!path || n < 0 || (n && !v)) throw std::invalid_argument("mm_write_vector: bad vector");
+    mscg::host::write_vector_market(path, v, n);
   });
 }
 

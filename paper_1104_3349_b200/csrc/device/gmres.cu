@@ -12,6 +12,8 @@
 // CTA order by the last CTA).  The host reads one 32-byte status record per
 // iteration (the reference's convergence test needs it); no other host
 // synchronisation happens inside a cycle.
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -288,14 +290,22 @@ struct Workspace {
 
 }  // namespace
 
+namespace {
+// ||b - A x|| / ||b|| with caller-provided scratch (r: n doubles, slot: 2).
+double true_residual_ws(Workspace& ws, const DevCsr& a, const double* x, const double* b,
+                        double* r, double* slot) {
+  spmv(a, x, r, b, 1, ws.ctx->stream);
+  const double rn = ws.host_nrm2(r, slot);
+  const double bn = ws.host_nrm2(b, slot + 1);
+  return bn == 0.0 ? rn : rn / bn;
+}
+}  // namespace
+
 double true_residual(Ctx* ctx, const DevCsr& a, const double* x, const double* b) {
   const int n = a.nrows;
   Workspace ws(ctx, n, 1);
   DevBuf r(sizeof(double) * std::max(1, n)), slot(sizeof(double) * 2);
-  spmv(a, x, r.as<double>(), b, 1, ctx->stream);
-  const double rn = ws.host_nrm2(r.as<double>(), slot.as<double>());
-  const double bn = ws.host_nrm2(b, slot.as<double>() + 1);
-  return bn == 0.0 ? rn : rn / bn;
+  return true_residual_ws(ws, a, x, b, r.as<double>(), slot.as<double>());
 }
 
 GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, double* x,
@@ -330,6 +340,20 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   st.status = st.scal + 16;
   double* hbuf = st.scal + 32;  // scratch for multidot results (<= m+1)
   DevBuf hscratch(sizeof(double) * (m + 2));
+  // page-locked status slots (two iterations in flight) and their events
+  struct HostStatus {
+    double* p = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~HostStatus() {
+      if (p) cudaFreeHost(p);
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+    }
+  } hs;
+  MSCG_CUDA(cudaMallocHost(&hs.p, 8 * sizeof(double)));
+  for (auto& e : hs.ev) MSCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  double* hstat = hs.p;
+  cudaEvent_t* hev = hs.ev;
   MSCG_CUDA(cudaMemsetAsync(small.p, 0, small.bytes, s));
   fill_kernel<<<G, kThreads, 0, s>>>(n, 0.0, x);
   ctx->launches++;
@@ -376,7 +400,7 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
     const double rel0 = beta / denom;
     if (res.history.empty()) res.history.push_back(rel0);
     if (rel0 <= cfg.rel_tol) {
-      last_true = true_residual(ctx, a, x, b);
+      last_true = true_residual_ws(ws, a, x, b, tmp.as<double>(), st.scal + 4);
       res.converged = last_true <= cfg.rel_tol;
       break;
     }
@@ -386,7 +410,11 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
 
     int mm = 0;
     bool breakdown = false, inner_conv = false;
-    for (int j = 0; j < m && res.iterations < cfg.max_iters; ++j) {
+    // Iteration j+1 is enqueued before iteration j's status is read, so the
+    // device never idles across the host round trip; if j ends the cycle the
+    // speculative iteration only touched H(:, j+1), g[j+1..j+2] and V_{j+2},
+    // none of which the cycle's solution uses.
+    auto enqueue_iteration = [&](int j) {
       double* vj = vbase + ld * j;
       double* wp = w.as<double>();
       apply_op(vj, wp);
@@ -412,14 +440,20 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
         }
       }
       ws.nrm2(wp, st.scal + 0);
-      // v_{j+1} = w / hnext, enqueued before the status read so it overlaps;
-      // on breakdown the (unused) vector is simply never referenced.
+      // v_{j+1} = w / hnext; on breakdown the (unused) vector is never referenced.
       scale_div_kernel<<<G, kThreads, 0, s>>>(n, wp, st.scal + 0, vbase + ld * (j + 1));
       givens_kernel<<<1, 32, 0, s>>>(st, j, denom);
       ctx->launches += 2;
-      double status[3];
-      MSCG_CUDA(cudaMemcpyAsync(status, st.status, sizeof(status), cudaMemcpyDeviceToHost, s));
-      MSCG_CUDA(cudaStreamSynchronize(s));
+      MSCG_CUDA(cudaMemcpyAsync(hstat + 4 * (j & 1), st.status, 3 * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+      MSCG_CUDA(cudaEventRecord(hev[j & 1], s));
+    };
+    const int jmax = std::min(m, cfg.max_iters - res.iterations);
+    if (jmax > 0) enqueue_iteration(0);
+    for (int j = 0; j < jmax; ++j) {
+      if (j + 1 < jmax) enqueue_iteration(j + 1);
+      MSCG_CUDA(cudaEventSynchronize(hev[j & 1]));
+      const double* status = hstat + 4 * (j & 1);
       breakdown = status[1] != 0.0;
       ++res.iterations;
       mm = j + 1;
@@ -440,7 +474,7 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
     }
     axpy1_kernel<<<G, kThreads, 0, s>>>(n, z, x);
     ctx->launches++;
-    last_true = true_residual(ctx, a, x, b);
+    last_true = true_residual_ws(ws, a, x, b, w.as<double>(), st.scal + 4);
     if (last_true <= cfg.rel_tol) {
       res.converged = true;
       done = true;
@@ -457,6 +491,10 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
       }
     }
     prev_cycle_true = last_true;
+    static const bool verbose = getenv("MSCG_VERBOSE") != nullptr;
+    if (verbose)
+      fprintf(stderr, "gmres: cycle done, %d iterations, %.3f s, true residual %.3e\n",
+              res.iterations, std::chrono::duration<double>(clk::now() - t0).count(), last_true);
   }
   res.history.push_back(last_true);
   res.final_true = last_true;

@@ -725,9 +725,14 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     if (smem > 227 * 1024)
       throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
                          " rows exceeds the shared-memory solution vector");
-    if (smem > 48 * 1024)
+    // the attribute is raised once per kernel (a driver call on every launch
+    // costs the stream its back-to-back launches)
+    static size_t smem_set = 48 * 1024;
+    if (smem > smem_set) {
       MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
+      smem_set = smem;
+    }
     static const bool verbose = getenv("MSCG_VERBOSE") != nullptr;
     if (verbose)
       fprintf(stderr, "block_trisolve: %d blocks, dim_max %d, far-sum slots %d, smem %zu B\n",

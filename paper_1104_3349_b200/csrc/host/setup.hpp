@@ -4,6 +4,7 @@
 // reproduced bit-identically so that GPU and CPU see the same matrix").
 #pragma once
 
+#include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
@@ -68,5 +69,16 @@ SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes,
                       Variant v, int threads = 0);
 
 int hardware_threads();
+
+// Matrix Market coordinate I/O (proj/src/matrix_market.cpp:20-142), the
+// wire format shared with the reference; failures throw IoError with the
+// reference's message text (proj/include/msc/matrix_market.hpp:16-24).
+struct IoError : std::runtime_error {
+  explicit IoError(const std::string& w) : std::runtime_error(w) {}
+};
+Csr load_matrix_market(const std::string& path);
+void write_matrix_market(const std::string& path, const Csr& a);
+std::vector<double> load_vector_market(const std::string& path);
+void write_vector_market(const std::string& path, const double* v, int n);
 
 }  // namespace mscg::host

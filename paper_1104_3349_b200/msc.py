@@ -20,6 +20,7 @@ CudaError (no CPU fallback).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -42,6 +43,10 @@ class CudaError(MscError):
     pass
 
 
+class IoError(MscError):
+    """msc::IoError (proj/include/msc/matrix_market.hpp:16-24)."""
+
+
 def _check(rc, st: api.Status):
     if rc == api.MSCG_OK:
         return
@@ -54,6 +59,8 @@ def _check(rc, st: api.Status):
         raise CudaError(msg)
     if rc == api.MSCG_ERR_OUT_OF_MEMORY:
         raise MemoryError(msg)
+    if rc == api.MSCG_ERR_IO:
+        raise IoError(msg)
     raise MscError(msg)
 
 
@@ -551,3 +558,47 @@ def true_residual(a: DeviceMatrix, x, b, ctx: Context | None = None) -> float:
 
 def fill_factor(b: MscPreconditioner, c: SparseMatrix) -> float:
     return b.stored_nnz() / c.nnz
+
+
+# ---- Matrix Market coordinate I/O (proj/include/msc/matrix_market.hpp:26-36)
+
+
+def load_matrix_market(path) -> SparseMatrix:
+    """Coordinate real/integer, general/symmetric/skew-symmetric; 1-based
+    indices, duplicates summed, zeros dropped (reference
+    load_matrix_market, matrix_market.cpp:20-90)."""
+    p = os.fsencode(path)
+    st = api.Status()
+    nr, nc, nnz = C.c_int(), C.c_int(), C.c_int64()
+    _check(api.lib().mscg_mm_read(p, C.byref(nr), C.byref(nc), C.byref(nnz), None, None,
+                                  None, C.byref(st)), st)
+    rp = np.empty(nr.value + 1, np.int32)
+    ci = np.empty(max(1, nnz.value), np.int32)
+    v = np.empty(max(1, nnz.value))
+    _check(api.lib().mscg_mm_read(p, C.byref(nr), C.byref(nc), C.byref(nnz), _ptr(rp),
+                                  _ptr(ci), _ptr(v), C.byref(st)), st)
+    return SparseMatrix(nr.value, nc.value, rp, ci[:nnz.value].copy(), v[:nnz.value].copy())
+
+
+def write_matrix_market(path, a: SparseMatrix) -> None:
+    """General coordinate file, 17 significant digits (matrix_market.cpp:92-110)."""
+    rp, ci, v = a.arrays()
+    st = api.Status()
+    _check(api.lib().mscg_mm_write(os.fsencode(path), a.nrows, a.ncols, _ptr(rp), _ptr(ci),
+                                   _ptr(v), C.byref(st)), st)
+
+
+def load_vector_market(path) -> np.ndarray:
+    p = os.fsencode(path)
+    st = api.Status()
+    n = C.c_int()
+    _check(api.lib().mscg_mm_read_vector(p, C.byref(n), None, C.byref(st)), st)
+    out = np.empty(n.value)
+    _check(api.lib().mscg_mm_read_vector(p, C.byref(n), _ptr(out), C.byref(st)), st)
+    return out
+
+
+def write_vector_market(path, v) -> None:
+    v = np.ascontiguousarray(v, np.float64)
+    st = api.Status()
+    _check(api.lib().mscg_mm_write_vector(os.fsencode(path), len(v), _ptr(v), C.byref(st)), st)
