@@ -26,6 +26,7 @@ struct mscg_csr {
   std::unique_ptr<mscg::DevCsr> owned;
   mscg::DevCsr* a = nullptr;
   mscg_ctx* ctx = nullptr;
+  mscg::Precond* owner = nullptr;  // set for a preconditioner's own C (saddle layout known)
 };
 struct mscg_precond {
   std::unique_ptr<mscg::Precond> pc;
@@ -290,6 +291,19 @@ void mscg_csr_destroy(mscg_csr* a) { delete a; }
 int mscg_spmv(mscg_csr* a, const double* x, double* y, int mem, mscg_status* st) {
   return guard(st, [&] {
     if (!a || !a->a) throw std::invalid_argument("matvec: null matrix (a shard has no full C)");
+    if (mem == MSCG_MEM_HOST && a->owner && is_pinned(x) && is_pinned(y)) {
+      // C of a preconditioner: block-chunked, copies overlapped with the rows
+      mscg_ctx* c = a->ctx;
+      std::lock_guard<std::mutex> lk(c->mu);
+      const size_t n = a->a->nrows;
+      const size_t need = sizeof(double) * 2 * std::max<size_t>(1, n);
+      if (c->scratch.bytes < need) c->scratch = mscg::DevBuf(need);
+      double* d_x = c->scratch.as<double>();
+      double* d_y = d_x + std::max<size_t>(1, n);
+      a->owner->spmv_host(x, y, d_x, d_y, c->ctx.stream);
+      MSCG_CUDA(cudaStreamSynchronize(c->ctx.stream));
+      return;
+    }
     with_vectors(a->ctx, x, a->a->ncols, y, a->a->nrows, mem, [&](const double* dx, double* dy) {
       mscg::spmv(*a->a, dx, dy, nullptr, 0, a->ctx->ctx.stream);
     });
@@ -311,6 +325,7 @@ int mscg_precond_build(mscg_ctx* ctx, int n, int p, const int* c_rp, const int* 
                                 s_ci, s_v, pairs(nschur, s_ranges), tol_a, s_a);
     h->matrix.a = h->pc->C.get();
     h->matrix.ctx = ctx;
+    h->matrix.owner = h->pc.get();
     *out = h.release();
   });
 }

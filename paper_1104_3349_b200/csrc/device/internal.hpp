@@ -60,6 +60,9 @@ std::unique_ptr<DevCsr> upload_csr(Ctx* ctx, int nrows, int ncols, const int* rp
 // y = base + A x                 (mode 2; base may alias y)
 void spmv(const DevCsr& a, const double* x, double* y, const double* base, int mode,
           cudaStream_t s);
+// the same for rows [row_lo, row_hi) only
+void spmv_rows(const DevCsr& a, const double* x, double* y, const double* base, int mode,
+               int row_lo, int row_hi, cudaStream_t s);
 
 // Per-block factors in the tiled solve layout (see trisolve.cu).  Rows of a
 // block are grouped in tiles of kTile = 32 rows.  For tile t:
@@ -251,6 +254,13 @@ struct Precond {
   // the solve of the others.  d_y, d_x: device scratch of n doubles.
   void apply_host(const double* y_host, double* x_host, double* d_y, double* d_x,
                   cudaStream_t s);
+  // y = C x with x, y page-locked host memory: an interior row of C only
+  // reads its own block's and the interface's columns, so each block
+  // chunk's rows are multiplied as soon as that chunk of x (and the
+  // interface part, copied first) has arrived, and leave while later
+  // chunks are still in flight.  d_x, d_y: device scratch of n doubles.
+  void spmv_host(const double* x_host, double* y_host, double* d_x, double* d_y,
+                 cudaStream_t s);
   ~Precond();
   void apply_shard_begin(const double* y_dev, double* tpart_dev, cudaStream_t s);
   void apply_shard_end(const double* y_dev, const double* tsum_dev, double* x_dev,
@@ -261,6 +271,8 @@ struct Precond {
                   cudaStream_t s);
 
  private:
+  void ensure_side_streams();
+  void chunk_rows(int c, int& lo, int& hi) const;
   cudaStream_t side[kSolveChunks] = {};
   cudaEvent_t ev_in[kSolveChunks] = {}, ev_out[kSolveChunks] = {}, ev_mid = nullptr;
 };

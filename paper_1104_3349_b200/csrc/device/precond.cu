@@ -209,26 +209,64 @@ Precond::~Precond() {
   if (ev_mid) cudaEventDestroy(ev_mid);
 }
 
+void Precond::ensure_side_streams() {
+  if (side[0]) return;
+  for (int c = 0; c < kSolveChunks; ++c) {
+    MSCG_CUDA(cudaStreamCreateWithFlags(&side[c], cudaStreamNonBlocking));
+    MSCG_CUDA(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
+    MSCG_CUDA(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
+  }
+  MSCG_CUDA(cudaEventCreateWithFlags(&ev_mid, cudaEventDisableTiming));
+}
+
+// Interior rows [lo, hi) of block chunk c (the interface starts at p).
+void Precond::chunk_rows(int c, int& lo, int& hi) const {
+  const int b0 = D->h_chunk[c], b1 = D->h_chunk[c + 1];
+  lo = b0 < D->nblocks ? D->h_row0[b0] : p;
+  hi = b1 < D->nblocks ? D->h_row0[b1] : p;
+}
+
+void Precond::spmv_host(const double* x_h, double* y_h, double* d_x, double* d_y,
+                        cudaStream_t s) {
+  if (shard.on || !C) throw Error(1, "matvec: this preconditioner holds no full C");
+  ensure_side_streams();
+  const int ng = n - p;
+  cudaEvent_t ev_if = ev_mid;
+  MSCG_CUDA(cudaEventRecord(ev_mid, s));  // after earlier work on s (scratch reuse)
+  if (ng > 0)
+    MSCG_CUDA(cudaMemcpyAsync(d_x + p, x_h + p, sizeof(double) * ng, cudaMemcpyHostToDevice, s));
+  MSCG_CUDA(cudaEventRecord(ev_if, s));
+  for (int c = 0; c < kSolveChunks; ++c) {
+    int lo, hi;
+    chunk_rows(c, lo, hi);
+    MSCG_CUDA(cudaStreamWaitEvent(side[c], ev_if, 0));
+    if (hi > lo)
+      MSCG_CUDA(cudaMemcpyAsync(d_x + lo, x_h + lo, sizeof(double) * (hi - lo),
+                                cudaMemcpyHostToDevice, side[c]));
+    MSCG_CUDA(cudaEventRecord(ev_in[c], side[c]));
+    spmv_rows(*C, d_x, d_y, nullptr, 0, lo, hi, side[c]);
+    if (hi > lo)
+      MSCG_CUDA(cudaMemcpyAsync(y_h + lo, d_y + lo, sizeof(double) * (hi - lo),
+                                cudaMemcpyDeviceToHost, side[c]));
+    MSCG_CUDA(cudaEventRecord(ev_out[c], side[c]));
+  }
+  // interface rows read every column: after all of x has arrived
+  for (int c = 0; c < kSolveChunks; ++c) MSCG_CUDA(cudaStreamWaitEvent(s, ev_in[c], 0));
+  spmv_rows(*C, d_x, d_y, nullptr, 0, p, n, s);
+  if (ng > 0)
+    MSCG_CUDA(cudaMemcpyAsync(y_h + p, d_y + p, sizeof(double) * ng, cudaMemcpyDeviceToHost, s));
+  for (int c = 0; c < kSolveChunks; ++c) MSCG_CUDA(cudaStreamWaitEvent(s, ev_out[c], 0));
+}
+
 void Precond::apply_host(const double* y_h, double* x_h, double* d_y, double* d_x,
                          cudaStream_t s) {
   if (shard.on) throw Error(1, "MscPreconditioner::apply: this is a shard (use apply_shard_*)");
-  if (!side[0]) {
-    for (int c = 0; c < kSolveChunks; ++c) {
-      MSCG_CUDA(cudaStreamCreateWithFlags(&side[c], cudaStreamNonBlocking));
-      MSCG_CUDA(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
-      MSCG_CUDA(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
-    }
-    MSCG_CUDA(cudaEventCreateWithFlags(&ev_mid, cudaEventDisableTiming));
-  }
+  ensure_side_streams();
   double* z1 = this->z1.as<double>();
   double* t = this->t.as<double>();
   double* w = this->w.as<double>();
   const int ng = n - p;
-  auto rows = [&](int c, int& lo, int& hi) {
-    const int b0 = D->h_chunk[c], b1 = D->h_chunk[c + 1];
-    lo = b0 < D->nblocks ? D->h_row0[b0] : p;
-    hi = b1 < D->nblocks ? D->h_row0[b1] : p;
-  };
+  auto rows = [&](int c, int& lo, int& hi) { chunk_rows(c, lo, hi); };
   // order the side streams after earlier work on s (scratch reuse)
   MSCG_CUDA(cudaEventRecord(ev_mid, s));
   // 1. per chunk: y rows in, z1 = D^-1 y1 on those blocks

@@ -17,12 +17,14 @@ namespace mscg {
 
 namespace {
 
+// Rows [row_lo, row_hi) are written; slices from row_lo / 32 are walked
+// (a slice straddling the range computes rows it does not write).
 __global__ void __launch_bounds__(256) sell_spmv_kernel(
-    int nrows, int nslices, const int64_t* __restrict__ sptr,
+    int row_lo, int row_hi, int nslices, const int64_t* __restrict__ sptr,
     const int* __restrict__ swidth, const int* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ x,
     double* __restrict__ y, const double* base, int mode) {
-  const int slice = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int slice = (row_lo >> 5) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (slice >= nslices) return;
   const int row = slice * 32 + lane;
@@ -35,7 +37,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(
     const double v = __ldg(val + p0 + 32 * k);
     if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
   }
-  if (row < nrows)
+  if (row >= row_lo && row < row_hi)
     y[row] = mode == 0 ? acc : (mode == 1 ? __dsub_rn(base[row], acc) : __dadd_rn(base[row], acc));
 }
 
@@ -82,16 +84,22 @@ std::unique_ptr<DevCsr> upload_csr(Ctx* ctx, int nrows, int ncols, const int* rp
   return a;
 }
 
-void spmv(const DevCsr& a, const double* x, double* y, const double* base, int mode,
-          cudaStream_t s) {
-  if (a.nslices == 0) return;
+void spmv_rows(const DevCsr& a, const double* x, double* y, const double* base, int mode,
+               int row_lo, int row_hi, cudaStream_t s) {
+  if (a.nslices == 0 || row_hi <= row_lo) return;
   const int threads = 256;
-  const int blocks = (a.nslices * 32 + threads - 1) / threads;
-  sell_spmv_kernel<<<blocks, threads, 0, s>>>(a.nrows, a.nslices, a.slice_ptr.as<int64_t>(),
+  const int nsl = ((row_hi + 31) >> 5) - (row_lo >> 5);
+  const int blocks = (nsl * 32 + threads - 1) / threads;
+  sell_spmv_kernel<<<blocks, threads, 0, s>>>(row_lo, row_hi, a.nslices, a.slice_ptr.as<int64_t>(),
                                               a.slice_width.as<int>(), a.col.as<int>(),
                                               a.val.as<double>(), x, y, base, mode);
   MSCG_CUDA(cudaGetLastError());
   a.ctx->launches++;
+}
+
+void spmv(const DevCsr& a, const double* x, double* y, const double* base, int mode,
+          cudaStream_t s) {
+  spmv_rows(a, x, y, base, mode, 0, a.nrows, s);
 }
 
 }  // namespace mscg

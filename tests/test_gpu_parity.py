@@ -321,3 +321,36 @@ def test_host_buffer_apply_chunked_matches_device(msc, ctx, ref):
                                             C.byref(st))
         assert rc == 0, st.message
         assert same_bits(xp.numpy(), want)
+
+
+@pytest.mark.gpu
+def test_host_buffer_spmv_chunked_matches_device(msc, ctx, ref, rs):
+    """matvec(C, x) of a preconditioner's own C with page-locked host
+    buffers runs block chunk by block chunk (copies overlapped with the
+    rows); it must equal the device-buffer SpMV and the reference bit for
+    bit."""
+    import ctypes as C
+    import torch
+    from paper_1104_3349_b200 import _capi
+    pb = msc.oseen_problem(128, 0.01, 16)
+    pb.build_msc("lum")
+    pc = msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=ctx)
+    x = ref.random_vector(pb.n, 5)
+    want = rs.matvec(*pb.C.arrays(), x)
+    mat = _capi.lib().mscg_precond_matrix(pc.h)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.full((pb.n,), float("nan"), dtype=torch.float64).pin_memory()
+    st = _capi.Status()
+    for _ in range(3):
+        rc = _capi.lib().mscg_spmv(mat, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()),
+                                   _capi.MEM_HOST, C.byref(st))
+        assert rc == 0, st.message
+        assert same_bits(yp.numpy(), want)
+    dev = torch.empty(pb.n, dtype=torch.float64, device="cuda")
+    xd = xp.cuda()
+    torch.cuda.synchronize()
+    rc = _capi.lib().mscg_spmv(mat, C.c_void_p(xd.data_ptr()), C.c_void_p(dev.data_ptr()),
+                               _capi.MEM_DEVICE, C.byref(st))
+    assert rc == 0, st.message
+    ctx.synchronize()
+    assert same_bits(dev.cpu().numpy(), want)
