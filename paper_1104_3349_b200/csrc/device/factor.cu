@@ -157,16 +157,17 @@ __device__ __forceinline__ void cache_insert(int f, unsigned lane, const longlon
   }
 }
 
-// Slots of a round that hold entries (warp-uniform).
-__device__ __forceinline__ int batch_slots(int len, int base) {
-  return min(kIlutBatch, (len - base + 31) >> 5);
+// Slots of a round of R entries per lane that hold entries (warp-uniform).
+template <int R>
+__device__ __forceinline__ int round_slots(int len, int base) {
+  return min(R, (len - base + 31) >> 5);
 }
-__device__ __forceinline__ void load_batch(const PoolView& pool, uint32_t s0, int len, int base,
-                                           unsigned lane, int (&jj)[kIlutBatch],
-                                           double (&uu)[kIlutBatch]) {
-  const int nr = batch_slots(len, base);
+template <int R>
+__device__ __forceinline__ void load_round(const PoolView& pool, uint32_t s0, int len, int base,
+                                           unsigned lane, int (&jj)[R], double (&uu)[R]) {
+  const int nr = round_slots<R>(len, base);
 #pragma unroll
-  for (int r = 0; r < kIlutBatch; ++r) {
+  for (int r = 0; r < R; ++r) {
     const int q = base + static_cast<int>(lane) + 32 * r;
     jj[r] = -1;
     if (r < nr && q < len) {
@@ -184,6 +185,44 @@ __device__ __forceinline__ void load_batch(const PoolView& pool, uint32_t s0, in
 constexpr long long kAbsent = 0x7ff4a85a5e5a0001LL;
 __device__ __forceinline__ double absent_value() { return __longlong_as_double(kAbsent); }
 __device__ __forceinline__ bool is_absent(double v) { return __double_as_longlong(v) == kAbsent; }
+
+// work[j] -= m * u_kj for one round of a U row (reference factorization.cpp:
+// 84-94: a new entry starts at 0.0), new entries' bits set, and new pending
+// columns below hi inserted into the candidate cache.
+template <int R>
+__device__ __forceinline__ void update_round(const int (&jj)[R], const double (&uu)[R], int nr,
+                                             double m, int kk, double* work, uint32_t* bits,
+                                             unsigned lane, const longlong2* brec, int& cand,
+                                             longlong2& rec, int& hi, bool& pf) {
+  double wv[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r < nr && jj[r] >= 0) wv[r] = work[jj[r]];
+  unsigned fills = 0;  // slots whose entry is new and a pending pivot below hi
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r < nr && jj[r] >= 0) {
+      const int j = jj[r];
+      const bool fresh = is_absent(wv[r]);
+      work[j] = __dsub_rn(fresh ? 0.0 : wv[r], __dmul_rn(m, uu[r]));
+      if (fresh) {
+        atomicOr(&bits[j >> 5], 1u << (j & 31));
+        if (j > kk && j < hi) fills |= 1u << r;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, fills != 0)) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      unsigned fm = __ballot_sync(0xffffffffu, (fills >> r) & 1u);
+      while (fm) {
+        const int src = __ffs(fm) - 1;
+        fm &= fm - 1;
+        cache_insert(__shfl_sync(0xffffffffu, jj[r], src), lane, brec, cand, rec, hi, pf);
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(32) ilut_kernel(
     int nblocks, const int* __restrict__ blk_row0, const int* __restrict__ blk_dim,
@@ -266,14 +305,15 @@ __global__ void __launch_bounds__(32) ilut_kernel(
         const double ukk = __longlong_as_double(rx);
         const uint32_t s0 = static_cast<uint32_t>(ry);
         const int len = static_cast<int>(static_cast<unsigned long long>(ry) >> 32);
-        if (!have) load_batch(pool, s0, len, 0, lane, jj, uu);
+        if (!have) load_round<kIlutBatch>(pool, s0, len, 0, lane, jj, uu);
         // the next candidate's U row goes in flight now
         const int k2 = __reduce_min_sync(0xffffffffu, cand);
         if (k2 != kNone) {
           const int own2 = __ffs(__ballot_sync(0xffffffffu, cand == k2)) - 1;
           const long long ry2 = __shfl_sync(0xffffffffu, rec.y, own2);
-          load_batch(pool, static_cast<uint32_t>(ry2),
-                     static_cast<int>(static_cast<unsigned long long>(ry2) >> 32), 0, lane, pj, pu);
+          load_round<kIlutBatch>(pool, static_cast<uint32_t>(ry2),
+                                 static_cast<int>(static_cast<unsigned long long>(ry2) >> 32), 0,
+                                 lane, pj, pu);
         }
         if (pf) {
           prefetch_urow(pool, rec.y);
@@ -284,49 +324,29 @@ __global__ void __launch_bounds__(32) ilut_kernel(
           if (lane == 0) work[kk] = 0.0;
         } else {
           if (lane == 0) work[kk] = m;
-          for (int base = 0;;) {
-            // next round's loads before this round's updates
-            const int nr = batch_slots(len, base);
-            const int nbase = base + 32 * kIlutBatch;
-            int nj[kIlutBatch];
-            double nu[kIlutBatch];
-            if (nbase < len) load_batch(pool, s0, len, nbase, lane, nj, nu);
-            double wv[kIlutBatch];
+          // the first round (prefetched, kIlutBatch entries per lane), then
+          // wider rounds for long rows, each round's loads in flight while
+          // the previous round updates
+          constexpr int kWide = 2 * kIlutBatch;
+          int nj[kWide];
+          double nu[kWide];
+          int base = 32 * kIlutBatch;
+          if (base < len) load_round<kWide>(pool, s0, len, base, lane, nj, nu);
+          update_round<kIlutBatch>(jj, uu, round_slots<kIlutBatch>(len, 0), m, kk, work, bits,
+                                   lane, brec, cand, rec, hi, pf);
+          while (base < len) {
+            int cj[kWide];
+            double cu[kWide];
 #pragma unroll
-            for (int r = 0; r < kIlutBatch; ++r)
-              if (r < nr && jj[r] >= 0) wv[r] = work[jj[r]];
-            unsigned fills = 0;  // slots whose entry is new and a pending pivot below hi
-#pragma unroll
-            for (int r = 0; r < kIlutBatch; ++r) {
-              if (r < nr && jj[r] >= 0) {
-                const int j = jj[r];
-                const bool fresh = is_absent(wv[r]);
-                // a new entry starts at 0.0 (reference: work[j] = 0, then -=)
-                work[j] = __dsub_rn(fresh ? 0.0 : wv[r], __dmul_rn(m, uu[r]));
-                if (fresh) {
-                  atomicOr(&bits[j >> 5], 1u << (j & 31));
-                  if (j > kk && j < hi) fills |= 1u << r;
-                }
-              }
+            for (int r = 0; r < kWide; ++r) {
+              cj[r] = nj[r];
+              cu[r] = nu[r];
             }
-            if (__any_sync(0xffffffffu, fills != 0)) {
-#pragma unroll
-              for (int r = 0; r < kIlutBatch; ++r) {
-                unsigned fm = __ballot_sync(0xffffffffu, (fills >> r) & 1u);
-                while (fm) {
-                  const int src = __ffs(fm) - 1;
-                  fm &= fm - 1;
-                  cache_insert(__shfl_sync(0xffffffffu, jj[r], src), lane, brec, cand, rec, hi, pf);
-                }
-              }
-            }
-            if (nbase >= len) break;
-            base = nbase;
-#pragma unroll
-            for (int r = 0; r < kIlutBatch; ++r) {
-              jj[r] = nj[r];
-              uu[r] = nu[r];
-            }
+            const int cbase = base;
+            base += 32 * kWide;
+            if (base < len) load_round<kWide>(pool, s0, len, base, lane, nj, nu);
+            update_round<kWide>(cj, cu, round_slots<kWide>(len, cbase), m, kk, work, bits, lane,
+                                brec, cand, rec, hi, pf);
           }
         }
         __syncwarp();
