@@ -6,6 +6,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -178,11 +181,22 @@ int64_t mscg_ctx_launches(mscg_ctx* ctx) { return ctx ? ctx->ctx.launches : 0; }
 int mscg_problem_oseen(int grid_n, double nu, int stretched, double stretch, int n_a,
                        int anchored, int threads, mscg_problem** out, mscg_status* st) {
   return guard(st, [&] {
+    using clk = std::chrono::steady_clock;
     auto pb = std::make_unique<mscg_problem>();
+    const auto t0 = clk::now();
     mscg::host::OseenSystem sys = mscg::host::generate_oseen(grid_n, nu, stretched != 0, stretch);
+    const auto t1 = clk::now();
     mscg::host::scale_rows(sys.C, sys.rhs);
+    const auto t2 = clk::now();
     pb->pm = mscg::host::partition_saddle(sys.C, sys.p, n_a, threads);
+    const auto t3 = clk::now();
     if (anchored) mscg::host::anchor_interface(pb->pm);
+    const auto t4 = clk::now();
+    if (getenv("MSCG_VERBOSE")) {
+      auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+      fprintf(stderr, "problem_oseen: generate %.3f s, scale %.3f s, partition %.3f s, anchor %.3f s\n",
+              sec(t0, t1), sec(t1, t2), sec(t2, t3), sec(t3, t4));
+    }
     pb->scaled_rhs.resize(sys.rhs.size());
     for (size_t k = 0; k < sys.rhs.size(); ++k) pb->scaled_rhs[k] = sys.rhs[pb->pm.perm[k]];
     flatten(pb->pm.d_ranges, pb->d_ranges_flat);
