@@ -750,6 +750,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     case 4:  // 8 far entries in flight per lane
       launch(trisolve_kernel<16, 8, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
       break;
+    case 6:  // 14 warps (72 registers): 13 workers, 6 far entries in flight per lane (~1 % either way)
+      launch(trisolve_kernel<14, 6, 2, true, false>, 14, smem_bytes<true>(d, 13, ns));
+      break;
     case 3:  // separate z and x vectors
       launch(trisolve_kernel<16, 4, 2, false, false>, 16, smem_bytes<false>(d, 15, ns));
       break;
