@@ -139,7 +139,7 @@ constexpr int kRing = 2;
 // kMaxSeg per row; the last item takes the remainder).  Item lists per block
 // and pass (L: rows ascending, U: rows descending) hold int4 {row, seg,
 // begin, end} (far-entry offsets within the block).
-constexpr int kSolveChunks = 4;
+constexpr int kSolveChunks = 8;
 // Rows of one tile whose far lists are short (<= kShortRow entries) are
 // grouped into one work item of at most kGroupEntries entries: a warp loads
 // them in one round and sums each row in shared memory (one memory round trip
