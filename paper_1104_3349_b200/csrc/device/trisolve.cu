@@ -98,6 +98,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -386,7 +389,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
   double* rbuf = scratch + kWorkers * kGroupEntries;  // solver: the tile's residuals
-  __shared__ __align__(8) uint64_t bars[kRing];
+  __shared__ __align__(8) uint64_t bars[kRing];   // near item landed (TMA)
+  __shared__ __align__(8) uint64_t empty[kRing];  // near item consumed (producer variant)
   __shared__ int done_l, done_u;
 
   const int b = a.order[a.pos0 + blockIdx.x];  // heaviest blocks first (LPT)
@@ -406,7 +410,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   if (threadIdx.x == 0) {
     done_l = 0;
     done_u = 0;
-    for (int r = 0; r < kRing; ++r) mbar_init(&bars[r], 1);
+    for (int r = 0; r < kRing; ++r) {
+      mbar_init(&bars[r], 1);
+      mbar_init(&empty[r], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -437,15 +444,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   auto next_bytes = [&](int q) {
     return static_cast<unsigned>(meta_int(ring + (q % kRing) * kSlotElems, kHdr + 1));
   };
-  // Producer: issue near items [q0, q1) as their slots free up (item q
-  // reuses the slot of item q - kRing, consumed once the solver published
-  // the matching pass counter).
+  // Producer: issue near items [q0, q1) as their slots free up — item q
+  // reuses the slot of item q - kRing, whose consumption the solver signals
+  // on the slot's empty barrier (use (q - kRing) / kRing of that slot).
   auto produce = [&](int q0, int q1) {
     for (int q = q0; q < q1; ++q) {
-      const int prev = q - kRing;  // item whose slot q reuses
-      const int* ctr = prev < nt ? &done_l : &done_u;
-      const int need = prev < nt ? prev + 1 : prev - nt + 1;
-      for (unsigned sl = 16; vload(ctr) < need; sl = min(2 * sl, 256u)) __nanosleep(sl);
+      const int prev = q - kRing;
+      mbar_wait(&empty[q % kRing], (prev / kRing) & 1);
       if (lane == 0) issue(q, next_bytes(prev));
       __syncwarp();
     }
@@ -496,6 +501,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (valid) *reinterpret_cast<volatile double*>(z + i) = zj;
       __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
+        if (kProducer) mbar_arrive(&empty[slot]);
         *reinterpret_cast<volatile int*>(&done_l) = t + 1;
         if (tr) tr[4 * t + 2] = clock64();
         if (!kProducer && t + kRing < 2 * nt) issue(t + kRing, next_bytes(t));
@@ -585,6 +591,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (valid) *reinterpret_cast<volatile double*>(x + i) = xj;
       __syncwarp();
       if (lane == 0) {
+        if (kProducer) mbar_arrive(&empty[slot]);
         if (kInPlace)
           st_release(&done_u, tt + 1);
         else
