@@ -104,6 +104,12 @@ const double *mscg_problem_scaled_rhs(const mscg_problem *pb); /* or NULL */
 int mscg_problem_build_schur(mscg_problem *pb, const char *variant, int mode,
                              int sz, int nsizes, const int *sizes, int threads,
                              mscg_status *st);
+/* The same on the device (one CTA per aggregate: dense LU of D_ii, multi-RHS
+ * solve, correction), S^ bit-identical to the host build and the reference
+ * (schur_approx.cpp:88-161). */
+int mscg_problem_build_schur_device(mscg_ctx *ctx, mscg_problem *pb, const char *variant,
+                                    int mode, int sz, int nsizes, const int *sizes,
+                                    mscg_status *st);
 int mscg_problem_num_aggregates(const mscg_problem *pb);
 const int *mscg_problem_schur_ranges(const mscg_problem *pb); /* 2*nagg */
 

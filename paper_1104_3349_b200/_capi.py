@@ -65,6 +65,8 @@ _SIGS = {
     "mscg_problem_perm": (ip, [vp]),
     "mscg_problem_d_ranges": (ip, [vp]),
     "mscg_problem_scaled_rhs": (dp, [vp]),
+    "mscg_problem_build_schur_device": (C.c_int, [vp, vp, C.c_char_p, C.c_int, C.c_int,
+                                                  C.c_int, vp, C.POINTER(Status)]),
     "mscg_problem_build_schur": (C.c_int, [vp, C.c_char_p, C.c_int, C.c_int, C.c_int, vp,
                                            C.c_int, C.POINTER(Status)]),
     "mscg_problem_num_aggregates": (C.c_int, [vp]),

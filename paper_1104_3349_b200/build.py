@@ -33,7 +33,7 @@ NVFLAGS = ARCH + ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
 SOURCES = [
     "host/oseen.cpp", "host/partition.cpp", "host/schur.cpp", "host/mmio.cpp", "capi.cpp",
     "device/runtime.cu", "device/spmv.cu", "device/factor.cu", "device/trisolve.cu",
-    "device/precond.cu", "device/gmres.cu",
+    "device/precond.cu", "device/gmres.cu", "device/schur.cu",
 ]
 HEADERS = ["host/csr.hpp", "host/setup.hpp", "device/common.cuh", "device/internal.hpp"]
 

@@ -278,6 +278,56 @@ int mscg_problem_build_schur(mscg_problem* pb, const char* variant, int mode, in
   });
 }
 
+int mscg_problem_build_schur_device(mscg_ctx* ctx, mscg_problem* pb, const char* variant,
+                                    int mode, int sz, int nsizes, const int* sizes,
+                                    mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx) throw std::invalid_argument("build_msc: null context");
+    const int ng = pb->pm.n_g(), p = pb->pm.p;
+    std::vector<int> sz_list;
+    if (mode == 2) {
+      sz_list.assign(sizes, sizes + nsizes);
+    } else if (mode == 1) {
+      sz_list = mscg::host::anchored_sizes(pb->pm, sz);
+    } else {
+      int s = sz <= 0 ? std::max(1, ng / 8) : sz;
+      s = std::min(s, ng);
+      sz_list = mscg::host::equal_sizes(ng, s);
+    }
+    const mscg::host::Variant v = mscg::host::variant_from_name(variant ? variant : "");
+    int total = 0;
+    for (int x : sz_list) {
+      if (x < 1) throw std::invalid_argument("aggregates: sizes must be >= 1");
+      total += x;
+    }
+    if (sz_list.empty() || total != ng)
+      throw std::invalid_argument("aggregates: sizes sum to " + std::to_string(total) +
+                                  ", expected " + std::to_string(ng));
+    mscg::host::SchurApprox out;
+    int b = 0;
+    for (int x : sz_list) {
+      out.ranges.push_back({b, b + x});
+      b += x;
+    }
+    if (v != mscg::host::Variant::Lum)
+      for (size_t i = 0; i < out.ranges.size(); ++i)
+        if (out.ranges[i].second > p)
+          throw std::invalid_argument("build_msc: aggregate " + std::to_string(i) +
+                                      " has a D-side index outside the (1,1) block");
+    const int kind = v == mscg::host::Variant::Lum     ? mscg::kMscLum
+                     : v == mscg::host::Variant::Mscnr ? mscg::kMscMscnr
+                                                       : mscg::kMscMscn;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const auto& c = pb->pm.C;
+    out.s_hat = mscg::host::Csr(ng, ng);
+    mscg::build_msc_device(&ctx->ctx, c.nrows, p, c.rp.data(), c.ci.data(), c.v.data(),
+                           out.ranges, kind, out.s_hat.rp, out.s_hat.ci, out.s_hat.v);
+    pb->schur = std::move(out);
+    pb->have_schur = true;
+    flatten(pb->schur.ranges, pb->s_ranges_flat);
+  });
+}
+
 int mscg_problem_num_aggregates(const mscg_problem* pb) {
   return pb->have_schur ? static_cast<int>(pb->schur.ranges.size()) : -1;
 }

@@ -288,6 +288,15 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
                                        double tol_a, int s_a, int block_begin = 0,
                                        int block_end = -1);
 
+// build_msc for numbering aggregates (ranges over the interface numbering)
+// on the device: S^ returned as a host CSR (n_g x n_g, block diagonal),
+// bit-identical to the reference.  Throws Error(SINGULAR) naming the first
+// aggregate whose D block is singular.
+constexpr int kMscMscn = 0, kMscMscnr = 1, kMscLum = 2;
+void build_msc_device(Ctx* ctx, int n, int p, const int* c_rp, const int* c_ci, const double* c_v,
+                      const std::vector<std::pair<int, int>>& ranges, int variant,
+                      std::vector<int>& s_rp, std::vector<int>& s_ci, std::vector<double>& s_v);
+
 // Download one block's factors in the reference layout.
 void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
                      std::vector<int>& lci, std::vector<double>& lv,

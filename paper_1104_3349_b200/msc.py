@@ -356,12 +356,19 @@ class Problem:
         p = api.lib().mscg_problem_scaled_rhs(self.h)
         return None if not p else np.ctypeslib.as_array(p, (self.n,)).copy()
 
-    def build_msc(self, variant="lum", sz=0, mode="equal", sizes=None, threads=0):
+    def build_msc(self, variant="lum", sz=0, mode="equal", sizes=None, threads=0,
+                  ctx: "Context | None" = None):
+        """build_msc (schur_approx.cpp:88-161) over numbering aggregates; on the
+        host (threads) or, with ctx, on the device — S^ bit-identical either way."""
         m = {"equal": 0, "anchored": 1, "explicit": 2}[mode]
         s = np.ascontiguousarray(sizes if sizes is not None else [0], np.int32)
         st = api.Status()
-        _check(api.lib().mscg_problem_build_schur(self.h, variant.encode(), m, sz, len(s),
-                                                  _ptr(s), threads, C.byref(st)), st)
+        if ctx is not None:
+            _check(api.lib().mscg_problem_build_schur_device(
+                ctx.h, self.h, variant.encode(), m, sz, len(s), _ptr(s), C.byref(st)), st)
+        else:
+            _check(api.lib().mscg_problem_build_schur(self.h, variant.encode(), m, sz, len(s),
+                                                      _ptr(s), threads, C.byref(st)), st)
         self.variant = variant
         return self
 

@@ -354,3 +354,35 @@ def test_host_buffer_spmv_chunked_matches_device(msc, ctx, ref, rs):
     assert rc == 0, st.message
     ctx.synchronize()
     assert same_bits(dev.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("grid,nu,n_a,anchored,sz", [
+    (32, 0.1, 8, False, 0),      # cfg1
+    (128, 0.01, 16, False, 0),   # cfg2 (aggregates of 158)
+    (64, 0.01, 16, False, 0),    # MSCN / MSCNR singular at aggregate 7
+    (64, 0.01, 16, True, 40),    # anchored aggregates
+])
+def test_device_build_msc_matches_reference(msc, ctx, ref, grid, nu, n_a, anchored, sz):
+    """build_msc on the device gives the reference's S^
+    bit for bit, and the reference's SingularMatrixError for a singular D
+    block."""
+    R = ref.Problem.oseen(grid, nu, n_a, anchored=anchored)
+    P = msc.oseen_problem(grid, nu, n_a, anchored=anchored)
+    mode_r, mode_p = (1, "anchored") if anchored else (0, "equal")
+    for variant in ("lum", "mscn", "mscnr"):
+        err_r = err_p = None
+        try:
+            R.build_schur(variant, sz, mode_r)
+        except ref.RefError as e:
+            err_r = str(e)
+        try:
+            P.build_msc(variant, sz=sz, mode=mode_p, ctx=ctx)
+        except (msc.SingularMatrixError, ValueError) as e:
+            err_p = str(e)
+        assert err_r == err_p, variant
+        if err_r:
+            continue
+        Rs, Ps = R.csr(5), P.s_hat
+        assert np.array_equal(Rs.rp, Ps.row_offsets) and np.array_equal(Rs.ci, Ps.col_indices)
+        assert same_bits(Rs.v, Ps.values), variant
+        assert np.array_equal(R.schur_ranges(), P.schur_ranges())
