@@ -125,18 +125,19 @@ class ClockSampler:
 
 
 def build_problem(cfg, threads=0, ctx=None):
-    """Host: generate + scale + partition (+ anchoring); then build_msc —
-    on the device when a context is given, else on the
-    host; S^ is bit-identical either way."""
+    """generate + scale (on the device when a context is given, SURVEY 8(f)
+    row 3), partition + anchoring (host), then build_msc (device with a
+    context, 8(f) row 1); everything bit-identical either way."""
     import paper_1104_3349_b200 as msc
     t0 = time.perf_counter()
     pb = msc.oseen_problem(cfg["grid"], cfg["nu"], cfg["n_a"], stretched=cfg["stretched"],
-                           stretch=cfg["stretch"], anchored=cfg["anchored"], threads=threads)
+                           stretch=cfg["stretch"], anchored=cfg["anchored"], threads=threads,
+                           ctx=ctx)
     t1 = time.perf_counter()
     pb.build_msc(cfg["variant"], sz=cfg["sz"], mode=cfg["mode"], threads=threads, ctx=ctx)
     t2 = time.perf_counter()
     return pb, {"generate_partition_s": t1 - t0, "build_msc_s": t2 - t1,
-                "build_msc_on": "device" if ctx is not None else "host"}
+                "assembly_and_msc_on": "device" if ctx is not None else "host"}
 
 
 def seeded_rhs(n, seed=0):

@@ -83,6 +83,12 @@ int mscg_problem_oseen(int grid_n, double nu, int stretched, double stretch,
                        int n_a, int anchored, int threads, mscg_problem **out,
                        mscg_status *st);
 /* PartitionedMatrix::from_split(C, p, d_ranges) (partitioned_matrix.hpp:28-29). */
+/* The same with generate_oseen's assembly and scale_rows on the device
+ * (oseen.cpp:108-212, row_scaling.cpp:8-31): bit-identical
+ * matrix and rhs; partition and anchoring stay on the host. */
+int mscg_problem_oseen_device(mscg_ctx *ctx, int grid_n, double nu, int stretched,
+                              double stretch, int n_a, int anchored, int threads,
+                              mscg_problem **out, mscg_status *st);
 int mscg_problem_from_csr(int n, const int *rp, const int *ci, const double *v,
                           int p, int nranges, const int *ranges,
                           mscg_problem **out, mscg_status *st);

@@ -56,6 +56,9 @@ _SIGS = {
     "mscg_ctx_launches": (C.c_int64, [vp]),
     "mscg_problem_oseen": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_double, C.c_int,
                                      C.c_int, C.c_int, C.POINTER(vp), C.POINTER(Status)]),
+    "mscg_problem_oseen_device": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, C.c_double,
+                                            C.c_int, C.c_int, C.c_int, C.POINTER(vp),
+                                            C.POINTER(Status)]),
     "mscg_problem_from_csr": (C.c_int, [C.c_int, vp, vp, vp, C.c_int, C.c_int, vp,
                                         C.POINTER(vp), C.POINTER(Status)]),
     "mscg_problem_destroy": (None, [vp]),

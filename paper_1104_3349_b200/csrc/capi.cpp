@@ -204,6 +204,31 @@ int mscg_problem_oseen(int grid_n, double nu, int stretched, double stretch, int
   });
 }
 
+int mscg_problem_oseen_device(mscg_ctx* ctx, int grid_n, double nu, int stretched,
+                              double stretch, int n_a, int anchored, int threads,
+                              mscg_problem** out, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx) throw std::invalid_argument("generate_oseen: null context");
+    mscg::host::check_oseen_args(grid_n, nu, stretched != 0, stretch);
+    auto pb = std::make_unique<mscg_problem>();
+    std::vector<double> x, y, xc, yc;
+    mscg::host::oseen_grid(grid_n, stretched != 0, stretch, x, y, xc, yc);
+    mscg::host::OseenSystem sys;
+    {
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      mscg::oseen_assemble_device(&ctx->ctx, grid_n, x, y, xc, yc, nu, sys.C.rp, sys.C.ci,
+                                  sys.C.v, sys.rhs, sys.p);
+    }
+    sys.C.nrows = sys.C.ncols = static_cast<int>(sys.C.rp.size()) - 1;
+    pb->pm = mscg::host::partition_saddle(sys.C, sys.p, n_a, threads);
+    if (anchored) mscg::host::anchor_interface(pb->pm);
+    pb->scaled_rhs.resize(sys.rhs.size());
+    for (size_t k = 0; k < sys.rhs.size(); ++k) pb->scaled_rhs[k] = sys.rhs[pb->pm.perm[k]];
+    flatten(pb->pm.d_ranges, pb->d_ranges_flat);
+    *out = pb.release();
+  });
+}
+
 int mscg_problem_from_csr(int n, const int* rp, const int* ci, const double* v, int p,
                           int nranges, const int* ranges, mscg_problem** out, mscg_status* st) {
   return guard(st, [&] {

@@ -297,6 +297,14 @@ void build_msc_device(Ctx* ctx, int n, int p, const int* c_rp, const int* c_ci, 
                       const std::vector<std::pair<int, int>>& ranges, int variant,
                       std::vector<int>& s_rp, std::vector<int>& s_ci, std::vector<double>& s_v);
 
+// generate_oseen's assembly + scale_rows on the device (one thread per row,
+// bit-identical; grid from the host): returns the scaled CSR and rhs.
+void oseen_assemble_device(Ctx* ctx, int n, const std::vector<double>& x,
+                           const std::vector<double>& y, const std::vector<double>& xc,
+                           const std::vector<double>& yc, double nu, std::vector<int>& rp,
+                           std::vector<int>& ci, std::vector<double>& v,
+                           std::vector<double>& rhs, int& p_out);
+
 // Download one block's factors in the reference layout.
 void download_factor(const FactorSet& fs, int idx, std::vector<int>& lrp,
                      std::vector<int>& lci, std::vector<double>& lv,

@@ -133,11 +133,24 @@ void flush_row(Csr& a, RowBuf& b) {
 
 }  // namespace
 
-OseenSystem generate_oseen(int grid_n, double nu, bool stretched, double stretch) {
+void check_oseen_args(int grid_n, double nu, bool stretched, double stretch) {
   if (grid_n < 8) throw std::invalid_argument("generate_oseen: grid_n must be >= 8");
   if (!(nu > 0.0)) throw std::invalid_argument("generate_oseen: viscosity must be positive");
   if (stretched && !(stretch > 1.0))
     throw std::invalid_argument("generate_oseen: stretch factor must exceed 1");
+}
+
+void oseen_grid(int grid_n, bool stretched, double stretch, std::vector<double>& x,
+                std::vector<double>& y, std::vector<double>& xc, std::vector<double>& yc) {
+  Grid g = make_grid(grid_n, stretched, stretch);
+  x = std::move(g.x);
+  y = std::move(g.y);
+  xc = std::move(g.xc);
+  yc = std::move(g.yc);
+}
+
+OseenSystem generate_oseen(int grid_n, double nu, bool stretched, double stretch) {
+  check_oseen_args(grid_n, nu, stretched, stretch);
   const Grid g = make_grid(grid_n, stretched, stretch);
   const int n = g.n;
   const int p = g.velocity_count();

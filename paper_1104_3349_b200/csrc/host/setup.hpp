@@ -21,6 +21,11 @@ struct OseenSystem {
 
 // generate_oseen(..., WindKind::Recirculating, stretch): proj/src/oseen.cpp:373-441.
 OseenSystem generate_oseen(int grid_n, double nu, bool stretched, double stretch);
+// Its argument checks and its grid (cell boundaries x, y and centres xc, yc;
+// oseen.cpp:19-71) for the device assembly (csrc/device/oseen.cu).
+void check_oseen_args(int grid_n, double nu, bool stretched, double stretch);
+void oseen_grid(int grid_n, bool stretched, double stretch, std::vector<double>& x,
+                std::vector<double>& y, std::vector<double>& xc, std::vector<double>& yc);
 
 // scale_rows: proj/src/row_scaling.cpp:8-31 (in place).
 void scale_rows(Csr& a, std::vector<double>& rhs);

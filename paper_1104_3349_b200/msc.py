@@ -386,12 +386,18 @@ class Problem:
 
 
 def oseen_problem(grid_n, nu, n_a, stretched=False, stretch=1.056, anchored=False,
-                  threads=0) -> Problem:
-    """generate_oseen -> scale_rows -> partition_saddle(Interleaved) [-> anchoring]."""
+                  threads=0, ctx: "Context | None" = None) -> Problem:
+    """generate_oseen -> scale_rows -> partition_saddle(Interleaved) [-> anchoring].
+    With ctx the assembly and row scaling run on the device (bit-identical)."""
     h = C.c_void_p()
     st = api.Status()
-    _check(api.lib().mscg_problem_oseen(grid_n, nu, int(stretched), stretch, n_a, int(anchored),
-                                        threads, C.byref(h), C.byref(st)), st)
+    if ctx is not None:
+        _check(api.lib().mscg_problem_oseen_device(ctx.h, grid_n, nu, int(stretched), stretch,
+                                                   n_a, int(anchored), threads, C.byref(h),
+                                                   C.byref(st)), st)
+    else:
+        _check(api.lib().mscg_problem_oseen(grid_n, nu, int(stretched), stretch, n_a,
+                                            int(anchored), threads, C.byref(h), C.byref(st)), st)
     return Problem(h)
 
 

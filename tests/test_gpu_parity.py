@@ -386,3 +386,35 @@ def test_device_build_msc_matches_reference(msc, ctx, ref, grid, nu, n_a, anchor
         assert np.array_equal(Rs.rp, Ps.row_offsets) and np.array_equal(Rs.ci, Ps.col_indices)
         assert same_bits(Rs.v, Ps.values), variant
         assert np.array_equal(R.schur_ranges(), P.schur_ranges())
+
+
+@pytest.mark.parametrize("grid,nu,n_a,stretched,stretch,anchored", [
+    (32, 0.1, 8, False, 1.056, False),     # cfg1
+    (128, 0.01, 16, False, 1.056, False),  # cfg2
+    (64, 0.002, 16, True, 1.1, False),     # stretched grid
+    (96, 0.001, 32, False, 1.056, True),   # anchored interface
+])
+def test_device_oseen_assembly_matches_reference(msc, ctx, ref, grid, nu, n_a, stretched,
+                                                  stretch, anchored):
+    """generate_oseen + scale_rows on the device: the
+    reference's matrix, permutation and scaled rhs bit for bit."""
+    R = ref.Problem.oseen(grid, nu, n_a, stretched=stretched, stretch=stretch, anchored=anchored)
+    P = msc.oseen_problem(grid, nu, n_a, stretched=stretched, stretch=stretch,
+                          anchored=anchored, ctx=ctx)
+    Rc, Pc = R.csr(0), P.C
+    assert np.array_equal(Rc.rp, Pc.row_offsets) and np.array_equal(Rc.ci, Pc.col_indices)
+    assert same_bits(Rc.v, Pc.values)
+    assert np.array_equal(R.perm(), P.perm())
+    assert np.array_equal(R.d_ranges(), P.d_ranges())
+    assert same_bits(R.scaled_rhs(), P.scaled_rhs())
+
+
+def test_device_oseen_assembly_cfg5_digest(msc, ctx):
+    """At cfg5 size the device-assembled problem equals the host one (whose
+    digests are pinned to the reference in tests/golden/cfg5.json)."""
+    import json
+    js = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg5.json")))
+    P = msc.oseen_problem(2048, 0.01, 4096, anchored=True, ctx=ctx)
+    from test_host_setup import csr_digest, digest
+    assert csr_digest(P.C) == js["c_sha"]
+    assert digest(P.perm().astype("<i4")) == js["perm_sha"]
