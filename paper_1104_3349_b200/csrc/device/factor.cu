@@ -1315,10 +1315,13 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
     fs->h_chunk.assign(kSolveChunks + 1, 0);
     for (int c = 0; c <= kSolveChunks; ++c)
       fs->h_chunk[c] = static_cast<int>(static_cast<long long>(nb) * c / kSolveChunks);
+    auto by_cost = [&](int x, int y) { return cost(x) > cost(y); };
+    std::vector<int> whole = ord;
+    std::stable_sort(whole.begin(), whole.end(), by_cost);
+    fs->order = upload_vec(whole, s);  // one launch over all blocks
     for (int c = 0; c < kSolveChunks; ++c)
-      std::stable_sort(ord.begin() + fs->h_chunk[c], ord.begin() + fs->h_chunk[c + 1],
-                       [&](int x, int y) { return cost(x) > cost(y); });
-    fs->order = upload_vec(ord, s);
+      std::stable_sort(ord.begin() + fs->h_chunk[c], ord.begin() + fs->h_chunk[c + 1], by_cost);
+    fs->order_chunked = upload_vec(ord, s);  // chunk launches (host-buffer paths)
   }
 
   if (times) times->pack_s += std::chrono::duration<double>(clk::now() - t3).count();

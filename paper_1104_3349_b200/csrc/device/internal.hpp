@@ -184,7 +184,8 @@ struct FactorSet {
   DevBuf litems, uitems;                   // int32 (row << 3 | seg)
   DevBuf udiag, urdiag;                    // fp64[total_rows]
   DevBuf perm;                             // int32[total_rows] (local), if has_perm
-  DevBuf order;                            // int32[nblocks] solve launch order
+  DevBuf order;                            // int32[nblocks] launch order, all blocks (LPT)
+  DevBuf order_chunked;                    // the same per chunk (positions h_chunk[c]..)
   // The blocks are cut into kSolveChunks contiguous chunks (block index
   // ranges h_chunk[c] .. h_chunk[c+1]); `order` lists each chunk's blocks
   // longest first (LPT) at the same positions, so a chunk can be solved on

@@ -700,7 +700,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.uslot = fs.uslot.as<int>();
   a.max_slots = fs.max_slots;
   a.perm = fs.has_perm ? fs.perm.as<int>() : nullptr;
-  a.order = fs.order.as<int>();
+  a.order = chunk < 0 ? fs.order.as<int>() : fs.order_chunked.as<int>();
   a.pos0 = pos0;
   a.dim_max = fs.max_dim;
   a.trace = trace;
