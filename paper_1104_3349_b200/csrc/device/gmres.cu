@@ -83,36 +83,50 @@ __global__ void __launch_bounds__(kThreads) nrm2_kernel(int n, const double* __r
 }
 
 // h[i] = V_i . w for i < nv: basis vectors in groups of kDotGroup, so w is
-// read once per group and each CTA reduces kDotGroup sums per pass.
+// read once per group and each CTA reduces kDotGroup sums per pass.  Rows
+// go in 16-byte pairs (the basis is stored with a 32-element-aligned
+// leading dimension), two pairs in flight per thread.
 constexpr int kDotGroup = 8;
 __global__ void __launch_bounds__(kThreads) multidot_kernel(int n, int nv, const double* __restrict__ V,
                                                             size_t ld, const double* __restrict__ w,
                                                             Reducer red, double* h) {
   __shared__ double sh[kThreads / 32][kDotGroup];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npair = n >> 1;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
   for (int i0 = 0; i0 < nv; i0 += kDotGroup) {
     const int ng = min(kDotGroup, nv - i0);
     double acc[kDotGroup];
 #pragma unroll
     for (int g = 0; g < kDotGroup; ++g) acc[g] = 0.0;
     const int stride = gridDim.x * blockDim.x;
-    int r = blockIdx.x * blockDim.x + threadIdx.x;
-    for (; r + stride < n; r += 2 * stride) {  // two rows in flight per thread
-      const double wr = w[r], wr2 = w[r + stride];
-      double va[kDotGroup], vb[kDotGroup];
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + stride < npair; q += 2 * stride) {
+      const double2 wa = w2[q], wb = w2[q + stride];
+      double2 va[kDotGroup], vb[kDotGroup];
 #pragma unroll
       for (int g = 0; g < kDotGroup; ++g) {
-        va[g] = g < ng ? __ldg(V + ld * (i0 + g) + r) : 0.0;
-        vb[g] = g < ng ? __ldg(V + ld * (i0 + g) + r + stride) : 0.0;
+        const double2* vg = reinterpret_cast<const double2*>(V + ld * (i0 + g));
+        va[g] = g < ng ? __ldg(vg + q) : make_double2(0.0, 0.0);
+        vb[g] = g < ng ? __ldg(vg + q + stride) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int g = 0; g < kDotGroup; ++g) acc[g] = fma(vb[g], wr2, fma(va[g], wr, acc[g]));
+      for (int g = 0; g < kDotGroup; ++g)
+        acc[g] = fma(vb[g].y, wb.y, fma(vb[g].x, wb.x, fma(va[g].y, wa.y, fma(va[g].x, wa.x, acc[g]))));
     }
-    if (r < n) {
-      const double wr = w[r];
+    if (q < npair) {
+      const double2 wa = w2[q];
 #pragma unroll
       for (int g = 0; g < kDotGroup; ++g)
-        if (g < ng) acc[g] = fma(__ldg(V + ld * (i0 + g) + r), wr, acc[g]);
+        if (g < ng) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(V + ld * (i0 + g)) + q);
+          acc[g] = fma(v.y, wa.y, fma(v.x, wa.x, acc[g]));
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: the last row
+#pragma unroll
+      for (int g = 0; g < kDotGroup; ++g)
+        if (g < ng) acc[g] = fma(__ldg(V + ld * (i0 + g) + (n - 1)), w[n - 1], acc[g]);
     }
 #pragma unroll
     for (int g = 0; g < kDotGroup; ++g) {
@@ -139,10 +153,21 @@ __global__ void __launch_bounds__(kThreads) multiaxpy_kernel(int n, int nv, cons
   __shared__ double sh[512];
   for (int i = threadIdx.x; i < nv; i += blockDim.x) sh[i] = h[i];
   __syncthreads();
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    double acc = w[r];
-    for (int i = 0; i < nv; ++i) acc = fma(-sh[i], V[ld * i + r], acc);
-    w[r] = acc;
+  const int npair = n >> 1;
+  double2* w2 = reinterpret_cast<double2*>(w);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npair; q += gridDim.x * blockDim.x) {
+    double2 acc = w2[q];
+    for (int i = 0; i < nv; ++i) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(V + ld * i) + q);
+      acc.x = fma(-sh[i], v.x, acc.x);
+      acc.y = fma(-sh[i], v.y, acc.y);
+    }
+    w2[q] = acc;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double acc = w[n - 1];
+    for (int i = 0; i < nv; ++i) acc = fma(-sh[i], V[ld * i + (n - 1)], acc);
+    w[n - 1] = acc;
   }
   if (blockIdx.x == 0 && hcol)
     for (int i = threadIdx.x; i < nv; i += blockDim.x) hcol[i] = accumulate ? hcol[i] + sh[i] : sh[i];
@@ -325,7 +350,8 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
 
   Workspace ws(ctx, n, m + 2);
   const int G = ws.grid();
-  const size_t ld = static_cast<size_t>(n);
+  // basis columns 256-byte aligned (16-byte pair loads in the CGS2 kernels)
+  const size_t ld = (static_cast<size_t>(n) + 31) & ~static_cast<size_t>(31);
   DevBuf V(sizeof(double) * ld * (m + 1)), w(sizeof(double) * n), tmp(sizeof(double) * n);
   DevBuf small(sizeof(double) * (static_cast<size_t>(m + 1) * m + 4 * (m + 1) + 64));
   double* sp = small.as<double>();
