@@ -20,12 +20,12 @@ def main():
     import paper_1104_3349_b200 as msc
     cfg = bench.CONFIGS[a.config]
     ctx = msc.Context(0)
-    pb, t = bench.build_problem(cfg)
+    pb, t = bench.build_problem(cfg, ctx=ctx)
     t0 = time.perf_counter()
     pc = msc.build_preconditioner(pb, tolA=bench.TOL_A, sA=bench.S_A, ctx=ctx)
     t["build_preconditioner_s"] = time.perf_counter() - t0
     t.update(pc.build_times())
-    print(a.config, {k: round(v, 3) for k, v in t.items()})
+    print(a.config, {k: (round(v, 3) if isinstance(v, float) else v) for k, v in t.items()})
 
 
 if __name__ == "__main__":
