@@ -71,7 +71,8 @@ __device__ __forceinline__ longlong2 load_rec(const longlong2* recs, int g) {
 
 constexpr int kIlutBatch = 4;  // U-row entries per lane in flight per round
 constexpr int kNone = 0x7fffffff;
-constexpr int kPfCands = 16;   // cached candidates whose U rows are L2-prefetched at refill
+constexpr int kPfCands = 32;   // cached candidates whose U rows are L2-prefetched at refill
+constexpr bool kIlutPrefetch = true;
 
 // Fire-and-forget L2 prefetch of a finished U row (values + columns): the
 // pivots' U rows are re-read from HBM (a block's U outgrows its share of
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(32) ilut_kernel(
                                  static_cast<int>(static_cast<unsigned long long>(ry2) >> 32), 0,
                                  lane, pj, pu);
         }
-        if (pf) {
+        if (kIlutPrefetch && pf) {
           prefetch_urow(pool, rec.y);
           pf = false;
         }
