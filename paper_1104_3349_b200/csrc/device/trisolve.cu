@@ -38,8 +38,12 @@
 //    epilogue.
 // Rounding differs from the reference's sequential row sums by ~1e-16
 // relative, far inside the 1e-10 apply bar.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -668,6 +672,27 @@ size_t smem_bytes(int dim_max, int workers, int slots) {
 
 }  // namespace
 
+namespace {
+void ensure_smem(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> set;  // kernel -> attribute value
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : set)
+    if (e.first == kern) {
+      if (smem > e.second) {
+        MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        e.second = smem;
+      }
+      return;
+    }
+  if (smem > 48 * 1024)
+    MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  set.push_back({kern, std::max<size_t>(smem, 48 * 1024)});
+}
+}  // namespace
+
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const double* sub,
                     cudaStream_t s, long long* trace, int chunk) {
   if (fs.nblocks == 0) return;
@@ -732,14 +757,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     if (smem > 227 * 1024)
       throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
                          " rows exceeds the shared-memory solution vector");
-    // the attribute is raised once per kernel (a driver call on every launch
-    // costs the stream its back-to-back launches)
-    static size_t smem_set = 48 * 1024;
-    if (smem > smem_set) {
-      MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-      smem_set = smem;
-    }
+    // the attribute is raised once per kernel and size (a driver call on
+    // every launch costs the stream its back-to-back launches)
+    ensure_smem(reinterpret_cast<const void*>(kern), smem);
     static const bool verbose = getenv("MSCG_VERBOSE") != nullptr;
     if (verbose)
       fprintf(stderr, "block_trisolve: %d blocks, dim_max %d, far-sum slots %d, smem %zu B\n",
@@ -747,6 +767,20 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     kern<<<npos, warps * 32, smem, s>>>(a, rhs, out, sub);
   };
   const int d = fs.max_dim, ns = fs.max_slots;
+  // Fewer blocks than SMs (cfg2/cfg3): each block has an SM to itself, so
+  // large blocks get 31 workers (1024 threads) instead of 15 (cfg2 D-solve
+  // 0.645 -> 0.417 ms); small ones (cfg1, ~400 rows) are faster without.
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  if (variant == 0 && npos <= sms && d > 1024) {
+    launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
+    MSCG_CUDA(cudaGetLastError());
+    return;
+  }
   switch (variant) {
     case 1:  // 3 CTAs/SM: 12 warps
       launch(trisolve_kernel<12, 4, 3, true, false>, 12, smem_bytes<true>(d, 11, ns));
