@@ -1329,6 +1329,12 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   return fs;
 }
 
+FactorSet::~FactorSet() {
+  if (tail_stream) cudaStreamDestroy(tail_stream);
+  for (auto e : tail_ev)
+    if (e) cudaEventDestroy(e);
+}
+
 int64_t FactorSet::nnz_l() const {
   int64_t s = 0;
   for (auto v : h_nnz_l) s += v;

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -192,6 +193,11 @@ struct FactorSet {
   // its own (host-buffer applies overlap the copies of one chunk with the
   // solve of another).
   std::vector<int> h_chunk;
+  // side stream for the last partial wave of a whole-set solve (trisolve.cu)
+  mutable std::mutex tail_mu;
+  mutable cudaStream_t tail_stream = nullptr;
+  mutable cudaEvent_t tail_ev[2] = {nullptr, nullptr};
+  ~FactorSet();
   int64_t nnz_l() const;
   int64_t nnz_u() const;
   int64_t far_l() const { return h_loff.empty() ? 0 : h_loff.back(); }

@@ -781,6 +781,43 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     MSCG_CUDA(cudaGetLastError());
     return;
   }
+  // Last partial wave (T < SMs blocks after the full waves of 2 CTAs per
+  // SM, cfg4: 1024 = 3 x 296 + 136): its blocks, the smallest in LPT order,
+  // run as 32-warp CTAs on a side stream so each gets a whole SM's workers
+  // as SMs drain, instead of half-empty SMs at the end of one launch.
+  const int tail = npos % (2 * sms);
+  static const bool split_tail = getenv("MSCG_TRI_NO_TAIL") == nullptr;
+  if (split_tail && variant == 0 && chunk < 0 && d > 1024 && npos > 2 * sms && tail > 0 &&
+      tail <= sms) {
+    std::lock_guard<std::mutex> lk(fs.tail_mu);
+    if (!fs.tail_stream) {
+      MSCG_CUDA(cudaStreamCreateWithFlags(&fs.tail_stream, cudaStreamNonBlocking));
+      MSCG_CUDA(cudaEventCreateWithFlags(&fs.tail_ev[0], cudaEventDisableTiming));
+      MSCG_CUDA(cudaEventCreateWithFlags(&fs.tail_ev[1], cudaEventDisableTiming));
+    }
+    MSCG_CUDA(cudaEventRecord(fs.tail_ev[0], s));
+    MSCG_CUDA(cudaStreamWaitEvent(fs.tail_stream, fs.tail_ev[0], 0));
+    const int head = npos - tail;
+    {
+      auto k16 = trisolve_kernel<16, 4, 2, true, false>;
+      const size_t sm16 = smem_bytes<true>(d, 15, ns);
+      ensure_smem(reinterpret_cast<const void*>(k16), sm16);
+      k16<<<head, 16 * 32, sm16, s>>>(a, rhs, out, sub);
+      MSCG_CUDA(cudaGetLastError());
+    }
+    {
+      TriArgs at = a;
+      at.pos0 = pos0 + head;
+      auto k32 = trisolve_kernel<32, 4, 1, true, false>;
+      const size_t sm32 = smem_bytes<true>(d, 31, ns);
+      ensure_smem(reinterpret_cast<const void*>(k32), sm32);
+      k32<<<tail, 32 * 32, sm32, fs.tail_stream>>>(at, rhs, out, sub);
+      MSCG_CUDA(cudaGetLastError());
+    }
+    MSCG_CUDA(cudaEventRecord(fs.tail_ev[1], fs.tail_stream));
+    MSCG_CUDA(cudaStreamWaitEvent(s, fs.tail_ev[1], 0));
+    return;
+  }
   switch (variant) {
     case 1:  // 3 CTAs/SM: 12 warps
       launch(trisolve_kernel<12, 4, 3, true, false>, 12, smem_bytes<true>(d, 11, ns));
