@@ -73,6 +73,16 @@ int mscg_ctx_set_stream(mscg_ctx *ctx, void *stream, int use_own,
 int mscg_ctx_synchronize(mscg_ctx *ctx, mscg_status *st);
 /* Kernels launched by this library since creation (evidence counter). */
 int64_t mscg_ctx_launches(mscg_ctx *ctx);
+/* Interior correction of preconditioners built later on this context (no
+ * reference counterpart; the result is the same operator): 0 = the
+ * reference's two steps w = E z2, x1 = z1 - D^-1 w; 1 = precompute
+ * W = D^-1 E per interior block at build time and apply x1 = z1 - W z2;
+ * 2 = auto (1 when W is smaller than the interior factors and fits; the
+ * default, overridable by MSCG_CORRECTION=off|on|auto); -1 = default. */
+#define MSCG_CORRECTION_OFF 0
+#define MSCG_CORRECTION_ON 1
+#define MSCG_CORRECTION_AUTO 2
+int mscg_ctx_set_correction(mscg_ctx *ctx, int mode, mscg_status *st);
 
 /* ---- host problem layer (setup, once) -------------------- */
 /* generate_oseen(grid_n, nu, Uniform|Stretched, Recirculating, stretch)
@@ -193,6 +203,11 @@ int mscg_precond_factor(const mscg_precond *pc, int kind, int idx, int *dim,
 /* Timing breakdown of the last build (seconds). */
 int mscg_precond_build_times(const mscg_precond *pc, double *ilut_s,
                              double *schur_lu_s, double *pack_s);
+/* Interior correction of this preconditioner: *on = 1 when W = D^-1 E is
+ * in use, *entries = its fp64 entries, *kmax = most interface columns of a
+ * block, *build_s = seconds spent building it. */
+int mscg_precond_correction(const mscg_precond *pc, int *on, int64_t *entries,
+                            int *kmax, double *build_s);
 /* The operator matrix C of the preconditioner, resident on the device. */
 mscg_csr *mscg_precond_matrix(mscg_precond *pc);
 

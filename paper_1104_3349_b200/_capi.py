@@ -54,6 +54,7 @@ _SIGS = {
     "mscg_ctx_synchronize": (C.c_int, [vp, C.POINTER(Status)]),
     "mscg_ctx_set_stream": (C.c_int, [vp, vp, C.c_int, C.POINTER(Status)]),
     "mscg_ctx_launches": (C.c_int64, [vp]),
+    "mscg_ctx_set_correction": (C.c_int, [vp, C.c_int, C.POINTER(Status)]),
     "mscg_problem_oseen": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_double, C.c_int,
                                      C.c_int, C.c_int, C.POINTER(vp), C.POINTER(Status)]),
     "mscg_problem_oseen_device": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, C.c_double,
@@ -98,6 +99,7 @@ _SIGS = {
     "mscg_precond_factor": (C.c_int, [vp, C.c_int, C.c_int, ip, i64p, i64p, vp, vp, vp, vp, vp,
                                       vp, vp, C.POINTER(Status)]),
     "mscg_precond_build_times": (C.c_int, [vp, dp, dp, dp]),
+    "mscg_precond_correction": (C.c_int, [vp, ip, i64p, ip, dp]),
     "mscg_precond_matrix": (vp, [vp]),
     "mscg_gmres": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(GmresConfig),
                              C.POINTER(GmresReport), vp, C.c_int, C.POINTER(Status)]),

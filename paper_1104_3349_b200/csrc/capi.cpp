@@ -175,6 +175,15 @@ int mscg_ctx_synchronize(mscg_ctx* ctx, mscg_status* st) {
   return guard(st, [&] { MSCG_CUDA(cudaStreamSynchronize(ctx->ctx.stream)); });
 }
 int64_t mscg_ctx_launches(mscg_ctx* ctx) { return ctx ? ctx->ctx.launches : 0; }
+int mscg_ctx_set_correction(mscg_ctx* ctx, int mode, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx) throw std::invalid_argument("mscg_ctx_set_correction: null context");
+    if (mode < -1 || mode > MSCG_CORRECTION_AUTO)
+      throw std::invalid_argument("mscg_ctx_set_correction: mode must be -1, 0, 1 or 2");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->ctx.correction = mode;
+  });
+}
 
 // ---- host problem layer ---------------------------------------------------
 
@@ -580,6 +589,17 @@ int mscg_precond_build_times(const mscg_precond* pc, double* ilut_s, double* sch
   if (ilut_s) *ilut_s = pc->pc->times.ilut_s;
   if (schur_lu_s) *schur_lu_s = pc->pc->times.lu_s;
   if (pack_s) *pack_s = pc->pc->times.pack_s;
+  return MSCG_OK;
+}
+
+int mscg_precond_correction(const mscg_precond* pc, int* on, int64_t* entries, int* kmax,
+                            double* build_s) {
+  if (!pc) return MSCG_ERR_INVALID_ARGUMENT;
+  const auto* c = pc->pc->corr.get();
+  if (on) *on = c ? 1 : 0;
+  if (entries) *entries = c ? c->entries : 0;
+  if (kmax) *kmax = c ? c->kmax : 0;
+  if (build_s) *build_s = c ? c->build_s : 0.0;
   return MSCG_OK;
 }
 

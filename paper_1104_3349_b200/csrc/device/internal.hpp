@@ -33,6 +33,7 @@ struct Ctx {
   cudaStream_t owned_stream = nullptr;  // the context's own (destroyed with it)
   int sm_count = 148;
   int64_t launches = 0;
+  int correction = -1;  // kCorr* for preconditioners built on this context (-1: default)
   // pinned staging for host<->device vector traffic
   double* pinned = nullptr;
   size_t pinned_elems = 0;
@@ -212,7 +213,7 @@ struct BlockSpec {
 };
 
 struct FactorTimes {
-  double ilut_s = 0, lu_s = 0, pack_s = 0;
+  double ilut_s = 0, lu_s = 0, pack_s = 0, corr_s = 0;
 };
 
 // Factor all blocks of `a_rp/a_ci/a_v` (device CSR arrays, int32) listed in
@@ -227,9 +228,42 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
 
 // x_b = U_b^-1 L_b^-1 P_b rhs_b for every block b, launched as one kernel
 // (one CTA per block).  out = x, or out = sub - x when sub != nullptr.
+// order/norder (optional): solve only the blocks order[0 .. norder) (device
+// list), in that order.
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out,
                     const double* sub, cudaStream_t s, long long* trace = nullptr,
-                    int chunk = -1);
+                    int chunk = -1, const int* order = nullptr, int norder = 0);
+// Raise a kernel's dynamic shared-memory limit once per kernel and size.
+void ensure_smem(const void* kern, size_t smem);
+
+// Explicit interior correction (correct.cu): W_b = D_b^-1 E_b[:, cols_b] per
+// interior block as a dense column-major panel, so the apply's second half
+// x1 = z1 - D^-1 (E z2) becomes x1_b = z1_b - W_b z2[cols_b] (one streaming
+// pass over W instead of an E SpMV and a second pass over the factors).
+constexpr int kCorrOff = 0, kCorrOn = 1, kCorrAuto = 2;
+int correction_mode_default();  // MSCG_CORRECTION=off|on|auto (default auto)
+struct Correction {
+  int nblocks = 0, kmax = 0;
+  int64_t entries = 0;         // sum over blocks of dim_b * k_b
+  const int* row0 = nullptr;   // the FactorSet's (borrowed)
+  const int* dim = nullptr;
+  DevBuf woff;                 // int64[nblocks+1] panel offsets
+  DevBuf wcoff;                // int32[nblocks+1] column-list offsets
+  DevBuf wcols;                // int32 interface columns per block, ascending
+  DevBuf wval;                 // fp64 panels
+  DevBuf items;                // int2 {block, first row} (512-row slices)
+  std::vector<int> h_item_chunk;  // item range of block chunk c
+  double build_s = 0;
+};
+// E rows numbered like D's rows (e_rp has D.total_rows + 1 entries), columns
+// = interface index.  r/o scratch: D.total_rows doubles each.  Returns null
+// when mode is off, or auto and the panels would not save bytes / memory.
+std::unique_ptr<Correction> build_correction(Ctx* ctx, const FactorSet& D, const int* e_rp,
+                                             const int* e_ci, const double* e_v, int mode,
+                                             double* r_scratch, double* o_scratch);
+// out_b = z1_b - W_b x2[cols_b] for all blocks (chunk < 0) or block chunk c.
+void apply_correction(const Correction& c, const double* x2, const double* z1, double* out,
+                      int chunk, cudaStream_t s);
 
 // A shard owns the interior blocks [b0, b1) (rows [row_lo, row_hi)) of a
 // preconditioner split across ranks.  Its D holds only those
@@ -251,6 +285,7 @@ struct Precond {
   int n = 0, p = 0;
   std::unique_ptr<DevCsr> C, E, F;
   std::unique_ptr<FactorSet> D, S;
+  std::unique_ptr<Correction> corr;  // explicit D^-1 E panels (null: two solves)
   int64_t stored_nnz = 0;
   FactorTimes times;
   Shard shard;

@@ -8,7 +8,9 @@
 //   w  = E z2                    SELL SpMV
 //   x1 = z1 - D^-1 w             block_trisolve with fused subtraction
 //
-// Five stream-ordered launches, no host synchronisation.
+// Five stream-ordered launches, no host synchronisation.  With the explicit
+// correction (correct.cu, built when it saves bytes) the last two become
+// one: x1 = z1 - W z2, W = D^-1 E precomputed per block.
 #include <algorithm>
 #include <chrono>
 
@@ -90,13 +92,15 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
   pc->n = n;
   pc->p = p;
   const int lo = d_ranges[block_begin].first, hi = d_ranges[block_end - 1].second;
+  std::vector<int> e_rp, e_ci;  // host E (rows of this set), kept for the correction
+  std::vector<double> e_v;
   {
     std::vector<int> rp, ci;
     std::vector<double> v;
     if (!sharded) {
       pc->C = upload_csr(ctx, n, n, c_rp, c_ci, c_v);
-      extract(c_rp, c_ci, c_v, 0, p, p, n, rp, ci, v);  // E = C[0:p, p:n]
-      pc->E = upload_csr(ctx, p, ng, rp.data(), ci.data(), v.data());
+      extract(c_rp, c_ci, c_v, 0, p, p, n, e_rp, e_ci, e_v);  // E = C[0:p, p:n]
+      pc->E = upload_csr(ctx, p, ng, e_rp.data(), e_ci.data(), e_v.data());
       extract(c_rp, c_ci, c_v, p, n, 0, p, rp, ci, v);  // F = C[p:n, 0:p]
       pc->F = upload_csr(ctx, ng, p, rp.data(), ci.data(), v.data());
     } else {
@@ -109,8 +113,8 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
       pc->shard.Cr = upload_csr(ctx, hi - lo, n, rp.data(), ci.data(), v.data());
       extract(c_rp, c_ci, c_v, p, n, p, n, rp, ci, v);  // G = C[p:n, p:n]
       pc->shard.G = upload_csr(ctx, ng, ng, rp.data(), ci.data(), v.data());
-      extract(c_rp, c_ci, c_v, lo, hi, p, n, rp, ci, v);  // E_r = C[lo:hi, p:n]
-      pc->E = upload_csr(ctx, hi - lo, ng, rp.data(), ci.data(), v.data());
+      extract(c_rp, c_ci, c_v, lo, hi, p, n, e_rp, e_ci, e_v);  // E_r = C[lo:hi, p:n]
+      pc->E = upload_csr(ctx, hi - lo, ng, e_rp.data(), e_ci.data(), e_v.data());
       extract(c_rp, c_ci, c_v, p, n, lo, hi, rp, ci, v);  // F_r = C[p:n, lo:hi]
       pc->F = upload_csr(ctx, ng, hi - lo, rp.data(), ci.data(), v.data());
     }
@@ -145,6 +149,12 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
   pc->z1 = DevBuf(sizeof(double) * std::max(1, p));
   pc->t = DevBuf(sizeof(double) * std::max(1, ng));
   pc->w = DevBuf(sizeof(double) * std::max(1, p));
+  if (pc->S && ng > 0) {
+    const int mode = ctx->correction >= 0 ? ctx->correction : correction_mode_default();
+    pc->corr = build_correction(ctx, *pc->D, e_rp.data(), e_ci.data(), e_v.data(), mode,
+                                pc->z1.as<double>(), pc->w.as<double>());
+    if (pc->corr) pc->times.corr_s = pc->corr->build_s;
+  }
   return pc;
 }
 
@@ -180,8 +190,12 @@ void Precond::apply_shard_end(const double* y, const double* tsum, double* x, cu
     block_trisolve(*S, t, x + p, nullptr, s);
     ctx->launches++;
     const int lo = shard.row_lo;
-    spmv(*E, x + p, w + lo, nullptr, 0, s);
-    block_trisolve(*D, w + lo, x + lo, z1 + lo, s);
+    if (corr) {
+      apply_correction(*corr, x + p, z1 + lo, x + lo, -1, s);
+    } else {
+      spmv(*E, x + p, w + lo, nullptr, 0, s);
+      block_trisolve(*D, w + lo, x + lo, z1 + lo, s);
+    }
     ctx->launches++;
   } else {
     MSCG_CUDA(cudaMemcpyAsync(x + shard.row_lo, z1 + shard.row_lo,
@@ -290,7 +304,7 @@ void Precond::apply_host(const double* y_h, double* x_h, double* d_y, double* d_
     block_trisolve(*S, t, d_x + p, nullptr, s);
     ctx->launches++;
     MSCG_CUDA(cudaMemcpyAsync(x_h + p, d_x + p, sizeof(double) * ng, cudaMemcpyDeviceToHost, s));
-    spmv(*E, d_x + p, w, nullptr, 0, s);
+    if (!corr) spmv(*E, d_x + p, w, nullptr, 0, s);
   }
   MSCG_CUDA(cudaEventRecord(ev_mid, s));
   // 3. per chunk: x1 = z1 - D^-1 w on those blocks, rows out
@@ -299,7 +313,10 @@ void Precond::apply_host(const double* y_h, double* x_h, double* d_y, double* d_
     rows(c, lo, hi);
     MSCG_CUDA(cudaStreamWaitEvent(side[c], ev_mid, 0));
     if (S) {
-      block_trisolve(*D, w, d_x, z1, side[c], nullptr, c);
+      if (corr)
+        apply_correction(*corr, d_x + p, z1, d_x, c, side[c]);
+      else
+        block_trisolve(*D, w, d_x, z1, side[c], nullptr, c);
       ctx->launches++;
     } else if (hi > lo) {
       MSCG_CUDA(cudaMemcpyAsync(d_x + lo, z1 + lo, sizeof(double) * (hi - lo),
@@ -333,9 +350,15 @@ void Precond::apply(const double* y, double* x, cudaStream_t s, cudaEvent_t* ev)
     block_trisolve(*S, t, x + p, nullptr, s);
     ctx->launches++;
     mark(3);
-    spmv(*E, x + p, w, nullptr, 0, s);
-    mark(4);
-    block_trisolve(*D, w, x, z1, s);
+    if (corr) {
+      // x1 = z1 - (D^-1 E) z2 with the precomputed panels (correct.cu)
+      mark(4);
+      apply_correction(*corr, x + p, z1, x, -1, s);
+    } else {
+      spmv(*E, x + p, w, nullptr, 0, s);
+      mark(4);
+      block_trisolve(*D, w, x, z1, s);
+    }
     ctx->launches++;
     mark(5);
   } else {

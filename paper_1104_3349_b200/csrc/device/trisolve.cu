@@ -672,7 +672,6 @@ size_t smem_bytes(int dim_max, int workers, int slots) {
 
 }  // namespace
 
-namespace {
 void ensure_smem(const void* kern, size_t smem) {
   static std::mutex mu;
   static std::vector<std::pair<const void*, size_t>> set;  // kernel -> attribute value
@@ -691,13 +690,13 @@ void ensure_smem(const void* kern, size_t smem) {
                                    static_cast<int>(smem)));
   set.push_back({kern, std::max<size_t>(smem, 48 * 1024)});
 }
-}  // namespace
 
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const double* sub,
-                    cudaStream_t s, long long* trace, int chunk) {
+                    cudaStream_t s, long long* trace, int chunk, const int* order, int norder) {
   if (fs.nblocks == 0) return;
+  if (order) chunk = -1;
   const int pos0 = chunk < 0 ? 0 : fs.h_chunk[chunk];
-  const int npos = chunk < 0 ? fs.nblocks : fs.h_chunk[chunk + 1] - pos0;
+  const int npos = order ? norder : (chunk < 0 ? fs.nblocks : fs.h_chunk[chunk + 1] - pos0);
   if (npos <= 0) return;
   TriArgs a;
   a.row0 = fs.row0.as<int>();
@@ -725,7 +724,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.uslot = fs.uslot.as<int>();
   a.max_slots = fs.max_slots;
   a.perm = fs.has_perm ? fs.perm.as<int>() : nullptr;
-  a.order = chunk < 0 ? fs.order.as<int>() : fs.order_chunked.as<int>();
+  a.order = order ? order : (chunk < 0 ? fs.order.as<int>() : fs.order_chunked.as<int>());
   a.pos0 = pos0;
   a.dim_max = fs.max_dim;
   a.trace = trace;

@@ -132,6 +132,15 @@ class Context:
         _check(api.lib().mscg_ctx_set_stream(self.h, C.c_void_p(stream_handle or None),
                                              int(stream_handle is None), C.byref(st)), st)
 
+    def set_correction(self, mode):
+        """Interior correction of preconditioners built later on this context:
+        "off" (the reference's E SpMV + second interior solve), "on" (W = D^-1 E
+        precomputed, x1 = z1 - W z2), "auto" (on when W saves bytes), None
+        (default: MSCG_CORRECTION or auto)."""
+        m = {"off": 0, "on": 1, "auto": 2, None: -1}[mode]
+        st = api.Status()
+        _check(api.lib().mscg_ctx_set_correction(self.h, m, C.byref(st)), st)
+
     def torch_stream(self):
         import torch
         return torch.cuda.ExternalStream(self.stream_handle, device=f"cuda:{self.device}")
@@ -253,6 +262,13 @@ class MscPreconditioner:
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         api.lib().mscg_precond_build_times(self.h, C.byref(a), C.byref(b), C.byref(c))
         return dict(ilut_s=a.value, schur_lu_s=b.value, pack_s=c.value)
+
+    def correction(self):
+        """Explicit interior correction in use: dict(on, entries, kmax, build_s)."""
+        on, k = C.c_int(), C.c_int()
+        e, t = C.c_int64(), C.c_double()
+        api.lib().mscg_precond_correction(self.h, C.byref(on), C.byref(e), C.byref(k), C.byref(t))
+        return dict(on=bool(on.value), entries=e.value, kmax=k.value, build_s=t.value)
 
     def apply(self, y):
         """x = B^-1 y.  Host ndarray in -> ndarray out; CUDA tensor in -> tensor out."""

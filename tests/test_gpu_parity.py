@@ -418,3 +418,115 @@ def test_device_oseen_assembly_cfg5_digest(msc, ctx):
     from test_host_setup import csr_digest, digest
     assert csr_digest(P.C) == js["c_sha"]
     assert digest(P.perm().astype("<i4")) == js["perm_sha"]
+
+
+def _interface_columns(pb):
+    """k_b: distinct interface columns of E in each interior block's rows."""
+    rp, ci, _ = csr_tuple(pb.C)
+    p = pb.p
+    out = []
+    for b, e in pb.d_ranges():
+        c = ci[rp[b]:rp[e]]
+        out.append((e - b, len(np.unique(c[c >= p]))))
+    return out
+
+
+@pytest.mark.parametrize("grid,nu,n_a,anchored", [(32, 0.1, 8, False), (128, 0.01, 16, False),
+                                                  (64, 0.01, 16, True), (256, 0.01, 64, True)])
+def test_correction_on_and_off_match_oracle(msc, rs, ref, grid, nu, n_a, anchored):
+    """Explicit interior correction (csrc/device/correct.cu): x1 = z1 - W z2
+    with W = D^-1 E precomputed per block.  Same operator as the reference's
+    w = E z2, x1 = z1 - D^-1 w (preconditioner.cpp:105-111); both modes must
+    meet the apply bar against the oracle and agree with each other."""
+    import torch
+    pb = msc.oseen_problem(grid, nu, n_a, anchored=anchored)
+    if anchored:
+        pb.build_msc("lum", sz=40, mode="anchored")
+    else:
+        pb.build_msc("lum")
+    M = oracle_msc(rs, pb, 1e-4, 0)
+    out = {}
+    for mode in ("off", "on"):
+        c = msc.Context(0)
+        c.set_correction(mode)
+        pc = msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=c)
+        info = pc.correction()
+        assert info["on"] == (mode == "on")
+        if info["on"]:
+            kb = _interface_columns(pb)
+            assert info["entries"] == sum(d * k for d, k in kb)
+            assert info["kmax"] == max(k for _, k in kb)
+        # the reference's stored_nnz does not count the panels
+        assert pc.stored_nnz() == M.stored_nnz
+        ys = [ref.random_vector(pb.n, s) for s in (0, 5)]
+        xs = [pc.apply(y) for y in ys]
+        for y, x in zip(ys, xs):
+            assert rel_err(x, M.apply(y)) <= APPLY_TOL
+        # host-buffer (chunked) path bit-identical to the device path
+        xd = pc.apply(torch.from_numpy(ys[0]).cuda()).cpu().numpy()
+        assert same_bits(xs[0], xd)
+        # deterministic
+        assert same_bits(pc.apply(ys[0]), xs[0])
+        out[mode] = xs[0]
+        del pc
+    assert rel_err(out["on"], out["off"]) <= 1e-12
+
+
+def test_correction_sharded_matches_full(msc, ref):
+    """Shards build their own panels from their rows of E."""
+    import torch
+    from paper_1104_3349_b200 import dist
+    c = msc.Context(0)
+    c.set_correction("on")
+    pb = msc.oseen_problem(128, 0.01, 16)
+    pb.build_msc("lum")
+    full = msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=c)
+    assert full.correction()["on"]
+    dr = pb.d_ranges()
+    ranges = dist.shard_blocks(dr[:, 1] - dr[:, 0], 2)
+    c.set_stream(torch.cuda.current_stream().cuda_stream)
+    try:
+        shards = [msc.build_preconditioner_shard(pb, b0, b1, tolA=1e-4, sA=0, ctx=c)
+                  for b0, b1 in ranges]
+        n, p = pb.n, pb.p
+        y_h = ref.random_vector(n, 4)
+        want = full.apply(y_h)
+        y = torch.from_numpy(y_h).cuda()
+        ts = [torch.empty(n - p, dtype=torch.float64, device="cuda") for _ in shards]
+        xs = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in shards]
+        for s, t in zip(shards, ts):
+            s.apply_begin(y, t)
+        tsum = torch.stack(ts).sum(0)
+        for s, x in zip(shards, xs):
+            s.apply_end(y, tsum, x)
+        got = np.empty(n)
+        for s, x in zip(shards, xs):
+            lo, hi = s.rows
+            got[lo:hi] = x[lo:hi].cpu().numpy()
+        got[p:] = xs[0][p:].cpu().numpy()
+        assert rel_err(got, want) <= 1e-12
+    finally:
+        c.set_stream(None)
+
+
+@pytest.mark.parametrize("mode", ["off", "on"])
+def test_gmres_cfg1_iterations_both_corrections(msc, cfg1, cfg1_oracle, ref, rs, mode):
+    c = msc.Context(0)
+    c.set_correction(mode)
+    pc = msc.build_preconditioner(cfg1, tolA=1e-4, sA=0, ctx=c)
+    assert pc.correction()["on"] == (mode == "on")
+    b = ref.random_vector(cfg1.n, 0)
+    x, rep = msc.gmres(pc.matrix, pc, b, msc.SolverConfig(restart=30, max_iters=3000,
+                                                          rel_tol=1e-8))
+    assert abs(rep.iterations - 88) <= 1
+    assert rep.converged and msc.true_residual(pc.matrix, x, b) <= 1e-8
+
+
+def test_set_correction_rejects_bad_mode(msc):
+    c = msc.Context(0)
+    with pytest.raises(KeyError):
+        c.set_correction("sometimes")
+    import ctypes as C
+    from paper_1104_3349_b200 import _capi
+    st = _capi.Status()
+    assert _capi.lib().mscg_ctx_set_correction(c.h, 7, C.byref(st)) != 0
