@@ -70,8 +70,22 @@ def main():
     go = os.path.join(ROOT, "gpurun_out")
     prof = os.path.join(ROOT, "profiles")
     per, seq = launches(os.path.join(go, f"{tag}_launches_{cfg}.csv"))
-    # one apply step = the last 6 launches of the list (d, f, s, e, d_sub, c spmv)
-    step = seq[-6:]
+    # one apply step = 6 launches (d, f, s, e, d_sub, c spmv), or 5 with the
+    # explicit correction (d, f, s, correct, c spmv): the last device-buffer
+    # step (the e2e host-buffer calls that follow run in chunks and do not
+    # match the pattern).
+    names = [k for k, _ in seq]
+    pat5 = ["trisolve", "sell_spmv", "trisolve", "correct_kernel", "sell_spmv"]
+    pat6 = ["trisolve", "sell_spmv"] * 3
+    step = []
+    for i in range(len(seq) - 5, -1, -1):
+        for pat in (pat5, pat6):
+            if i + len(pat) <= len(seq) and all(names[i + j].startswith(pat[j])
+                                                for j in range(len(pat))):
+                step = seq[i:i + len(pat)]
+                break
+        if step:
+            break
     tot = sum(ns for _, ns in step)
     summ = {
         "source": f"ncu --metrics gpu__time_duration.sum --clock-control none (serialised, "
@@ -86,11 +100,22 @@ def main():
     json.dump(d, open(os.path.join(prof, f"{tag}_ncu_trisolve_{cfg}.json"), "w"), indent=1)
     rd = float(d["dram__bytes_read.sum"]["value"]) * UNIT[d["dram__bytes_read.sum"]["unit"]]
     wr = float(d["dram__bytes_write.sum"]["value"]) * UNIT[d["dram__bytes_write.sum"]["unit"]]
+    tri_bytes = rd + wr
     json.dump({"config": cfg, "dram_bytes_per_launch": rd + wr,
                "source": f"profiles/{tag}_ncu_trisolve_{cfg}.json (ncu --set full, one launch)"},
               open(os.path.join(prof, "trisolve_traffic.json"), "w"), indent=1)
+    rep = os.path.join(go, f"{tag}_correct_{cfg}.ncu-rep")
+    if os.path.exists(rep):
+        d = full(rep)
+        json.dump(d, open(os.path.join(prof, f"{tag}_ncu_correct_{cfg}.json"), "w"), indent=1)
+        rd = float(d["dram__bytes_read.sum"]["value"]) * UNIT[d["dram__bytes_read.sum"]["unit"]]
+        wr = float(d["dram__bytes_write.sum"]["value"]) * UNIT[d["dram__bytes_write.sum"]["unit"]]
+        json.dump({"config": cfg, "dram_bytes_per_launch": rd + wr,
+                   "source": f"profiles/{tag}_ncu_correct_{cfg}.json (ncu --set full, one launch)"},
+                  open(os.path.join(prof, "correct_traffic.json"), "w"), indent=1)
+        print("correct dram bytes/launch", rd + wr)
     print(json.dumps(summ["last_step"], indent=1))
-    print("trisolve dram bytes/launch", rd + wr)
+    print("trisolve dram bytes/launch", tri_bytes)
 
 
 if __name__ == "__main__":
