@@ -20,7 +20,8 @@
 //
 // Layout: per block, W_b column-major (column k = dim_b consecutive fp64),
 // blocks back to back; cols_b ascending interface columns (int32).  A work
-// item is (block, 512-row slice); a CTA of 256 threads owns one item, stages
+// item is (block, 512-row slice; 256 or 128 when there are too few blocks to
+// fill the GPU); a CTA of 256 threads owns one item, stages
 // z2[cols_b] in shared memory and each thread accumulates rows i and i+256
 // over k in ascending order (one fma per entry, deterministic).  Roofline:
 // HBM, 8 B per W entry (read once per apply, streaming loads so W does not
@@ -76,14 +77,16 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(
     const int* __restrict__ dim, const long long* __restrict__ woff,
     const int* __restrict__ wcoff, const int* __restrict__ wcols,
     const double* __restrict__ W, const double* __restrict__ x2,
-    const double* __restrict__ z1, double* __restrict__ out) {
+    const double* __restrict__ z1, double* __restrict__ out, int slice) {
   extern __shared__ double zs[];
   const int2 it = items[item0 + blockIdx.x];
   const int b = it.x, i0 = it.y;
   const int c0 = wcoff[b], kb = wcoff[b + 1] - c0;
   for (int k = threadIdx.x; k < kb; k += kCorrThreads) zs[k] = __ldg(x2 + __ldg(wcols + c0 + k));
   __syncthreads();
-  const int d = dim[b], r0 = row0[b];
+  const int r0 = row0[b];
+  const int d = dim[b], de = min(d, i0 + slice);  // rows [i0, de) of this item
+  if (static_cast<int>(threadIdx.x) >= slice) return;
   const int ia = i0 + threadIdx.x, ib = ia + kCorrThreads;
   // rows past the block read a valid row (clamped, same sectors as their
   // neighbours) and are not written; the second row is walked only by warps
@@ -92,12 +95,12 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(
   const double* wa = wbase + min(ia, d - 1);
   const double* wb = wbase + min(ib, d - 1);
   double a0 = 0.0, a1 = 0.0;
-  if (i0 + kCorrThreads + static_cast<int>(threadIdx.x & ~31u) < d)
+  if (i0 + kCorrThreads + static_cast<int>(threadIdx.x & ~31u) < de)
     corr_rows<true>(wa, wb, d, kb, zs, a0, a1);
   else
     corr_rows<false>(wa, wb, d, kb, zs, a0, a1);
-  if (ia < d) out[r0 + ia] = __dsub_rn(z1[r0 + ia], a0);
-  if (ib < d) out[r0 + ib] = __dsub_rn(z1[r0 + ib], a1);
+  if (ia < de) out[r0 + ia] = __dsub_rn(z1[r0 + ia], a0);
+  if (ib < de) out[r0 + ib] = __dsub_rn(z1[r0 + ib], a1);
 }
 
 // Setup: r[row0_b + rows of column k of E_b] = values (or 0 when clearing).
@@ -213,12 +216,19 @@ std::unique_ptr<Correction> build_correction(Ctx* ctx, const FactorSet& D, const
   c->wcols = upload(wcols, s);
   c->wval = DevBuf(sizeof(double) * std::max<int64_t>(1, c->entries));
   // work items (block, slice) in block order; chunk c = blocks h_chunk[c]..
+  // slices of 512 rows (two per thread); fewer blocks than fill the GPU
+  // (cfg1/cfg2) get slices of 256 or 128 rows so every SM has items
+  int sms = 148, dev = 0;
+  MSCG_CUDA(cudaGetDevice(&dev));
+  MSCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  c->slice = kCorrSlice;
+  while (c->slice > 128 && static_cast<int64_t>(D.total_rows) / c->slice < 4 * sms) c->slice /= 2;
   std::vector<int2> items;
   c->h_item_chunk.assign(kSolveChunks + 1, 0);
   for (int ch = 0; ch < kSolveChunks; ++ch) {
     c->h_item_chunk[ch] = static_cast<int>(items.size());
     for (int b = D.h_chunk[ch]; b < D.h_chunk[ch + 1]; ++b)
-      for (int i = 0; i < D.h_dim[b]; i += kCorrSlice) items.push_back(make_int2(b, i));
+      for (int i = 0; i < D.h_dim[b]; i += c->slice) items.push_back(make_int2(b, i));
   }
   c->h_item_chunk[kSolveChunks] = static_cast<int>(items.size());
   c->items = upload(items, s);
@@ -262,7 +272,7 @@ void apply_correction(const Correction& c, const double* x2, const double* z1, d
   ensure_smem(reinterpret_cast<const void*>(correct_kernel), smem);
   correct_kernel<<<i1 - i0, kCorrThreads, smem, s>>>(
       c.items.as<int2>(), i0, c.row0, c.dim, c.woff.as<long long>(), c.wcoff.as<int>(),
-      c.wcols.as<int>(), c.wval.as<double>(), x2, z1, out);
+      c.wcols.as<int>(), c.wval.as<double>(), x2, z1, out, c.slice);
   MSCG_CUDA(cudaGetLastError());
 }
 

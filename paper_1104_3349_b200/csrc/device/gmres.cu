@@ -62,6 +62,20 @@ __device__ __forceinline__ bool last_block(Reducer red) {
 // out[i] (i < nvec) = sum over CTAs of partials[i][cta]; scale: out = f(sum).
 __device__ void finish(Reducer red, int nvec, double* out, int mode) {
   __threadfence();
+  if (nvec == 1 && red.nblk <= 1024) {
+    // one sum (norms): stage the partials in shared memory with one coalesced
+    // round trip, then add them in CTA order (same order as below)
+    __shared__ double stage[1024];
+    for (int c = threadIdx.x; c < red.nblk; c += blockDim.x) stage[c] = __ldcg(red.partials + c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int c = 0; c < red.nblk; ++c) s += stage[c];
+      out[0] = mode == 1 ? sqrt(s) : s;
+      *red.counter = 0u;
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     double s = 0.0;
     for (int c = 0; c < red.nblk; ++c) s += red.partials[static_cast<size_t>(i) * red.nblk + c];
@@ -75,8 +89,17 @@ __global__ void __launch_bounds__(kThreads) nrm2_kernel(int n, const double* __r
                                                         Reducer red, double* out) {
   __shared__ double sh[kThreads / 32];
   double acc = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    acc = fma(x[i], x[i], acc);
+  // grid-stride, four loads in flight per thread (summation order unchanged)
+  const int stride = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    const double a = x[i], b = x[i + stride], c = x[i + 2 * stride], d = x[i + 3 * stride];
+    acc = fma(a, a, acc);
+    acc = fma(b, b, acc);
+    acc = fma(c, c, acc);
+    acc = fma(d, d, acc);
+  }
+  for (; i < n; i += stride) acc = fma(x[i], x[i], acc);
   const double s = block_sum(acc, sh);
   if (threadIdx.x == 0) red.partials[blockIdx.x] = s;
   if (last_block(red)) finish(red, 1, out, 1);

@@ -251,7 +251,8 @@ struct Correction {
   DevBuf wcoff;                // int32[nblocks+1] column-list offsets
   DevBuf wcols;                // int32 interface columns per block, ascending
   DevBuf wval;                 // fp64 panels
-  DevBuf items;                // int2 {block, first row} (512-row slices)
+  DevBuf items;                // int2 {block, first row} (slices of `slice` rows)
+  int slice = 512;
   std::vector<int> h_item_chunk;  // item range of block chunk c
   double build_s = 0;
 };
