@@ -532,10 +532,14 @@ def test_set_correction_rejects_bad_mode(msc):
     assert _capi.lib().mscg_ctx_set_correction(c.h, 7, C.byref(st)) != 0
 
 
-def test_cfg4_scale_apply_parity(msc, ctx, ref):
-    """BASELINE cfg4 at full size (1024^2, 1024 blocks, anchored LUM sz 256).
+@pytest.mark.parametrize("grid,nu,n_a,sample", [
+    (1024, 0.001, 1024, (0, 511, 1023)),   # BASELINE cfg4
+    (2048, 0.01, 4096, (0, 2047, 4095)),   # BASELINE cfg5
+])
+def test_full_scale_apply_parity(msc, ctx, ref, grid, nu, n_a, sample):
+    """BASELINE cfg4 / cfg5 at full size (anchored LUM sz 256).
     The CPU reference cannot build the whole preconditioner in test time
-    (~580 s of ILUT), so parity is checked block by block on a sample:
+    (cfg4: ~580 s of ILUT), so parity is checked block by block on a sample:
       * the reference's own factor_ilut on the sampled block gives the same
         factors (pattern + bits) as the GPU;
       * x1_b = solve(y1_b) - solve(E_b x2) with the reference's solve, given
@@ -543,7 +547,7 @@ def test_cfg4_scale_apply_parity(msc, ctx, ref):
         (with and without the explicit correction);
       * both correction modes agree over the whole vector to 1e-12."""
     import torch
-    pb = msc.oseen_problem(1024, 0.001, 1024, anchored=True, ctx=ctx)
+    pb = msc.oseen_problem(grid, nu, n_a, anchored=True, ctx=ctx)
     pb.build_msc("lum", sz=256, mode="anchored", ctx=ctx)
     n, p = pb.n, pb.p
     rp, ci, v = csr_tuple(pb.C)
@@ -557,7 +561,7 @@ def test_cfg4_scale_apply_parity(msc, ctx, ref):
         assert pc.correction()["on"] == (mode == "on")
         xs[mode] = pc.apply(torch.from_numpy(y).cuda()).cpu().numpy()
         if mode == "on":
-            facs = {int(b): pc.d_factors(int(b)) for b in (0, 511, 1023)}
+            facs = {int(b): pc.d_factors(int(b)) for b in sample}
         del pc
         torch.cuda.empty_cache()
     assert rel_err(xs["on"], xs["off"]) <= 1e-12
