@@ -13,6 +13,9 @@
 // (= depth-first) order, so the block list and separator are identical.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <thread>
 
@@ -78,10 +81,13 @@ struct Graph {
   int deg(int u) const { return static_cast<int>(off[u + 1] - off[u]); }
 };
 
+// Per-thread scratch.  st[v] packs (piece epoch << 32 | visited epoch) so the
+// BFS membership and visited tests are one random access per edge.
 struct Scratch {
-  std::vector<int> mem, vis, lev, left;
+  std::vector<uint64_t> st;
+  std::vector<int> left;
   int epoch = 0;
-  explicit Scratch(int n) : mem(n, 0), vis(n, 0), lev(n, 0), left(n, 0) {}
+  explicit Scratch(int n) : st(n, 0), left(n, 0) {}
 };
 
 struct LevelOrder {
@@ -89,25 +95,44 @@ struct LevelOrder {
 };
 
 // bfs_levels (graph.cpp:70-92).  When only_first is set, stop after the
-// start's component (all pseudo_peripheral needs).
+// start's component (all pseudo_peripheral needs).  Visit order and levels
+// are the reference's: FIFO queue, neighbours in adjacency order; levels are
+// read off the queue's level boundaries.  The queue runs ahead with software
+// prefetches (adjacency lists kPfAdj nodes ahead, their neighbours' state
+// kPfSt nodes ahead): the walk is bound by random accesses to st[].
 void bfs_levels(const Graph& g, const std::vector<int>& nodes, Scratch& s,
                 int mem_ep, int start, bool only_first, LevelOrder& lo) {
-  const int ep = ++s.epoch;
+  constexpr std::size_t kPfAdj = 16, kPfSt = 6;
+  const uint32_t ep = static_cast<uint32_t>(++s.epoch);
+  const uint64_t mem_hi = static_cast<uint64_t>(static_cast<uint32_t>(mem_ep)) << 32;
+  uint64_t* st = s.st.data();
+  const int64_t* off = g.off.data();
+  const int* adj = g.adj.data();
   lo.order.clear();
   lo.level.clear();
   auto run = [&](int src) {
     std::size_t head = lo.order.size();
-    s.vis[src] = ep;
-    s.lev[src] = 0;
+    st[src] = mem_hi | ep;
     lo.order.push_back(src);
+    int level = 0;
+    std::size_t level_end = head + 1;
     while (head < lo.order.size()) {
+      if (head == level_end) {
+        ++level;
+        level_end = lo.order.size();
+      }
+      if (head + kPfAdj < lo.order.size()) __builtin_prefetch(adj + off[lo.order[head + kPfAdj]]);
+      if (head + kPfSt < lo.order.size()) {
+        const int w = lo.order[head + kPfSt];
+        for (int64_t k = off[w]; k < off[w + 1]; ++k) __builtin_prefetch(st + adj[k]);
+      }
       const int u = lo.order[head++];
-      lo.level.push_back(s.lev[u]);
-      for (int64_t k = g.off[u]; k < g.off[u + 1]; ++k) {
-        const int v = g.adj[k];
-        if (s.mem[v] == mem_ep && s.vis[v] != ep) {
-          s.vis[v] = ep;
-          s.lev[v] = s.lev[u] + 1;
+      lo.level.push_back(level);
+      for (int64_t k = off[u]; k < off[u + 1]; ++k) {
+        const int v = adj[k];
+        const uint64_t sv = st[v];
+        if ((sv & 0xffffffff00000000ull) == mem_hi && static_cast<uint32_t>(sv) != ep) {
+          st[v] = mem_hi | ep;
           lo.order.push_back(v);
         }
       }
@@ -116,7 +141,7 @@ void bfs_levels(const Graph& g, const std::vector<int>& nodes, Scratch& s,
   if (start >= 0) run(start);
   if (only_first) return;
   for (int u : nodes)
-    if (s.vis[u] != ep) run(u);
+    if (static_cast<uint32_t>(st[u]) != ep) run(u);
 }
 
 struct Split {
@@ -127,7 +152,8 @@ struct Split {
 // bisect (graph.cpp:136-176) with pseudo_peripheral (graph.cpp:94-117).
 Split bisect(const Graph& g, const std::vector<int>& nodes, Scratch& s) {
   const int mem_ep = ++s.epoch;
-  for (int u : nodes) s.mem[u] = mem_ep;
+  const uint64_t mem_hi = static_cast<uint64_t>(static_cast<uint32_t>(mem_ep)) << 32;
+  for (int u : nodes) s.st[u] = mem_hi;  // member, not visited
   int start = nodes.front();
   int best = g.deg(start);
   for (int u : nodes)
@@ -136,6 +162,8 @@ Split bisect(const Graph& g, const std::vector<int>& nodes, Scratch& s) {
       start = u;
     }
   LevelOrder lo;
+  lo.order.reserve(nodes.size());
+  lo.level.reserve(nodes.size());
   bfs_levels(g, nodes, s, mem_ep, start, true, lo);
   const int f1 = lo.order.back();
   bfs_levels(g, nodes, s, mem_ep, f1, true, lo);
@@ -149,25 +177,31 @@ Split bisect(const Graph& g, const std::vector<int>& nodes, Scratch& s) {
     ++cut;
   Split r;
   const int lep = ++s.epoch;
-  for (std::size_t i = 0; i < lo.order.size(); ++i) {
-    if (i < cut) {
-      r.left.push_back(lo.order[i]);
-      s.left[lo.order[i]] = lep;
-    }
-  }
+  const int sep_ep = ++s.epoch;
+  for (std::size_t i = 0; i < cut && i < lo.order.size(); ++i) s.left[lo.order[i]] = lep;
+  std::size_t nleft = std::min(cut, lo.order.size()), nsep = 0;
   for (std::size_t i = cut; i < lo.order.size(); ++i) {
     const int u = lo.order[i];
-    bool boundary = false;
+    if (i + 6 < lo.order.size()) {
+      const int w = lo.order[i + 6];
+      for (int64_t k = g.off[w]; k < g.off[w + 1]; ++k) __builtin_prefetch(&s.left[g.adj[k]]);
+    }
     for (int64_t k = g.off[u]; k < g.off[u + 1]; ++k)
       if (s.left[g.adj[k]] == lep) {
-        boundary = true;
+        s.left[u] = sep_ep;
+        ++nsep;
         break;
       }
-    (boundary ? r.sep : r.right).push_back(u);
   }
-  std::sort(r.left.begin(), r.left.end());
-  std::sort(r.right.begin(), r.right.end());
-  std::sort(r.sep.begin(), r.sep.end());
+  // the piece's node list is ascending, so one pass over it yields the three
+  // sorted sides without sorting
+  r.left.reserve(nleft);
+  r.sep.reserve(nsep);
+  r.right.reserve(nodes.size() - nleft - nsep);
+  for (int u : nodes) {
+    const int m = s.left[u];
+    (m == lep ? r.left : m == sep_ep ? r.sep : r.right).push_back(u);
+  }
   r.degenerate = r.left.empty() || r.right.empty();
   return r;
 }
@@ -194,6 +228,8 @@ void nested_dissection(const Graph& g, int target_blocks, int threads,
   }
   int depth = 0;
   while ((1 << depth) < target_blocks) ++depth;
+  static const bool verbose = getenv("MSCG_VERBOSE") != nullptr;
+  auto tl = std::chrono::steady_clock::now();
   std::vector<Piece> pieces(1);
   pieces[0].nodes.resize(g.n);
   for (int i = 0; i < g.n; ++i) pieces[0].nodes[i] = i;
@@ -233,6 +269,12 @@ void nested_dissection(const Graph& g, int target_blocks, int threads,
       next.push_back(Piece{std::move(sp.right), false});
     }
     pieces = std::move(next);
+    if (verbose) {
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "nested_dissection: level %d, %zu pieces, %.3f s\n", d, todo.size(),
+              std::chrono::duration<double>(now - tl).count());
+      tl = now;
+    }
   }
   std::sort(separator.begin(), separator.end());
   for (auto& pc : pieces) blocks.push_back(std::move(pc.nodes));
@@ -246,6 +288,7 @@ Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads
   if (threads <= 0) threads = hardware_threads();
   const int n = c.nrows;
   const int ng = n - p;
+  const auto t_start = std::chrono::steady_clock::now();
 
   // attached[q]: first-block nodes coupled to second-block unknown q
   // (partitioned_matrix.cpp:112-124), as a sorted, unique CSR list.
@@ -327,9 +370,16 @@ Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads
     std::copy(raw.begin() + cnt[i], raw.begin() + cnt[i] + ulen[i], g.adj.begin() + g.off[i]);
   std::vector<int>().swap(raw);
 
+  static const bool verbose = getenv("MSCG_VERBOSE") != nullptr;
+  const auto tg = std::chrono::steady_clock::now();
+  if (verbose)
+    fprintf(stderr, "partition_saddle: enriched graph %d nodes, %lld edges, %.3f s\n", p,
+            static_cast<long long>(g.off[p]),
+            std::chrono::duration<double>(tg - t_start).count());
   std::vector<std::vector<int>> blocks;
   std::vector<int> separator;
   nested_dissection(g, target_blocks, threads, blocks, separator);
+  const auto tn = std::chrono::steady_clock::now();
 
   // Second-block unknowns follow their interior couplings
   // (partitioned_matrix.cpp:146-175).
@@ -387,6 +437,10 @@ Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads
   if (bad)
     throw std::runtime_error("partition_saddle: interior blocks remained coupled (" +
                              std::to_string(bad) + " entries)");
+  if (verbose)
+    fprintf(stderr, "partition_saddle: dissection %.3f s, permutation %.3f s\n",
+            std::chrono::duration<double>(tn - tg).count(),
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - tn).count());
   return out;
 }
 
