@@ -172,14 +172,23 @@ def algorithmic_bytes(pc, cnt):
     return dict(d_solve=d_solve, apply=apply_b, spmv=spmv_b, d_lu_nnz=d_lu, s_lu_nnz=s_lu)
 
 
-def correction_line(corr, pc, ms, peak):
+def correction_line(corr, pc, ms, peak, config):
     """The explicit interior correction x1 = z1 - W z2 (W = D^-1 E per block,
     csrc/device/correct.cu): 8 B per panel entry + the z1 read / x1 write."""
     if not corr["on"]:
         return {"on": False}
     b = 8 * corr["entries"] + 16 * pc.p
     gbs = b / (ms / 1e3) / 1e9
-    return {"on": True, "kernel": "correct_kernel (W = D^-1 E panel GEMV)",
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "correct_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            if tj.get("config") == config:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    return {"on": True, "kernel": "correct_kernel (W = D^-1 E panel GEMV)", "traffic": traffic,
             "panel_entries": corr["entries"], "kmax": corr["kmax"],
             "build_s": corr["build_s"], "ms": ms, "algorithmic_bytes": b,
             "achieved_gbs": gbs, "frac": gbs / peak}
@@ -595,7 +604,7 @@ def main():
             "stage_ms": {k: v / args.steps for k, v in zip(
                 ["d_solve", "f_spmv", "s_solve", "e_spmv",
                  "correction" if corr["on"] else "d_solve_sub", "c_spmv"], stage_ms)},
-            "correction": correction_line(corr, pc, stage_ms[4] / args.steps, peak),
+            "correction": correction_line(corr, pc, stage_ms[4] / args.steps, peak, args.config),
             "factor_nnz": {"interior_LU": ab["d_lu_nnz"], "schur_LU": ab["s_lu_nnz"]},
             "setup": setup,
         }
