@@ -2,7 +2,7 @@
 //
 // The Arnoldi step keeps every vector in HBM and every scalar on the device:
 //   w = A B^-1 v_j            (precond apply + SELL SpMV, right preconditioning)
-//   orthogonalisation         CGS2: two fused multi-dot + multi-axpy passes
+//   orthogonalisation         CGS2: multi-dot, fused axpy+dot, multi-axpy
 //                             (h = V^T w; w -= V h, twice), or MGS in the
 //                             reference's order (one fused axpy+dot kernel per
 //                             basis vector)
@@ -194,6 +194,81 @@ __global__ void __launch_bounds__(kThreads) multiaxpy_kernel(int n, int nv, cons
   }
   if (blockIdx.x == 0 && hcol)
     for (int i = threadIdx.x; i < nv; i += blockDim.x) hcol[i] = accumulate ? hcol[i] + sh[i] : sh[i];
+}
+
+// CGS2 middle step, fused: w -= V h (first pass's projection, same per-row
+// arithmetic as multiaxpy_kernel) and h2 = V^T w (second pass's dots) in one
+// sweep, so the basis streams from HBM three times per Arnoldi step instead of
+// four (the dot re-reads the rows this thread just loaded: L1/L2 hits).  Per
+// row pair the 32 products of a group of 32 basis vectors are reduced across
+// the warp by a transposing butterfly (31 shuffles; lane k ends with vector
+// 32g + k), accumulated per warp in shared memory, then per CTA into the
+// partials, which the last CTA sums in CTA order (deterministic).  CTA 0
+// stores H(:,j) = h.
+__global__ void __launch_bounds__(kThreads) axpy_dot_kernel(int n, int nv, const double* __restrict__ V,
+                                                            size_t ld, const double* __restrict__ h,
+                                                            double* __restrict__ w, double* hcol,
+                                                            Reducer red, double* hout) {
+  __shared__ double sh[512];
+  __shared__ double acc_sh[kThreads / 32][512];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) sh[i] = h[i];
+  for (int i = lane; i < nv; i += 32) acc_sh[warp][i] = 0.0;
+  __syncthreads();
+  const int npair = n >> 1;
+  double2* w2 = reinterpret_cast<double2*>(w);
+  const int stride = gridDim.x * blockDim.x;
+  for (int qb = blockIdx.x * blockDim.x; qb < npair; qb += stride) {  // CTA-uniform trip count
+    const int q = qb + threadIdx.x;
+    const bool on = q < npair;
+    double2 acc = make_double2(0.0, 0.0);
+    if (on) {
+      acc = w2[q];
+      for (int i = 0; i < nv; ++i) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(V + ld * i) + q);
+        acc.x = fma(-sh[i], v.x, acc.x);
+        acc.y = fma(-sh[i], v.y, acc.y);
+      }
+      w2[q] = acc;
+    }
+    for (int g0 = 0; g0 < nv; g0 += 32) {
+      double p[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int i = g0 + k;
+        double2 v = make_double2(0.0, 0.0);
+        if (on && i < nv) v = __ldg(reinterpret_cast<const double2*>(V + ld * i) + q);
+        p[k] = fma(v.y, acc.y, v.x * acc.x);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const bool hi = lane & off;
+#pragma unroll
+        for (int k = 0; k < off; ++k) {
+          const double send = hi ? p[k] : p[k + off];
+          const double keep = hi ? p[k + off] : p[k];
+          p[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      if (g0 + lane < nv) acc_sh[warp][g0 + lane] += p[0];
+    }
+  }
+  __syncthreads();
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: the last row
+    double a = w[n - 1];
+    for (int i = 0; i < nv; ++i) a = fma(-sh[i], V[ld * i + (n - 1)], a);
+    w[n - 1] = a;
+    for (int i = 0; i < nv; ++i) acc_sh[0][i] = fma(V[ld * i + (n - 1)], a, acc_sh[0][i]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double t = 0.0;
+    for (int k = 0; k < kThreads / 32; ++k) t += acc_sh[k][i];
+    red.partials[static_cast<size_t>(i) * red.nblk + blockIdx.x] = t;
+  }
+  if (blockIdx.x == 0 && hcol)
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hcol[i] = sh[i];
+  if (last_block(red)) finish(red, nv, hout, 0);
 }
 
 // MGS step (reference order, gmres.cpp:112-116), fused: apply the previous
@@ -388,7 +463,10 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   st.scal = st.y + (m + 1);
   st.status = st.scal + 16;
   double* hbuf = st.scal + 32;  // scratch for multidot results (<= m+1)
-  DevBuf hscratch(sizeof(double) * (m + 2));
+  DevBuf hscratch(sizeof(double) * 2 * (m + 2));
+  // MSCG_CGS2_FUSED=0: the four-sweep CGS2 (two multi-dot + multi-axpy pairs)
+  const char* fused_env = std::getenv("MSCG_CGS2_FUSED");
+  const bool cgs2_fused = !(fused_env && fused_env[0] == '0');
   // page-locked status slots (two iterations in flight) and their events
   struct HostStatus {
     double* p = nullptr;
@@ -480,6 +558,16 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
         ctx->launches++;
       } else {
         // CGS2: h = V^T w; w -= V h; twice, H(:,j) = h1 + h2.
+        if (cgs2_fused) {
+          // dot, fused axpy + dot, axpy: three sweeps over the basis
+          multidot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
+                                                 hscratch.as<double>());
+          axpy_dot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, hscratch.as<double>(), wp,
+                                                 Hc, ws.red, hscratch.as<double>() + (m + 2));
+          multiaxpy_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld,
+                                                  hscratch.as<double>() + (m + 2), wp, Hc, 1);
+          ctx->launches += 3;
+        } else
         for (int pass = 0; pass < 2; ++pass) {
           multidot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
                                                  hscratch.as<double>());
