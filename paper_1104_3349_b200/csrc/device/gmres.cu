@@ -224,14 +224,35 @@ __global__ void __launch_bounds__(kThreads) axpy_dot_kernel(int n, int nv, const
     double2 acc = make_double2(0.0, 0.0);
     if (on) {
       acc = w2[q];
-      for (int i = 0; i < nv; ++i) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(V + ld * i) + q);
-        acc.x = fma(-sh[i], v.x, acc.x);
-        acc.y = fma(-sh[i], v.y, acc.y);
+      // software-pipelined: the next kU rows are in flight while the current
+      // kU are applied (same i-ascending order as multiaxpy_kernel)
+      constexpr int kU = 16;
+      double2 cur[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        cur[u] = u < nv ? __ldg(reinterpret_cast<const double2*>(V + ld * u) + q)
+                        : make_double2(0.0, 0.0);
+      for (int i0 = 0; i0 < nv; i0 += kU) {
+        double2 nxt[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int i = i0 + kU + u;
+          nxt[u] = i < nv ? __ldg(reinterpret_cast<const double2*>(V + ld * i) + q)
+                          : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (i0 + u < nv) {
+            acc.x = fma(-sh[i0 + u], cur[u].x, acc.x);
+            acc.y = fma(-sh[i0 + u], cur[u].y, acc.y);
+          }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) cur[u] = nxt[u];
       }
       w2[q] = acc;
     }
-    for (int g0 = 0; g0 < nv; g0 += 32) {
+    // groups last to first: the rows loaded last are the likeliest L2 hits
+    for (int g0 = (nv - 1) & ~31; g0 >= 0; g0 -= 32) {
       double p[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
@@ -467,6 +488,13 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   // MSCG_CGS2_FUSED=0: the four-sweep CGS2 (two multi-dot + multi-axpy pairs)
   const char* fused_env = std::getenv("MSCG_CGS2_FUSED");
   const bool cgs2_fused = !(fused_env && fused_env[0] == '0');
+  // The fused kernel re-reads each thread's basis rows after its axpy: fewer
+  // resident rows keep that footprint (rows x (j+1) x 8 B) inside L2.
+  const char* cps_env = std::getenv("MSCG_AXPYDOT_CPS");
+  const int cps = cps_env ? std::max(1, std::atoi(cps_env)) : 1;
+  const int G_ad = std::max(1, std::min(G, ctx->sm_count * cps));
+  Reducer red_ad = ws.red;
+  red_ad.nblk = G_ad;
   // page-locked status slots (two iterations in flight) and their events
   struct HostStatus {
     double* p = nullptr;
@@ -562,8 +590,8 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
           // dot, fused axpy + dot, axpy: three sweeps over the basis
           multidot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
                                                  hscratch.as<double>());
-          axpy_dot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, hscratch.as<double>(), wp,
-                                                 Hc, ws.red, hscratch.as<double>() + (m + 2));
+          axpy_dot_kernel<<<G_ad, kThreads, 0, s>>>(n, j + 1, vbase, ld, hscratch.as<double>(), wp,
+                                                    Hc, red_ad, hscratch.as<double>() + (m + 2));
           multiaxpy_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld,
                                                   hscratch.as<double>() + (m + 2), wp, Hc, 1);
           ctx->launches += 3;
