@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(kThreads) nrm2_kernel(int n, const double* __r
 // read once per group and each CTA reduces kDotGroup sums per pass.  Rows
 // go in 16-byte pairs (the basis is stored with a 32-element-aligned
 // leading dimension), two pairs in flight per thread.
-constexpr int kDotGroup = 8;
+// Groups of 16 (184 registers, one CTA per SM) halve the w re-reads on long
+// vectors; short ones keep groups of 8 (two CTAs per SM, one wave).
+template <int kDotGroup>
 __global__ void __launch_bounds__(kThreads) multidot_kernel(int n, int nv, const double* __restrict__ V,
                                                             size_t ld, const double* __restrict__ w,
                                                             Reducer red, double* h) {
@@ -488,6 +490,7 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   // MSCG_CGS2_FUSED=0: the four-sweep CGS2 (two multi-dot + multi-axpy pairs)
   const char* fused_env = std::getenv("MSCG_CGS2_FUSED");
   const bool cgs2_fused = !(fused_env && fused_env[0] == '0');
+  const bool dot16 = G >= 4 * ctx->sm_count;
   // The fused kernel re-reads each thread's basis rows after its axpy: fewer
   // resident rows keep that footprint (rows x (j+1) x 8 B) inside L2.
   const char* cps_env = std::getenv("MSCG_AXPYDOT_CPS");
@@ -588,7 +591,7 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
         // CGS2: h = V^T w; w -= V h; twice, H(:,j) = h1 + h2.
         if (cgs2_fused) {
           // dot, fused axpy + dot, axpy: three sweeps over the basis
-          multidot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
+          (dot16 ? multidot_kernel<16> : multidot_kernel<8>)<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
                                                  hscratch.as<double>());
           axpy_dot_kernel<<<G_ad, kThreads, 0, s>>>(n, j + 1, vbase, ld, hscratch.as<double>(), wp,
                                                     Hc, red_ad, hscratch.as<double>() + (m + 2));
@@ -597,7 +600,7 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
           ctx->launches += 3;
         } else
         for (int pass = 0; pass < 2; ++pass) {
-          multidot_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
+          (dot16 ? multidot_kernel<16> : multidot_kernel<8>)<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, wp, ws.red,
                                                  hscratch.as<double>());
           multiaxpy_kernel<<<G, kThreads, 0, s>>>(n, j + 1, vbase, ld, hscratch.as<double>(), wp,
                                                   Hc, pass);
