@@ -194,124 +194,130 @@ def correction_line(corr, pc, ms, peak, config):
             "achieved_gbs": gbs, "frac": gbs / peak}
 
 
-def cpu_baseline(pc, pb, y, seconds_target=12.0, workers=1):
-    """The reference's own `solve` (factorization.cpp:129-158) timed on host
-    cores on a sample of interior blocks, extrapolated to a full apply
-    (two D passes over all blocks; E/F/Schur/SpMV terms < 5% omitted)."""
+def cpu_baseline(pc, pb, y, seconds_target=15.0, nsample=128):
+    """The reference's own `solve` (factorization.cpp:129-158), one core, on
+    an evenly spaced sample of interior blocks whose factors (downloaded from
+    the GPU, bit-identical to the reference ILUT) are far larger than the
+    host's last-level cache, visited round-robin so every solve streams its
+    factors from DRAM; extrapolated to the apply's two D passes over all
+    blocks (E/F/Schur/SpMV terms < 5%, omitted)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy
+    refpy.lib()
     nb = pc.nblocks
-    ns = min(nb, 8)
-    idx = np.unique(np.linspace(0, nb - 1, ns).astype(int))
+    idx = np.unique(np.linspace(0, nb - 1, min(nb, nsample)).astype(int))
     ranges = pb.d_ranges()
-    facs, rhs = [], []
-    kind = "reference"
-    try:
-        import refpy
-        refpy.lib()
-        for b in idx:
-            f = pc.d_factors(int(b))
-            L = refpy.Csr(f.lower.nrows, f.lower.ncols, f.lower.row_offsets, f.lower.col_indices,
-                          f.lower.values)
-            U = refpy.Csr(f.upper.nrows, f.upper.ncols, f.upper.row_offsets, f.upper.col_indices,
-                          f.upper.values)
-            facs.append(refpy.factors_from_arrays(f.lower.nrows, L, U))
-            rhs.append(y[ranges[b, 0]:ranges[b, 1]])
-        rhs = np.concatenate(rhs)
-        secs, _ = refpy.time_block_solves(facs, rhs, 1, workers)
-        reps = max(1, int(seconds_target / max(secs, 1e-6)))
-        secs, _ = refpy.time_block_solves(facs, rhs, reps, workers)
-    except Exception as e:  # reference library absent -> oracle port
-        log("cpu_baseline: reference unavailable, using the oracle port:", e)
-        import restatepy as rs
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from helpers import split_blocks
-        kind = "port"
-        D, _, _ = split_blocks(pb.C, pb.p)
-        facs = [rs.factor_ilut(int(ranges[b, 1] - ranges[b, 0]),
-                               *rs._sub_csr(*D, int(ranges[b, 0]), int(ranges[b, 1])), TOL_A)
-                for b in idx]
-        rhs = [y[ranges[b, 0]:ranges[b, 1]] for b in idx]
-        t0 = time.perf_counter()
-        reps = 0
-        while time.perf_counter() - t0 < seconds_target:
-            for f, r in zip(facs, rhs):
-                f.solve(r)
-            reps += 1
-        secs = time.perf_counter() - t0
-    # single worker: mean per-block solve time, two D passes over all blocks
+    facs, rhs, fbytes = [], [], 0
+    for b in idx:
+        f = pc.d_factors(int(b))
+        L = refpy.Csr(f.lower.nrows, f.lower.ncols, f.lower.row_offsets, f.lower.col_indices,
+                      f.lower.values)
+        U = refpy.Csr(f.upper.nrows, f.upper.ncols, f.upper.row_offsets, f.upper.col_indices,
+                      f.upper.values)
+        facs.append(refpy.factors_from_csr(f.lower.nrows, L, U))
+        fbytes += 12 * (L.nnz + U.nnz) + 8 * (L.nrows + 1)
+        rhs.append(y[ranges[b, 0]:ranges[b, 1]])
+    rhs = np.concatenate(rhs)
+    secs, _ = refpy.time_block_solves(facs, rhs, 1, 1)
+    reps = max(1, int(seconds_target / max(secs, 1e-6)))
+    secs, _ = refpy.time_block_solves(facs, rhs, reps, 1)
     per_block = secs / (reps * len(idx))
     t_apply = 2.0 * per_block * nb
+    info = refpy.cpu_info()
     return {
-        "value": 1.0 / t_apply, "unit": "applies/s", "cores": workers, "kind": kind,
-        "sample": (f"{len(idx)} of {nb} interior blocks x {reps} reps of the reference solve "
-                   f"(factorization.cpp:129-158) on GPU-built factors bit-identical to the "
-                   f"reference ILUT; extrapolated to 2 D passes over all blocks "
-                   f"({secs:.1f} s measured)"),
+        "value": 1.0 / t_apply, "unit": "applies/s", "cores": 1, "kind": "reference",
+        "cpu": info["model"], "nproc": info["nproc"],
+        "sample": (f"{len(idx)} of {nb} interior blocks ({fbytes / 1e9:.2f} GB of reference "
+                   f"CSR factors, > LLC; visited round-robin, cold) x {reps} sweeps of the "
+                   f"reference solve (factorization.cpp:129-158) on one core; factors are the "
+                   f"GPU's, bit-identical to the reference ILUT; extrapolated to 2 D passes "
+                   f"over all blocks ({secs:.1f} s measured)"),
         "seconds_per_apply": t_apply,
     }
 
 
 def run_reference_arm(args, cfg):
+    """`--impl reference`: the UNMODIFIED reference (oracle/_ref/libmscref.so,
+    its own sources compiled in place) on this host's cores, on the same
+    workload and step as our arm, without loading libmscg.so:
+      setup   generate_oseen -> scale_rows -> partition_saddle (+ SURVEY §8(d)
+              anchoring) -> aggregates -> build_msc, then the interior blocks
+              factored by the reference factor_ilut on all threads
+              (ref_build_precond_parallel: the MscPreconditioner
+              build_preconditioner returns, block loop concurrent);
+      step    one FULL preconditioner apply over every block (the reference
+              apply, preconditioner.cpp:85-114, with block_solve's independent
+              per-block `solve` calls on all threads; bit-identical to the
+              stock apply) + one reference matvec(C);
+      also    the stock single-threaded MscPreconditioner::apply, timed over
+              3 applies (`stock_apply`).
+    No extrapolation: every step covers all blocks."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import refpy
-    import paper_1104_3349_b200 as msc
     threads = refpy.hardware_threads()
-    pb, _ = build_problem(cfg)
-    # Reference ILUT on a sample of blocks (its own factor_ilut), then the
-    # reference solve over that sample on all host threads per step.
-    ranges = pb.d_ranges()
-    C = pb.C
-    nb = pb.nblocks
-    ns = min(nb, max(8, 2 * threads))
-    idx = np.unique(np.linspace(0, nb - 1, ns).astype(int))
-    from concurrent.futures import ThreadPoolExecutor
-
-    def fac(b):
-        b0, b1 = ranges[b]
-        rp = C.row_offsets[b0:b1 + 1] - C.row_offsets[b0]
-        ci = C.col_indices[C.row_offsets[b0]:C.row_offsets[b1]]
-        v = C.values[C.row_offsets[b0]:C.row_offsets[b1]]
-        keep = (ci >= b0) & (ci < b1)
-        rows = np.repeat(np.arange(b1 - b0), np.diff(rp))[keep]
-        nrp = np.zeros(b1 - b0 + 1, np.int32)
-        np.add.at(nrp, rows + 1, 1)
-        A = refpy.Csr(b1 - b0, b1 - b0, np.cumsum(nrp).astype(np.int32),
-                      (ci[keep] - b0).astype(np.int32), v[keep].copy())
-        return refpy.factor_ilut(A, TOL_A)
-
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        facs = list(ex.map(fac, idx))
-    t_fac = time.perf_counter() - t0
-    y = seeded_rhs(pb.n, 0)
-    rhs = np.concatenate([y[ranges[b, 0]:ranges[b, 1]] for b in idx])
+    P = refpy.Problem.oseen(cfg["grid"], cfg["nu"], cfg["n_a"], stretched=cfg["stretched"],
+                            stretch=cfg["stretch"], anchored=cfg["anchored"])
+    t1 = time.perf_counter()
+    P.build_schur(cfg["variant"], cfg["sz"], 1 if cfg["mode"] == "anchored" else 0,
+                  workers=threads)
+    t2 = time.perf_counter()
+    P.build_precond_parallel(TOL_A, S_A, workers=threads)
+    t3 = time.perf_counter()
+    y = refpy.random_vector(P.n, 0)
+
+    def step():
+        P.apply_threads(y, threads)
+        P.matvec(y)
+
     for _ in range(args.warmup):
-        refpy.time_block_solves(facs, rhs, 1, threads)
-    step_secs = []
+        step()
+    clk = None
+    step_s = []
     for _ in range(args.steps):
-        s, _ = refpy.time_block_solves(facs, rhs, 2, threads)  # two D passes
-        step_secs.append(s)
-    t = float(np.mean(step_secs))
-    value = (len(idx) / nb) / t  # full applies per second, extrapolated
+        s0 = time.perf_counter()
+        step()
+        step_s.append(time.perf_counter() - s0)
+    total = sum(step_s)
+    value = args.steps / total
+    stock_s, _ = P.time_apply(y, 3)
+    info = refpy.cpu_info()
     line = {
         "impl": "reference", "metric": "precond_applies_per_s", "value": value,
         "unit": "applies/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Oseen generator)",
-        "config": {"workload": args.config, **{k: cfg[k] for k in ("grid", "nu", "n_a")}},
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform[-1,1] rhs; the reference's own Oseen generator)",
+        "config": config_block(args.config, cfg, P.nblocks, P.n),
         "cpu_baseline": {
             "value": value, "unit": "applies/s", "cores": threads, "kind": "reference",
-            "sample": (f"reference factor_ilut + solve on {len(idx)} of {nb} interior blocks, "
-                       f"{threads} threads (reference parallel_for), extrapolated to a full "
-                       f"apply (2 D passes); ILUT of the sample took {t_fac:.1f} s"),
+            "cpu": info["model"], "nproc": info["nproc"],
+            "sample": (f"every step = 1 full reference apply over all {P.nblocks} interior "
+                       f"blocks (block solves on {threads} threads) + 1 reference matvec(C); "
+                       f"no extrapolation"),
         },
+        "stock_apply": {"applies_per_s": 3.0 / stock_s, "cores": 1, "applies": 3,
+                        "what": "stock MscPreconditioner::apply (preconditioner.cpp:85-114), "
+                                "single-threaded as shipped, all blocks"},
+        "setup": {"generate_scale_partition_s": t1 - t0, "aggregates_build_msc_s": t2 - t1,
+                  "ilut_all_blocks_s": t3 - t2, "ilut_threads": threads},
         "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "clocks": clk,
     }
     print(json.dumps(line), flush=True)
+
+
+def config_block(name, cfg, nblocks, n):
+    """`config` object shared by both arms (same keys)."""
+    return {"workload": name, "grid": cfg["grid"], "nu": cfg["nu"], "subdomains": nblocks,
+            "unknowns": n, "variant": cfg["variant"], "sz": cfg["sz"],
+            "aggregates_mode": cfg["mode"], "tolA": TOL_A, "sA": S_A,
+            "step": "1 MSC apply + 1 SpMV(C)",
+            "rhs": "std::mt19937(0) uniform[-1,1] in the final numbering"}
 
 
 def run_sharded(args, cfg, ws, rank, local, pg, ctx):
@@ -445,6 +451,67 @@ def run_sharded(args, cfg, ws, rank, local, pg, ctx):
     pg.destroy_process_group()
 
 
+REF_GMRES = {  # the reference's own numbers on the same problems (tests/golden)
+    "cfg2": ("cfg2.json", "gmres"),
+    "cfg4": ("cfg4.json", "gmres_first_cycle"),
+}
+
+
+def reference_gmres_context(name):
+    try:
+        fn, key = REF_GMRES[name]
+        g = json.load(open(os.path.join(ROOT, "tests", "golden", fn)))[key]
+        return {"iterations": g["iterations"], "converged": g["converged"],
+                "solve_s": g["seconds"], "true_residual": g["history"][-1],
+                "max_iters": g.get("max_iters", 3000),
+                "what": "reference gmres (gmres.cpp:35-191), 1 core, this container"}
+    except Exception:
+        return None
+
+
+def gmres_run(name, ctx, local, max_iters=3000, orth="cgs2", threads=0):
+    """BASELINE time-to-solution: full setup (device assembly, host
+    partition, device build_msc, device ILUT + Schur LU + correction) and
+    right-preconditioned GMRES(restart) to rtol 1e-8 from the seeded rhs,
+    end to end through the public API (rhs from host memory, x back)."""
+    import torch
+    import paper_1104_3349_b200 as msc
+    from paper_1104_3349_b200.msc import SolverConfig
+    cfg = CONFIGS[name]
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    pb, setup = build_problem(cfg, threads=threads, ctx=ctx)
+    t1 = time.perf_counter()
+    pc = msc.build_preconditioner(pb, tolA=TOL_A, sA=S_A, ctx=ctx)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    b = seeded_rhs(pb.n, 0)
+    scfg = SolverConfig(restart=cfg["restart"], max_iters=max_iters, rel_tol=1e-8, orth=orth)
+    l0 = ctx.launches
+    t3 = time.perf_counter()
+    x, rep = msc.gmres(pc.matrix, pc, b, scfg)
+    t4 = time.perf_counter()
+    clk = clocks.stop()
+    tr = msc.true_residual(pc.matrix, x, b)
+    out = {
+        "config": {"workload": name, "grid": cfg["grid"], "nu": cfg["nu"],
+                   "subdomains": pb.nblocks, "unknowns": pb.n, "restart": cfg["restart"],
+                   "rel_tol": 1e-8, "max_iters": max_iters, "orth": orth,
+                   "correction": pc.correction()["on"]},
+        "iterations": rep.iterations, "converged": rep.converged,
+        "final_true_residual": tr, "final_recurrence_or_true": rep.residual_history[-1],
+        "solve_s": t4 - t3, "setup_s": t2 - t0, "setup_plus_solve_s": t4 - t0,
+        "ms_per_iteration": 1e3 * (t4 - t3) / max(1, rep.iterations),
+        "setup": dict(setup, device_factorisation_s=t2 - t1, **pc.build_times()),
+        "gpu_launches": ctx.launches - l0, "clocks": clk,
+        "reference": reference_gmres_context(name),
+    }
+    del pc, pb, x
+    torch.cuda.synchronize()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -456,6 +523,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-iters", type=int, default=3000)
     ap.add_argument("--orth", default="cgs2", choices=["cgs2", "mgs"])
+    ap.add_argument("--no-gmres", action="store_true",
+                    help="skip the GMRES time-to-solution runs (cfg2, cfg4) in apply mode")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: run N independent single-GPU replicas instead of sharding "
                          "the interior blocks")
@@ -576,17 +645,37 @@ def main():
             except Exception:
                 pass
         apply_ms = sum(stage_ms[:5]) / args.steps
+        lb = (C.c_int64 * 10)()
+        L.mscg_precond_layout_bytes(pc.h, lb)
+        lb = list(lb)
+        moved = (lb[0] + lb[1] + lb[3] + lb[5] + (lb[2] if corr["on"] else lb[0]))
+        corr_off = None
+        if corr["on"]:
+            # the reference's second half (E SpMV + second interior solve)
+            # on the same preconditioner, for comparison
+            L.mscg_precond_use_correction(pc.h, 0)
+            bench(2)
+            off_ms, off_st, _ = bench(5)
+            L.mscg_precond_use_correction(pc.h, 1)
+            off_apply = sum(off_st[:5]) / 5
+            corr_off = {"applies_per_s": 5 / (off_ms / 1e3), "apply_ms": off_apply,
+                        "d_solve_ms": (off_st[0] + off_st[4]) / 10,
+                        "what": "same preconditioner, correction panels unused: the "
+                                "reference's E SpMV + second interior solve; step = apply "
+                                "+ SpMV"}
         result = {
             "metric": "precond_applies_per_s", "value": value, "unit": "applies/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform[-1,1] rhs; reference Oseen generator, bit-identical)",
-            "config": {"workload": args.config, "grid": cfg["grid"], "nu": cfg["nu"],
-                       "subdomains": pb.nblocks, "unknowns": pb.n, "variant": cfg["variant"],
-                       "aggregates": len(pb.schur_ranges()), "tolA": TOL_A, "sA": S_A,
-                       "step": "1 MSC apply + 1 SpMV(C)",
-                       "l2": "inputs larger than L2 (factors %.1f GB)" % (ab["d_lu_nnz"] * 10 / 1e9),
-                       "parallelism": "replicas" if ws > 1 else "single GPU"},
+            "config": dict(config_block(args.config, cfg, pb.nblocks, pb.n),
+                           aggregates=len(pb.schur_ranges()),
+                           l2="inputs larger than L2 (factors %.1f GB)" % (
+                               ab["d_lu_nnz"] * 10 / 1e9),
+                           parallelism="replicas" if ws > 1 else "single GPU",
+                           steps_note=("BASELINE cfg5 names 1000 back-to-back applies; the "
+                                       "steady-state rate is measured over --steps (default "
+                                       "20) after --warmup")),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "trisolve_kernel (interior-block L+U solve)",
@@ -597,10 +686,20 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk,
             "apply_ms": apply_ms,
-            "apply_gbs": ab["apply"] / (apply_ms / 1e3) / 1e9,
+            "apply_ref_equiv_gbs": ab["apply"] / (apply_ms / 1e3) / 1e9,
+            "apply_moved_bytes": moved,
+            "d_solve_layout": {"bytes_per_pass": lb[0], "near_tiles": lb[6], "far_entries": lb[7],
+                               "work_items": lb[8], "dense_near_tiles": lb[9],
+                               "algorithmic_bytes": ab["d_solve"]},
+            "apply_moved_gbs": moved / (apply_ms / 1e3) / 1e9,
+            "apply_correction_off": corr_off,
             "spmv_ms": stage_ms[5] / args.steps,
             "spmv_gbs": ab["spmv"] / (stage_ms[5] / args.steps / 1e3) / 1e9,
-            "apply_bytes_basis": "reference algorithm (SURVEY 8(d): two interior passes, 12 B/entry)",
+            "apply_bytes_basis": ("apply_ref_equiv_gbs: the reference algorithm's bytes (SURVEY "
+                                  "8(d): two interior passes, 12 B/entry) / apply time - a "
+                                  "reference-equivalent rate, not DRAM traffic; "
+                                  "apply_moved_gbs: the device layout's bytes one apply "
+                                  "streams (mscg_precond_layout_bytes) / apply time"),
             "stage_ms": {k: v / args.steps for k, v in zip(
                 ["d_solve", "f_spmv", "s_solve", "e_spmv",
                  "correction" if corr["on"] else "d_solve_sub", "c_spmv"], stage_ms)},
@@ -609,35 +708,32 @@ def main():
             "setup": setup,
         }
     else:
-        from paper_1104_3349_b200.msc import SolverConfig
-        b = y
-        scfg = SolverConfig(restart=cfg["restart"], max_iters=args.max_iters, rel_tol=1e-8,
-                            orth=args.orth)
-        l0 = ctx.launches
-        t0 = time.perf_counter()
-        x, rep = msc.gmres(pc.matrix, pc, torch.from_numpy(b).to(dev), scfg)
-        torch.cuda.synchronize()
-        tts = time.perf_counter() - t0
+        g = gmres_run(args.config, ctx, local, max_iters=args.max_iters, orth=args.orth,
+                      threads=max(1, (os.cpu_count() or 8) // ws))
         result = {
-            "metric": "gmres_time_to_solution_s", "value": tts, "unit": "s", "n_gpus": ws,
-            "steps": 1, "warmup": 0, "ms_per_step": tts * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "restart": cfg["restart"], "rel_tol": 1e-8,
-                       "max_iters": args.max_iters, "orth": args.orth},
-            "iterations": rep.iterations, "converged": rep.converged,
-            "final_true_residual": rep.residual_history[-1],
-            # BASELINE cfg4 times setup + solve: problem generation and
-            # partition (host), MSC build, device factorisation, then GMRES
-            "setup_plus_solve_s": tts + sum(setup[k] for k in ("generate_partition_s",
-                                                               "build_msc_s",
-                                                               "device_factorisation_s")),
-            "setup": setup, "gpu_launches": ctx.launches - l0,
-        }
+            "metric": "gmres_time_to_solution_s", "value": g["setup_plus_solve_s"], "unit": "s",
+            "n_gpus": ws, "steps": 1, "warmup": 0, "ms_per_step": g["solve_s"] * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded uniform[-1,1] rhs; reference Oseen generator)", **g}
     if rank == 0 and ws == 1 and args.mode == "apply" and not args.no_cpu_baseline:
         try:
             result["cpu_baseline"] = cpu_baseline(pc, pb, y)
         except Exception as e:
             result["cpu_baseline"] = {"value": None, "error": str(e)}
+    if ws == 1 and args.mode == "apply" and not args.no_gmres:
+        # BASELINE's second half: GMRES time-to-solution, cfg2 (converges)
+        # and cfg4 (full setup + solve, GMRES(100), 3000-iteration cap)
+        del pc, pb
+        x_d = y_d = w_d = None
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        result["gmres"] = {}
+        for name in ("cfg2", "cfg4"):
+            try:
+                result["gmres"][name] = gmres_run(name, ctx, local,
+                                                  threads=max(1, (os.cpu_count() or 8)))
+            except Exception as e:
+                result["gmres"][name] = {"error": repr(e)}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if pg:

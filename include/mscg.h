@@ -57,6 +57,7 @@ typedef struct mscg_ctx mscg_ctx;         /* device, stream, scratch */
 typedef struct mscg_csr mscg_csr;         /* device-resident sparse matrix */
 typedef struct mscg_precond mscg_precond; /* device-resident MSC preconditioner */
 typedef struct mscg_problem mscg_problem; /* host setup: partitioned system */
+typedef struct mscg_factors mscg_factors; /* device-resident factors of one block */
 
 int mscg_abi_version(void);
 
@@ -152,6 +153,24 @@ int mscg_precond_build(mscg_ctx *ctx, int n, int p, const int *c_rp,
                        const double *s_v, int nschur, const int *s_ranges,
                        double tol_a, int s_a, mscg_precond **out,
                        mscg_status *st);
+/* factor_ilut(a, tol) (kind 0, factorization.hpp:38, factorization.cpp:34-127)
+ * or factor_exact(a) (kind 1, factorization.hpp:32, dense_lu with partial
+ * pivoting) of one square CSR block on the device.  Errors as the reference:
+ * "factor_ilut: zero pivot at index i" / "dense_lu: zero pivot at index i"
+ * (MSCG_ERR_SINGULAR, pivot_index = i), "factor_ilut: negative drop
+ * tolerance" (MSCG_ERR_INVALID_ARGUMENT).  Blocks up to 65535 rows. */
+int mscg_factor(mscg_ctx *ctx, int n, const int *rp, const int *ci, const double *v,
+                int kind, double tol, mscg_factors **out, mscg_status *st);
+/* TriangularFactors in the reference CSR (factorization.hpp:18-27): L strictly
+ * lower (unit diagonal implicit), U with its diagonal, row_perm.forward.
+ * Call with lrp == NULL first to get the sizes. */
+int mscg_factors_get(const mscg_factors *f, int *dim, int64_t *nnz_l, int64_t *nnz_u,
+                     int *lrp, int *lci, double *lv, int *urp, int *uci, double *uv,
+                     int *perm, mscg_status *st);
+/* x = U^-1 L^-1 P b (solve, factorization.hpp:41, factorization.cpp:129-158). */
+int mscg_factors_solve(mscg_factors *f, const double *b, double *x, int mem,
+                       mscg_status *st);
+void mscg_factors_destroy(mscg_factors *f);
 int mscg_precond_build_problem(mscg_ctx *ctx, const mscg_problem *pb,
                                double tol_a, int s_a, mscg_precond **out,
                                mscg_status *st);
@@ -189,6 +208,13 @@ int mscg_precond_spmv_shard(mscg_precond *pc, const double *x_dev,
 int mscg_precond_apply(mscg_precond *pc, const double *y, double *x, int mem,
                        mscg_status *st);
 /* stored_nnz (preconditioner.cpp:116-121): factor nnz + nnz(E) + nnz(F). */
+/* x = B^-1 y with device vectors, enqueued on `stream` (NULL = legacy
+ * default stream) instead of the context's.  Applies on different streams,
+ * from any threads, run concurrently: each stream gets its own scratch
+ * (the reference promises apply is safe from several threads,
+ * preconditioner.hpp:17-18). */
+int mscg_precond_apply_stream(mscg_precond *pc, const double *y_dev, double *x_dev,
+                              void *stream, mscg_status *st);
 int64_t mscg_precond_stored_nnz(const mscg_precond *pc);
 int mscg_precond_dims(const mscg_precond *pc, int *n, int *p, int *nblocks,
                       int *nschur);
@@ -214,6 +240,18 @@ mscg_csr *mscg_precond_matrix(mscg_precond *pc);
 /* Stored-entry counts for roofline bookkeeping: interior-block L and U
  * (U without its diagonal), Schur-block L and U, E, F and C. */
 int mscg_precond_nnz(const mscg_precond *pc, int64_t counts[7]);
+/* Select, per preconditioner, whether applies use the explicit correction
+ * panels when they were built (1, default) or the reference's E SpMV +
+ * second interior solve (0).  Same operator; used by the bench to report
+ * both apply rates.  Not synchronised with in-flight applies. */
+int mscg_precond_use_correction(mscg_precond *pc, int on);
+/* Bytes of the device layout one apply streams (what the kernels move, as
+ * opposed to the reference-CSR "algorithmic" count): [0] one interior
+ * solve pass, [1] one Schur solve pass, [2] correction panels + z1/x1,
+ * [3] E and F (SELL), [4] C (SELL), [5] vectors; breakdown of [0]: [6] near
+ * tiles (copied prefixes, both triangles), [7] far entries, [8] work items,
+ * [9] number of near tiles kept dense. */
+int mscg_precond_layout_bytes(const mscg_precond *pc, int64_t out[10]);
 
 /* ---- measurement helpers ------------------------------------------------ */
 /* oracle::random_vector (proj/tests/oracles.hpp:92-98): std::mt19937(seed)

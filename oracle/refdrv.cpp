@@ -122,6 +122,58 @@ std::vector<int> anchored_interface_order(const PartitionedMatrix& pm, int nsep,
   return order;
 }
 
+// ---- private-member access (test infrastructure) -------------------------
+// MscPreconditioner can only be filled by build_preconditioner (a friend,
+// preconditioner.hpp:45-48), whose interior-block loop is sequential
+// (preconditioner.cpp:44-56: 16-23 min at cfg5).  To run the reference's
+// OWN apply (preconditioner.cpp:85-114) on reference factors computed
+// concurrently, or on factors downloaded from the GPU, the driver fills the
+// object's members directly.  Explicit template instantiation may name
+// private members ([temp.spec.general]/6), which is the standard way to do
+// this without modifying the reference headers.
+template <class Tag, typename Tag::type M>
+struct Rob {
+  friend typename Tag::type get(Tag) { return M; }
+};
+#define REF_ROB(TAG, CLS, TYPE, MEMBER)                   \
+  struct TAG {                                           \
+    using type = TYPE CLS::*;                            \
+    friend type get(TAG);                                \
+  };                                                     \
+  template struct Rob<TAG, &CLS::MEMBER>;
+
+using RangeVec = std::vector<std::pair<int, int>>;
+REF_ROB(PcN, MscPreconditioner, int, n_)
+REF_ROB(PcP, MscPreconditioner, int, p_)
+REF_ROB(PcKind, MscPreconditioner, std::string, kind_)
+REF_ROB(PcDR, MscPreconditioner, RangeVec, d_ranges_)
+REF_ROB(PcDF, MscPreconditioner, std::vector<TriangularFactors>, d_factors_)
+REF_ROB(PcSR, MscPreconditioner, RangeVec, schur_ranges_)
+REF_ROB(PcSF, MscPreconditioner, std::vector<TriangularFactors>, schur_factors_)
+REF_ROB(PcSS, MscPreconditioner, bool, schur_single_)
+REF_ROB(PcE, MscPreconditioner, SparseMatrix, e_)
+REF_ROB(PcF, MscPreconditioner, SparseMatrix, f_)
+REF_ROB(SmR, SparseMatrix, int, nrows_)
+REF_ROB(SmC, SparseMatrix, int, ncols_)
+REF_ROB(SmRP, SparseMatrix, std::vector<int>, row_offsets_)
+REF_ROB(SmCI, SparseMatrix, std::vector<int>, col_indices_)
+REF_ROB(SmV, SparseMatrix, std::vector<double>, values_)
+#undef REF_ROB
+
+// CSR arrays straight into a SparseMatrix (the caller guarantees the
+// reference's invariants: sorted rows, no explicit zeros) — no triplet sort.
+SparseMatrix csr_direct(int nrows, int ncols, const int* rp, const int* ci,
+                        const double* v) {
+  SparseMatrix a;
+  a.*get(SmR{}) = nrows;
+  a.*get(SmC{}) = ncols;
+  a.*get(SmRP{}) = std::vector<int>(rp, rp + nrows + 1);
+  const std::size_t nnz = static_cast<std::size_t>(rp[nrows]);
+  a.*get(SmCI{}) = std::vector<int>(ci, ci + nnz);
+  a.*get(SmV{}) = std::vector<double>(v, v + nnz);
+  return a;
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -327,6 +379,222 @@ int ref_build_precond(RefProblem* p, double tolA, int sA) {
   });
 }
 
+// build_preconditioner (preconditioner.cpp:26-83) with its interior-block
+// factorisation loop spread over the reference's own parallel_for
+// (parallel.cpp:21-50).  Every block runs the reference factor_ilut /
+// factor_exact exactly as the sequential loop does, so the resulting
+// MscPreconditioner is member-for-member the one build_preconditioner
+// returns; a singular block raises the reference's message for the LOWEST
+// failing block index, as the sequential loop would.
+int ref_build_precond_parallel(RefProblem* p, double tolA, int sA, int workers) {
+  return guarded([&] {
+    const PartitionedMatrix& c = p->pm;
+    const SchurApproximation& schur = p->schur;
+    if (schur.s_hat.rows() != c.n_g())
+      throw std::invalid_argument(
+          "build_preconditioner: Schur approximation does not match the split");
+    if (c.d_block_ranges.empty())
+      throw std::invalid_argument("build_preconditioner: no interior D blocks");
+    auto b = std::make_unique<MscPreconditioner>();
+    (*b).*get(PcN{}) = c.n();
+    (*b).*get(PcP{}) = c.p;
+    (*b).*get(PcKind{}) = schur.exact ? "exact-schur" : variant_name(schur.variant);
+    (*b).*get(PcDR{}) = c.d_block_ranges;
+    (*b).*get(PcE{}) = c.E;
+    (*b).*get(PcF{}) = c.F;
+    const int nb = static_cast<int>(c.d_block_ranges.size());
+    auto& df = (*b).*get(PcDF{});
+    df.resize(nb);
+    std::vector<std::string> err(nb);
+    std::vector<int> errpiv(nb, -2);
+    parallel_for(nb, workers, [&](int i) {
+      const auto [begin, end] = c.d_block_ranges[i];
+      SparseMatrix block = extract_block(c.D, begin, end, begin, end);
+      try {
+        const int dim = end - begin;
+        df[i] = dim <= sA ? factor_exact(block) : factor_ilut(block, tolA);
+      } catch (const SingularMatrixError& e) {
+        err[i] = e.what();
+        errpiv[i] = e.pivot_index;
+      }
+    });
+    for (int i = 0; i < nb; ++i)
+      if (errpiv[i] != -2)
+        throw SingularMatrixError("build_preconditioner: (1,1) block " +
+                                      std::to_string(i) + ": " + err[i],
+                                  errpiv[i]);
+    if (schur.overlapped) {
+      (*b).*get(PcSS{}) = true;
+      try {
+        ((*b).*get(PcSF{})).push_back(factor_exact(schur.s_hat));
+      } catch (const SingularMatrixError& e) {
+        throw SingularMatrixError(
+            std::string("build_preconditioner: overlapped Schur band: ") + e.what(),
+            e.pivot_index);
+      }
+    } else {
+      (*b).*get(PcSR{}) = schur.owned_ranges;
+      for (std::size_t i = 0; i < schur.owned_ranges.size(); ++i) {
+        const auto [begin, end] = schur.owned_ranges[i];
+        SparseMatrix block = extract_block(schur.s_hat, begin, end, begin, end);
+        try {
+          ((*b).*get(PcSF{})).push_back(factor_exact(block));
+        } catch (const SingularMatrixError& e) {
+          throw SingularMatrixError("build_preconditioner: Schur block " +
+                                        std::to_string(i) + ": " + e.what(),
+                                    e.pivot_index);
+        }
+      }
+    }
+    p->prec = std::move(b);
+  });
+}
+
+// A reference problem whose C, split, interior ranges and Schur
+// approximation come from arrays (e.g. the product's bit-identical setup):
+// C through csr_direct, D/E/F/G by the reference's from_split.
+int ref_problem_from_arrays(int n, const int* rp, const int* ci, const double* v,
+                            int p, int nranges, const int* ranges,
+                            RefProblem** out) {
+  return guarded([&] {
+    std::vector<std::pair<int, int>> rr;
+    for (int i = 0; i < nranges; ++i) rr.push_back({ranges[2 * i], ranges[2 * i + 1]});
+    auto pr = std::make_unique<RefProblem>();
+    pr->pm = PartitionedMatrix::from_split(csr_direct(n, n, rp, ci, v), p, rr);
+    pr->perm.resize(n);
+    for (int i = 0; i < n; ++i) pr->perm[i] = i;
+    *out = pr.release();
+  });
+}
+
+// Install a block-diagonal Schur approximation (S^ + owned ranges).
+int ref_problem_set_schur(RefProblem* p, const char* variant, const int* rp,
+                          const int* ci, const double* v, int nranges,
+                          const int* ranges) {
+  return guarded([&] {
+    const int ng = p->pm.n_g();
+    p->schur = SchurApproximation{};
+    p->schur.s_hat = csr_direct(ng, ng, rp, ci, v);
+    p->schur.variant = variant_from_name(variant);
+    for (int i = 0; i < nranges; ++i) {
+      p->schur.owned_ranges.push_back({ranges[2 * i], ranges[2 * i + 1]});
+      p->schur.spans.push_back({ranges[2 * i], ranges[2 * i + 1]});
+    }
+    p->have_schur = true;
+  });
+}
+
+// Stage 1 of "reference apply on given interior factors": an
+// MscPreconditioner whose ranges/E/F come from the problem, Schur blocks
+// factored by the reference factor_exact (as build_preconditioner does),
+// interior factors to be installed block by block.
+int ref_precond_begin(RefProblem* p) {
+  return guarded([&] {
+    const PartitionedMatrix& c = p->pm;
+    auto b = std::make_unique<MscPreconditioner>();
+    (*b).*get(PcN{}) = c.n();
+    (*b).*get(PcP{}) = c.p;
+    (*b).*get(PcKind{}) = variant_name(p->schur.variant);
+    (*b).*get(PcDR{}) = c.d_block_ranges;
+    (*b).*get(PcE{}) = c.E;
+    (*b).*get(PcF{}) = c.F;
+    ((*b).*get(PcDF{})).resize(c.d_block_ranges.size());
+    (*b).*get(PcSR{}) = p->schur.owned_ranges;
+    auto& sf = (*b).*get(PcSF{});
+    sf.resize(p->schur.owned_ranges.size());
+    const auto& sr = p->schur.owned_ranges;
+    const SparseMatrix& sh = p->schur.s_hat;
+    parallel_for(static_cast<int>(sr.size()), 0, [&](int i) {
+      sf[i] = factor_exact(extract_block(sh, sr[i].first, sr[i].second, sr[i].first,
+                                         sr[i].second));
+    });
+    p->prec = std::move(b);
+  });
+}
+
+int ref_precond_set_dfactor(RefProblem* p, int b, int n, const int* lrp, const int* lci,
+                            const double* lv, const int* urp, const int* uci,
+                            const double* uv) {
+  return guarded([&] {
+    auto& df = (*p->prec).*get(PcDF{});
+    TriangularFactors f;
+    f.lower = csr_direct(n, n, lrp, lci, lv);
+    f.upper = csr_direct(n, n, urp, uci, uv);
+    f.row_perm = Permutation::identity(n);
+    f.kind = FactorKind::Incomplete;
+    df.at(b) = std::move(f);
+  });
+}
+
+// MscPreconditioner::apply (preconditioner.cpp:85-114), operation for
+// operation, with block_solve's independent per-block `solve` calls
+// (preconditioner.cpp:13-22) spread over parallel_for.  Each block's
+// arithmetic is the reference's own, so the result is bit-identical to the
+// stock single-threaded apply (tests/test_oracle.py checks it).
+int ref_apply_threads(RefProblem* p, const double* y, double* x, int workers) {
+  return guarded([&] {
+    const MscPreconditioner& b = *p->prec;
+    const int n = b.*get(PcN{});
+    const int pp = b.*get(PcP{});
+    const int ng = n - pp;
+    const auto& dr = b.*get(PcDR{});
+    const auto& df = b.*get(PcDF{});
+    auto bsolve = [&](const double* in, double* out) {
+      parallel_for(static_cast<int>(dr.size()), workers, [&](int i) {
+        const auto [begin, end] = dr[i];
+        std::vector<double> local(in + begin, in + end);
+        std::vector<double> s = solve(df[i], local);
+        std::copy(s.begin(), s.end(), out + begin);
+      });
+    };
+    std::vector<double> z1(pp, 0.0);
+    bsolve(y, z1.data());
+    std::vector<double> t = matvec(b.*get(PcF{}), z1);
+    for (int i = 0; i < ng; ++i) t[i] = y[pp + i] - t[i];
+    std::vector<double> z2(ng, 0.0);
+    const auto& sf = b.*get(PcSF{});
+    if (b.*get(PcSS{})) {
+      std::vector<double> s = solve(sf[0], t);
+      std::copy(s.begin(), s.end(), z2.begin());
+    } else {
+      const auto& sr = b.*get(PcSR{});
+      for (std::size_t i = 0; i < sr.size(); ++i) {
+        std::vector<double> local(t.begin() + sr[i].first, t.begin() + sr[i].second);
+        std::vector<double> s = solve(sf[i], local);
+        std::copy(s.begin(), s.end(), z2.begin() + sr[i].first);
+      }
+    }
+    std::vector<double> w = matvec(b.*get(PcE{}), z2);
+    std::vector<double> corr(pp, 0.0);
+    bsolve(w.data(), corr.data());
+    for (int i = 0; i < pp; ++i) x[i] = z1[i] - corr[i];
+    std::copy(z2.begin(), z2.end(), x + pp);
+  });
+}
+
+// Wall seconds of `reps` stock applies (MscPreconditioner::apply).
+double ref_time_apply(RefProblem* p, const double* y, double* x, int reps) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < reps; ++r) {
+    std::vector<double> o = p->prec->apply(std::span<const double>(y, p->pm.n()));
+    std::memcpy(x, o.data(), sizeof(double) * o.size());
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Wall seconds of `reps` threaded applies (ref_apply_threads).
+double ref_time_apply_threads(RefProblem* p, const double* y, double* x, int reps,
+                              int workers) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < reps; ++r)
+    if (ref_apply_threads(p, y, x, workers) != 0) return -1.0;
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int ref_num_dfactors(RefProblem* p) {
+  return p->prec ? static_cast<int>(p->prec->d_factors().size()) : -1;
+}
+
 int64_t ref_stored_nnz(RefProblem* p) {
   return p->prec ? static_cast<int64_t>(p->prec->stored_nnz()) : -1;
 }
@@ -436,6 +704,17 @@ RefFactors* ref_factors_from_arrays(int n, const int* lrp, const int* lci,
   f->f.row_perm = Permutation::from_forward(fwd);
   return f.release();
 }
+// Same, straight from reference-invariant CSR arrays (no triplet sort).
+RefFactors* ref_factors_from_csr(int n, const int* lrp, const int* lci, const double* lv,
+                                 const int* urp, const int* uci, const double* uv) {
+  auto f = std::make_unique<RefFactors>();
+  f->f.lower = csr_direct(n, n, lrp, lci, lv);
+  f->f.upper = csr_direct(n, n, urp, uci, uv);
+  f->f.row_perm = Permutation::identity(n);
+  f->f.kind = FactorKind::Incomplete;
+  return f.release();
+}
+
 int ref_solve(RefFactors* f, const double* b, double* x) {
   return guarded([&] {
     std::vector<double> r = solve(f->f, std::span<const double>(b, f->f.dim()));
@@ -470,6 +749,21 @@ int ref_hardware_threads() {
 struct RefMat {
   SparseMatrix a;
 };
+
+// oracle::random_dd_sparse(n, density, mt19937(seed)) (tests/oracles.hpp:100-120).
+RefMat* ref_random_dd_sparse(int n, double density, unsigned seed) {
+  std::mt19937 rng(seed);
+  return new RefMat{oracle::random_dd_sparse(n, density, rng)};
+}
+
+// The raw (unscaled, unpermuted) (1,1) block D of generate_oseen(grid, nu)
+// on the uniform grid with the recirculating wind (acceptance.cpp:513-519).
+int ref_oseen_raw_d(int grid_n, double nu, RefMat** out) {
+  return guarded([&] {
+    auto prob = generate_oseen(grid_n, nu, GridKind::Uniform, WindKind::Recirculating);
+    *out = new RefMat{prob.matrices.D};
+  });
+}
 int ref_mm_read(const char* path, RefMat** out) {
   return guarded([&] { *out = new RefMat{load_matrix_market(path)}; });
 }

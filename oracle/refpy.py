@@ -64,6 +64,20 @@ def lib():
         L.ref_num_aggregates.argtypes = [vp]
         L.ref_get_schur_ranges.argtypes = [vp, _i32p]
         L.ref_build_precond.argtypes = [vp, C.c_double, C.c_int]
+        L.ref_build_precond_parallel.argtypes = [vp, C.c_double, C.c_int, C.c_int]
+        L.ref_problem_from_arrays.argtypes = [C.c_int, _i32p, _i32p, _f64p, C.c_int,
+                                              C.c_int, _i32p, C.POINTER(vp)]
+        L.ref_problem_set_schur.argtypes = [vp, C.c_char_p, _i32p, _i32p, _f64p, C.c_int,
+                                            _i32p]
+        L.ref_precond_begin.argtypes = [vp]
+        L.ref_precond_set_dfactor.argtypes = [vp, C.c_int, C.c_int, _i32p, _i32p, _f64p,
+                                              _i32p, _i32p, _f64p]
+        L.ref_apply_threads.argtypes = [vp, _f64p, _f64p, C.c_int]
+        L.ref_time_apply.restype = C.c_double
+        L.ref_time_apply.argtypes = [vp, _f64p, _f64p, C.c_int]
+        L.ref_time_apply_threads.restype = C.c_double
+        L.ref_time_apply_threads.argtypes = [vp, _f64p, _f64p, C.c_int, C.c_int]
+        L.ref_num_dfactors.argtypes = [vp]
         L.ref_stored_nnz.restype = C.c_int64
         L.ref_stored_nnz.argtypes = [vp]
         L.ref_factor_dims.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_int),
@@ -86,12 +100,17 @@ def lib():
         L.ref_factors_from_arrays.restype = vp
         L.ref_factors_from_arrays.argtypes = [C.c_int, _i32p, _i32p, _f64p, _i32p,
                                               _i32p, _f64p, C.c_void_p]
+        L.ref_factors_from_csr.restype = vp
+        L.ref_factors_from_csr.argtypes = [C.c_int, _i32p, _i32p, _f64p, _i32p, _i32p, _f64p]
         L.ref_solve.argtypes = [vp, _f64p, _f64p]
         L.ref_time_block_solves.restype = C.c_double
         L.ref_time_block_solves.argtypes = [C.c_int, C.POINTER(vp), _f64p, _f64p,
                                             C.c_int, C.c_int]
         L.ref_hardware_threads.restype = C.c_int
         L.ref_mm_read.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.ref_random_dd_sparse.restype = vp
+        L.ref_random_dd_sparse.argtypes = [C.c_int, C.c_double, C.c_uint]
+        L.ref_oseen_raw_d.argtypes = [C.c_int, C.c_double, C.POINTER(vp)]
         L.ref_mat_dims.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                    C.POINTER(C.c_int64)]
         L.ref_mat_get.argtypes = [vp, vp, vp, vp]
@@ -189,6 +208,28 @@ def factors_from_arrays(n, L: Csr, U: Csr, perm=None):
     return f
 
 
+def factors_from_csr(n, L: Csr, U: Csr):
+    """ILUT factors from reference-invariant CSR (sorted rows, no explicit
+    zeros, identity row permutation), without the triplet sort."""
+    c = lambda a, t: np.ascontiguousarray(a, t)  # noqa: E731
+    h = lib().ref_factors_from_csr(n, c(L.rp, np.int32), c(L.ci, np.int32), c(L.v, np.float64),
+                                   c(U.rp, np.int32), c(U.ci, np.int32), c(U.v, np.float64))
+    return Factors(h)
+
+
+def cpu_info():
+    """CPU model and logical CPU count of this host."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
 class Problem:
     """A reference PartitionedMatrix + MSC preconditioner pipeline."""
 
@@ -215,6 +256,18 @@ class Problem:
             rr = np.zeros(2, np.int32)
         _check(lib().ref_problem_from_csr(a.nrows, a.rp, a.ci, a.v, p,
                                           len(ranges), rr, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_arrays(cls, a: Csr, p, ranges):
+        """C given as reference-invariant CSR (sorted rows, no zeros), e.g.
+        the product's bit-identical setup; no triplet sort."""
+        h = C.c_void_p()
+        rr = np.ascontiguousarray(np.asarray(ranges, np.int32).reshape(-1))
+        _check(lib().ref_problem_from_arrays(a.nrows, np.ascontiguousarray(a.rp, np.int32),
+                                             np.ascontiguousarray(a.ci, np.int32),
+                                             np.ascontiguousarray(a.v, np.float64), p,
+                                             len(rr) // 2, rr, C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -274,6 +327,51 @@ class Problem:
     def build_precond(self, tolA=1e-4, sA=0):
         _check(lib().ref_build_precond(self.h, tolA, sA))
 
+    def build_precond_parallel(self, tolA=1e-4, sA=0, workers=0):
+        """build_preconditioner with the per-block factorisations on
+        `workers` threads (0 = all): the same MscPreconditioner."""
+        _check(lib().ref_build_precond_parallel(self.h, tolA, sA, workers))
+
+    def set_schur(self, variant, s_hat: Csr, ranges):
+        rr = np.ascontiguousarray(np.asarray(ranges, np.int32).reshape(-1))
+        _check(lib().ref_problem_set_schur(self.h, variant.encode(),
+                                           np.ascontiguousarray(s_hat.rp, np.int32),
+                                           np.ascontiguousarray(s_hat.ci, np.int32),
+                                           np.ascontiguousarray(s_hat.v, np.float64),
+                                           len(rr) // 2, rr))
+
+    def precond_from_factors(self, get_block):
+        """MscPreconditioner with the reference's own Schur factors and the
+        interior factors get_block(b) -> (n, L: Csr, U: Csr) (e.g. downloaded
+        from the GPU)."""
+        _check(lib().ref_precond_begin(self.h))
+        for b in range(self.nblocks):
+            n, L, U = get_block(b)
+            _check(lib().ref_precond_set_dfactor(
+                self.h, b, n, np.ascontiguousarray(L.rp, np.int32),
+                np.ascontiguousarray(L.ci, np.int32), np.ascontiguousarray(L.v, np.float64),
+                np.ascontiguousarray(U.rp, np.int32), np.ascontiguousarray(U.ci, np.int32),
+                np.ascontiguousarray(U.v, np.float64)))
+
+    def apply_threads(self, y, workers=0):
+        x = np.empty(self.n)
+        _check(lib().ref_apply_threads(self.h, np.ascontiguousarray(y, np.float64), x,
+                                       workers))
+        return x
+
+    def time_apply(self, y, reps=1, workers=None):
+        """Wall seconds of `reps` applies: the stock single-threaded
+        MscPreconditioner::apply (workers None) or the threaded block sweep."""
+        x = np.empty(self.n)
+        y = np.ascontiguousarray(y, np.float64)
+        if workers is None:
+            s = lib().ref_time_apply(self.h, y, x, reps)
+        else:
+            s = lib().ref_time_apply_threads(self.h, y, x, reps, workers)
+            if s < 0:
+                _check(-1)
+        return s, x
+
     def stored_nnz(self):
         return int(lib().ref_stored_nnz(self.h))
 
@@ -332,9 +430,7 @@ def _vp(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def mm_read(path) -> Csr:
-    h = C.c_void_p()
-    _check(lib().ref_mm_read(os.fsencode(path), C.byref(h)))
+def _mat_to_csr(h) -> Csr:
     try:
         nr, nc, nnz = C.c_int(), C.c_int(), C.c_int64()
         lib().ref_mat_dims(h, C.byref(nr), C.byref(nc), C.byref(nnz))
@@ -345,6 +441,24 @@ def mm_read(path) -> Csr:
         return Csr(nr.value, nc.value, rp, ci[:nnz.value].copy(), v[:nnz.value].copy())
     finally:
         lib().ref_mat_free(h)
+
+
+def mm_read(path) -> Csr:
+    h = C.c_void_p()
+    _check(lib().ref_mm_read(os.fsencode(path), C.byref(h)))
+    return _mat_to_csr(h)
+
+
+def random_dd_sparse(n, density, seed) -> Csr:
+    """oracle::random_dd_sparse with std::mt19937(seed) (tests/oracles.hpp:100-120)."""
+    return _mat_to_csr(C.c_void_p(lib().ref_random_dd_sparse(n, density, seed)))
+
+
+def oseen_raw_d(grid_n, nu) -> Csr:
+    """generate_oseen(grid_n, nu).matrices.D (unscaled, original numbering)."""
+    h = C.c_void_p()
+    _check(lib().ref_oseen_raw_d(grid_n, nu, C.byref(h)))
+    return _mat_to_csr(h)
 
 
 def mm_write(path, a: Csr) -> None:

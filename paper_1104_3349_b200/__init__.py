@@ -4,6 +4,7 @@ plus a Python mirror of the reference's C++ API."""
 from .msc import (  # noqa: F401
     Context,
     CudaError,
+    DeviceFactors,
     DeviceMatrix,
     IoError,
     MscError,
@@ -19,6 +20,8 @@ from .msc import (  # noqa: F401
     build_preconditioner_arrays,
     build_preconditioner_shard,
     default_context,
+    factor_exact,
+    factor_ilut,
     fill_factor,
     gmres,
     load_matrix_market,

@@ -94,16 +94,25 @@ _SIGS = {
     "mscg_precond_spmv_shard": (C.c_int, [vp, vp, vp, vp, C.c_int, C.POINTER(Status)]),
     "mscg_precond_destroy": (None, [vp]),
     "mscg_precond_apply": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(Status)]),
+    "mscg_precond_apply_stream": (C.c_int, [vp, vp, vp, vp, C.POINTER(Status)]),
     "mscg_precond_stored_nnz": (C.c_int64, [vp]),
     "mscg_precond_dims": (C.c_int, [vp, ip, ip, ip, ip]),
     "mscg_precond_factor": (C.c_int, [vp, C.c_int, C.c_int, ip, i64p, i64p, vp, vp, vp, vp, vp,
                                       vp, vp, C.POINTER(Status)]),
     "mscg_precond_build_times": (C.c_int, [vp, dp, dp, dp]),
+    "mscg_factor": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, C.c_double, C.POINTER(vp),
+                              C.POINTER(Status)]),
+    "mscg_factors_get": (C.c_int, [vp, ip, i64p, i64p, vp, vp, vp, vp, vp, vp, vp,
+                                   C.POINTER(Status)]),
+    "mscg_factors_solve": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(Status)]),
+    "mscg_factors_destroy": (None, [vp]),
     "mscg_precond_correction": (C.c_int, [vp, ip, i64p, ip, dp]),
     "mscg_precond_matrix": (vp, [vp]),
     "mscg_gmres": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(GmresConfig),
                              C.POINTER(GmresReport), vp, C.c_int, C.POINTER(Status)]),
     "mscg_precond_nnz": (C.c_int, [vp, C.POINTER(C.c_int64)]),
+    "mscg_precond_use_correction": (C.c_int, [vp, C.c_int]),
+    "mscg_precond_layout_bytes": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "mscg_random_vector": (None, [C.c_int, C.c_uint, vp]),
     "mscg_bench_apply": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, dp, dp, i64p,
                                    C.POINTER(Status)]),

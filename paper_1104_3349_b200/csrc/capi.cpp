@@ -36,6 +36,10 @@ struct mscg_precond {
   mscg_ctx* ctx = nullptr;
   mscg_csr matrix;  // borrowed view of pc->C
 };
+struct mscg_factors {
+  std::unique_ptr<mscg::FactorSet> fs;
+  mscg_ctx* ctx = nullptr;
+};
 struct mscg_problem {
   mscg::host::Partitioned pm;
   std::vector<double> scaled_rhs;
@@ -428,6 +432,70 @@ int mscg_precond_build(mscg_ctx* ctx, int n, int p, const int* c_rp, const int* 
   });
 }
 
+int mscg_factor(mscg_ctx* ctx, int n, const int* rp, const int* ci, const double* v, int kind,
+                double tol, mscg_factors** out, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx || !out) throw std::invalid_argument("factor: null context or output");
+    if (kind != 0 && kind != 1) throw std::invalid_argument("factor: kind must be 0 or 1");
+    if (kind == 0 && tol < 0.0) throw std::invalid_argument("factor_ilut: negative drop tolerance");
+    if (n < 1) throw std::invalid_argument(kind ? "factor_exact: empty matrix"
+                                                : "factor_ilut: empty matrix");
+    cudaStream_t s = ctx->ctx.stream;
+    const int64_t nnz = rp[n];
+    mscg::DevBuf drp(sizeof(int) * (n + 1)), dci(sizeof(int) * std::max<int64_t>(1, nnz)),
+        dv(sizeof(double) * std::max<int64_t>(1, nnz));
+    MSCG_CUDA(cudaMemcpyAsync(drp.p, rp, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
+    if (nnz) {
+      MSCG_CUDA(cudaMemcpyAsync(dci.p, ci, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+      MSCG_CUDA(cudaMemcpyAsync(dv.p, v, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    }
+    auto h = std::make_unique<mscg_factors>();
+    h->ctx = ctx;
+    h->fs = mscg::factor_blocks(&ctx->ctx, drp.as<int>(), dci.as<int>(), dv.as<double>(),
+                                {mscg::BlockSpec{0, n, 0}}, {static_cast<char>(kind)}, tol, "",
+                                nullptr);
+    MSCG_CUDA(cudaStreamSynchronize(s));
+    *out = h.release();
+  });
+}
+
+int mscg_factors_get(const mscg_factors* f, int* dim, int64_t* nnz_l, int64_t* nnz_u, int* lrp,
+                     int* lci, double* lv, int* urp, int* uci, double* uv, int* perm,
+                     mscg_status* st) {
+  return guard(st, [&] {
+    if (!f) throw std::invalid_argument("factors: null handle");
+    const auto& fs = *f->fs;
+    const int d = fs.h_dim[0];
+    if (dim) *dim = d;
+    if (nnz_l) *nnz_l = fs.h_nnz_l[0];
+    if (nnz_u) *nnz_u = fs.h_nnz_u[0] + d;
+    if (!lrp) return;
+    std::vector<int> a, b2, c2, d2, e2;
+    std::vector<double> f2, g2;
+    mscg::download_factor(fs, 0, a, b2, f2, c2, d2, g2, e2);
+    std::memcpy(lrp, a.data(), sizeof(int) * a.size());
+    std::memcpy(lci, b2.data(), sizeof(int) * b2.size());
+    std::memcpy(lv, f2.data(), sizeof(double) * f2.size());
+    std::memcpy(urp, c2.data(), sizeof(int) * c2.size());
+    std::memcpy(uci, d2.data(), sizeof(int) * d2.size());
+    std::memcpy(uv, g2.data(), sizeof(double) * g2.size());
+    if (perm) std::memcpy(perm, e2.data(), sizeof(int) * e2.size());
+  });
+}
+
+int mscg_factors_solve(mscg_factors* f, const double* b, double* x, int mem, mscg_status* st) {
+  return guard(st, [&] {
+    if (!f) throw std::invalid_argument("solve: null factors");
+    const size_t n = f->fs->h_dim[0];
+    with_vectors(f->ctx, b, n, x, n, mem, [&](const double* db, double* dx) {
+      mscg::block_trisolve(*f->fs, db, dx, nullptr, f->ctx->ctx.stream);
+      f->ctx->ctx.launches++;
+    });
+  });
+}
+
+void mscg_factors_destroy(mscg_factors* f) { delete f; }
+
 int mscg_precond_build_problem(mscg_ctx* ctx, const mscg_problem* pb, double tol_a, int s_a,
                                mscg_precond** out, mscg_status* st) {
   if (!pb || !pb->have_schur) {
@@ -521,7 +589,14 @@ int mscg_precond_apply(mscg_precond* pc, const double* y, double* x, int mem, ms
     if (!pc) throw std::invalid_argument("MscPreconditioner::apply: null preconditioner");
     const size_t n = pc->pc->n;
     if (mem == MSCG_MEM_DEVICE) {
-      pc->pc->apply(y, x, pc->ctx->ctx.stream);
+      // concurrent applies are safe: per-stream scratch (Precond::apply);
+      // the stream is read under the context lock (mscg_ctx_set_stream)
+      cudaStream_t s;
+      {
+        std::lock_guard<std::mutex> lk(pc->ctx->mu);
+        s = pc->ctx->ctx.stream;
+      }
+      pc->pc->apply(y, x, s);
       return;
     }
     // Host vectors: chunked apply, copies of one block chunk overlap the
@@ -545,6 +620,14 @@ int mscg_precond_apply(mscg_precond* pc, const double* y, double* x, int mem, ms
     pc->pc->apply_host(src, dst, d_y, d_x, s);
     MSCG_CUDA(cudaStreamSynchronize(s));
     if (!pin_out) std::memcpy(x, dst, sizeof(double) * n);
+  });
+}
+
+int mscg_precond_apply_stream(mscg_precond* pc, const double* y_dev, double* x_dev, void* stream,
+                              mscg_status* st) {
+  return guard(st, [&] {
+    if (!pc) throw std::invalid_argument("MscPreconditioner::apply: null preconditioner");
+    pc->pc->apply(y_dev, x_dev, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -581,6 +664,52 @@ int mscg_precond_factor(const mscg_precond* pc, int kind, int idx, int* dim, int
     std::memcpy(uv, g2.data(), sizeof(double) * g2.size());
     if (perm) std::memcpy(perm, e2.data(), sizeof(int) * e2.size());
   });
+}
+
+int mscg_precond_use_correction(mscg_precond* pc, int on) {
+  if (!pc) return MSCG_ERR_INVALID_ARGUMENT;
+  pc->pc->use_corr = on != 0;
+  return MSCG_OK;
+}
+
+int mscg_precond_layout_bytes(const mscg_precond* pc, int64_t out[10]) {
+  if (!pc) return MSCG_ERR_INVALID_ARGUMENT;
+  for (int k = 0; k < 10; ++k) out[k] = 0;
+  auto pass_bytes = [](const mscg::FactorSet& f) -> int64_t {
+    // one solve pass reads: every near tile's copied prefix, the far
+    // entries (fp64 + uint16 column), their row offsets, the work items
+    // (int4), the U diagonal and reciprocal; rhs in + x out
+    int64_t b = 0;
+    for (int w : f.h_lwidth) b += 8 * static_cast<int64_t>(mscg::tile_elems(w));
+    for (int w : f.h_uwidth) b += 8 * static_cast<int64_t>(mscg::tile_elems(w));
+    b += 10 * (f.far_l() + f.far_u());
+    b += 8 * static_cast<int64_t>(f.total_rows + f.nblocks);
+    if (!f.h_lioff.empty()) b += 16 * (f.h_lioff.back() + f.h_uioff.back());
+    b += 16 * static_cast<int64_t>(f.total_rows) * 2;
+    return b;
+  };
+  const auto& p = *pc->pc;
+  auto csr_bytes = [](const mscg::DevCsr* a) -> int64_t {
+    return a ? 12 * a->padded + 8 * static_cast<int64_t>(a->nslices + 1) : 0;
+  };
+  if (p.D) out[0] = pass_bytes(*p.D);
+  if (p.S) out[1] = pass_bytes(*p.S);
+  if (p.corr) out[2] = 8 * p.corr->entries + 16 * static_cast<int64_t>(p.p);
+  out[3] = csr_bytes(p.E.get()) + csr_bytes(p.F.get());
+  out[4] = csr_bytes(p.C.get());
+  out[5] = static_cast<int64_t>(p.n) * 8 * 4;  // y, x, z1 and interface vectors
+  if (p.D) {  // breakdown of one interior solve pass
+    const auto& f = *p.D;
+    for (int w : f.h_lwidth) out[6] += 8 * static_cast<int64_t>(mscg::tile_elems(w));
+    for (int w : f.h_uwidth) out[6] += 8 * static_cast<int64_t>(mscg::tile_elems(w));
+    out[7] = 10 * (f.far_l() + f.far_u());
+    if (!f.h_lioff.empty()) out[8] = 16 * (f.h_lioff.back() + f.h_uioff.back());
+    int64_t dense = 0;
+    for (int w : f.h_lwidth) dense += w == mscg::kDenseNbr;
+    for (int w : f.h_uwidth) dense += w == mscg::kDenseNbr;
+    out[9] = dense;  // near tiles kept dense (of 2 * tiles)
+  }
+  return MSCG_OK;
 }
 
 int mscg_precond_build_times(const mscg_precond* pc, double* ilut_s, double* schur_lu_s,

@@ -1192,7 +1192,11 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
     if (hc[2] != ~0ull) {
       const int blk = static_cast<int>(hc[2] >> 32), piv = static_cast<int>(hc[2] & 0xffffffffu);
       const bool ex = exact[blk] != 0;
-      std::string msg = std::string(what) + " " + std::to_string(blk) + ": " +
+      // what == "" : a standalone factor_ilut / factor_exact call, whose
+      // message carries no block prefix (factorization.cpp:113,
+      // dense_matrix.cpp:103)
+      std::string msg = (what[0] ? std::string(what) + " " + std::to_string(blk) + ": "
+                                 : std::string()) +
                         (ex ? "dense_lu" : "factor_ilut") + ": zero pivot at index " +
                         std::to_string(piv);
       throw Error(2, msg, blk, piv);

@@ -290,7 +290,16 @@ struct Precond {
   int64_t stored_nnz = 0;
   FactorTimes times;
   Shard shard;
-  DevBuf z1, t, w;  // scratch (apply is stream-ordered on ctx->stream)
+  // Build-time and shard scratch (a shard's z1 lives from apply_shard_begin
+  // to apply_shard_end, so a shard is one apply at a time by contract).
+  DevBuf z1, t, w;
+  // Use the explicit correction panels when built (false: the reference's
+  // E SpMV + second interior solve, for measurement and cross-checks).
+  bool use_corr = true;
+  // x = B^-1 y on stream s.  The apply's own vectors (z1, t, w) come from a
+  // per-stream scratch set: calls on one stream are ordered by the stream,
+  // calls on different streams get different sets, so concurrent applies
+  // from several threads are safe (preconditioner.hpp:17-18).
   void apply(const double* y_dev, double* x_dev, cudaStream_t s, cudaEvent_t* ev = nullptr);
   // x = B^-1 y with y, x in page-locked host memory: the interior rows move
   // in kSolveChunks pieces on side streams so that each piece's copy overlaps
@@ -316,6 +325,12 @@ struct Precond {
  private:
   void ensure_side_streams();
   void chunk_rows(int c, int& lo, int& hi) const;
+  struct Scratch {
+    DevBuf z1, t, w;
+  };
+  Scratch& scratch_for(cudaStream_t s);
+  std::mutex scratch_mu;
+  std::vector<std::pair<cudaStream_t, std::unique_ptr<Scratch>>> scratch;
   cudaStream_t side[kSolveChunks] = {};
   cudaEvent_t ev_in[kSolveChunks] = {}, ev_out[kSolveChunks] = {}, ev_mid = nullptr;
 };

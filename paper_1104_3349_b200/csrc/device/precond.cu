@@ -223,6 +223,18 @@ Precond::~Precond() {
   if (ev_mid) cudaEventDestroy(ev_mid);
 }
 
+Precond::Scratch& Precond::scratch_for(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(scratch_mu);
+  for (auto& e : scratch)
+    if (e.first == s) return *e.second;
+  auto sc = std::make_unique<Scratch>();
+  sc->z1 = DevBuf(sizeof(double) * std::max(1, p));
+  sc->t = DevBuf(sizeof(double) * std::max(1, n - p));
+  sc->w = DevBuf(sizeof(double) * std::max(1, p));
+  scratch.emplace_back(s, std::move(sc));
+  return *scratch.back().second;
+}
+
 void Precond::ensure_side_streams() {
   if (side[0]) return;
   for (int c = 0; c < kSolveChunks; ++c) {
@@ -276,10 +288,15 @@ void Precond::apply_host(const double* y_h, double* x_h, double* d_y, double* d_
                          cudaStream_t s) {
   if (shard.on) throw Error(1, "MscPreconditioner::apply: this is a shard (use apply_shard_*)");
   ensure_side_streams();
-  double* z1 = this->z1.as<double>();
-  double* t = this->t.as<double>();
-  double* w = this->w.as<double>();
+  // keyed by this preconditioner's private side stream: host-buffer applies
+  // are serialised by the context lock, and a device-buffer apply on s from
+  // another thread must not share these vectors
+  Scratch& sc = scratch_for(side[0]);
+  double* z1 = sc.z1.as<double>();
+  double* t = sc.t.as<double>();
+  double* w = sc.w.as<double>();
   const int ng = n - p;
+  const bool corr_on = corr && use_corr;
   auto rows = [&](int c, int& lo, int& hi) { chunk_rows(c, lo, hi); };
   // order the side streams after earlier work on s (scratch reuse)
   MSCG_CUDA(cudaEventRecord(ev_mid, s));
@@ -304,7 +321,7 @@ void Precond::apply_host(const double* y_h, double* x_h, double* d_y, double* d_
     block_trisolve(*S, t, d_x + p, nullptr, s);
     ctx->launches++;
     MSCG_CUDA(cudaMemcpyAsync(x_h + p, d_x + p, sizeof(double) * ng, cudaMemcpyDeviceToHost, s));
-    if (!corr) spmv(*E, d_x + p, w, nullptr, 0, s);
+    if (!corr_on) spmv(*E, d_x + p, w, nullptr, 0, s);
   }
   MSCG_CUDA(cudaEventRecord(ev_mid, s));
   // 3. per chunk: x1 = z1 - D^-1 w on those blocks, rows out
@@ -313,7 +330,7 @@ void Precond::apply_host(const double* y_h, double* x_h, double* d_y, double* d_
     rows(c, lo, hi);
     MSCG_CUDA(cudaStreamWaitEvent(side[c], ev_mid, 0));
     if (S) {
-      if (corr)
+      if (corr_on)
         apply_correction(*corr, d_x + p, z1, d_x, c, side[c]);
       else
         block_trisolve(*D, w, d_x, z1, side[c], nullptr, c);
@@ -334,9 +351,10 @@ void Precond::apply(const double* y, double* x, cudaStream_t s, cudaEvent_t* ev)
   if (shard.on) throw Error(1, "MscPreconditioner::apply: this is a shard (use apply_shard_*)");
   // ev (optional): 6 events bracketing the 5 stages (ev[0] before stage 0,
   // ev[k+1] after stage k) for the bench's per-kernel timing.
-  double* z1 = this->z1.as<double>();
-  double* t = this->t.as<double>();
-  double* w = this->w.as<double>();
+  Scratch& sc = scratch_for(s);
+  double* z1 = sc.z1.as<double>();
+  double* t = sc.t.as<double>();
+  double* w = sc.w.as<double>();
   auto mark = [&](int k) {
     if (ev) MSCG_CUDA(cudaEventRecord(ev[k], s));
   };
@@ -350,7 +368,7 @@ void Precond::apply(const double* y, double* x, cudaStream_t s, cudaEvent_t* ev)
     block_trisolve(*S, t, x + p, nullptr, s);
     ctx->launches++;
     mark(3);
-    if (corr) {
+    if (corr && use_corr) {
       // x1 = z1 - (D^-1 E) z2 with the precomputed panels (correct.cu)
       mark(4);
       apply_correction(*corr, x + p, z1, x, -1, s);

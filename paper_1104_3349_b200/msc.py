@@ -235,6 +235,69 @@ class TriangularFactors:
         return self.lower.nnz + self.upper.nnz
 
 
+class DeviceFactors(TriangularFactors):
+    """factor_ilut / factor_exact of one block, resident on the device
+    (factorization.hpp:18-43): the reference CSR fields are downloaded once,
+    `solve` runs the device triangular solve."""
+
+    def __init__(self, ctx: Context, handle, kind: str):
+        self.ctx, self.h = ctx, handle
+        st = api.Status()
+        d, nl, nu = C.c_int(), C.c_int64(), C.c_int64()
+        L = api.lib()
+        _check(L.mscg_factors_get(handle, C.byref(d), C.byref(nl), C.byref(nu), None, None,
+                                  None, None, None, None, None, C.byref(st)), st)
+        n = d.value
+        lrp, urp = np.empty(n + 1, np.int32), np.empty(n + 1, np.int32)
+        lci, lv = np.empty(max(1, nl.value), np.int32), np.empty(max(1, nl.value))
+        uci, uv = np.empty(max(1, nu.value), np.int32), np.empty(max(1, nu.value))
+        perm = np.empty(n, np.int32)
+        _check(L.mscg_factors_get(handle, C.byref(d), C.byref(nl), C.byref(nu), _ptr(lrp),
+                                  _ptr(lci), _ptr(lv), _ptr(urp), _ptr(uci), _ptr(uv),
+                                  _ptr(perm), C.byref(st)), st)
+        super().__init__(SparseMatrix(n, n, lrp, lci[: nl.value], lv[: nl.value]),
+                         SparseMatrix(n, n, urp, uci[: nu.value], uv[: nu.value]), perm, kind)
+
+    def solve(self, b):
+        """x = U^-1 L^-1 P b (factorization.cpp:129-158) on the device."""
+        b = np.ascontiguousarray(b, np.float64)
+        if b.shape != (self.dim(),):
+            raise ValueError("solve: rhs length mismatch")
+        x = np.empty(self.dim())
+        st = api.Status()
+        _check(api.lib().mscg_factors_solve(self.h, _ptr(b), _ptr(x), api.MEM_HOST,
+                                            C.byref(st)), st)
+        return x
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            api.lib().mscg_factors_destroy(self.h)
+            self.h = None
+
+
+def _factor(a: SparseMatrix, kind: int, tol: float, ctx: Context | None):
+    if a.nrows != a.ncols:
+        raise ValueError("factor_exact: matrix not square" if kind else
+                         "factor_ilut: matrix not square")
+    ctx = ctx or default_context()
+    rp, ci, v = a.arrays()
+    h = C.c_void_p()
+    st = api.Status()
+    _check(api.lib().mscg_factor(ctx.h, a.nrows, _ptr(rp), _ptr(ci), _ptr(v), kind, tol,
+                                 C.byref(h), C.byref(st)), st)
+    return DeviceFactors(ctx, h, "exact" if kind else "incomplete")
+
+
+def factor_ilut(a: SparseMatrix, drop_tol: float, ctx: Context | None = None) -> DeviceFactors:
+    """Row-wise ILUT (factorization.hpp:38) on the device (ilut_kernel)."""
+    return _factor(a, 0, drop_tol, ctx)
+
+
+def factor_exact(a: SparseMatrix, ctx: Context | None = None) -> DeviceFactors:
+    """LU with partial pivoting (factorization.hpp:32) on the device."""
+    return _factor(a, 1, 0.0, ctx)
+
+
 class MscPreconditioner:
     """Device-resident MSC preconditioner B = [D 0; F S^][D^-1 0; 0 S^-1][D E; 0 S^]."""
 
@@ -286,6 +349,19 @@ class MscPreconditioner:
         if is_t:
             self.ctx.synchronize()
         return x
+
+    def apply_on_stream(self, y, x, stream_handle: int):
+        """Enqueue x = B^-1 y (contiguous float64 CUDA tensors) on the given
+        cudaStream_t; safe to call from several threads at once."""
+        st = api.Status()
+        _check(api.lib().mscg_precond_apply_stream(self.h, C.c_void_p(y.data_ptr()),
+                                                   C.c_void_p(x.data_ptr()),
+                                                   C.c_void_p(stream_handle), C.byref(st)), st)
+
+    def use_correction(self, on: bool):
+        """Apply with the explicit correction panels (when built) or the
+        reference's E SpMV + second interior solve."""
+        api.lib().mscg_precond_use_correction(self.h, int(bool(on)))
 
     def apply_async(self, y_ptr: int, x_ptr: int):
         """Enqueue x = B^-1 y on the context stream (raw device pointers)."""

@@ -8,6 +8,16 @@ oracle restatement.
 
     python tests/golden/make_golden.py [--cfg2]     (--cfg2 adds the 3-minute
                                                      GMRES(50) reference solve)
+    python tests/golden/make_golden.py --only cfg3p|cfg4|cfg5
+        cfg3p: BASELINE cfg3 at stretch 1.0313: full apply(y) + the capped
+               GMRES(50) history (3000 its, ~15 min);
+        cfg4:  apply(y) fingerprint + the first GMRES(100) cycle (100 its,
+               ~10 min after a ~2 min threaded ILUT);
+        cfg5:  apply(y) fingerprint (~55 GB host RAM).
+    The large configs factor their interior blocks with the reference's
+    factor_ilut on all host threads (ref_build_precond_parallel: the same
+    MscPreconditioner build_preconditioner returns, only the block loop is
+    concurrent); apply and gmres are the reference's own, single-threaded.
 """
 import argparse
 import hashlib
@@ -168,6 +178,98 @@ def cfg2(run_gmres: bool):
         json.dump(s, f, indent=1)
 
 
+def apply_fingerprint(x, d_ranges, schur_ranges, p, nsample=50000):
+    """Size-independent summary of an apply output that still touches every
+    unknown: per interior block and per Schur aggregate the 2-norm and the
+    plain sum, the global norm, and an evenly strided sample."""
+    x = np.asarray(x, np.float64)
+    stride = max(1, len(x) // nsample)
+    blk = [x[a:b] for a, b in d_ranges]
+    agg = [x[p + a:p + b] for a, b in schur_ranges]
+    return dict(block_norm=np.array([np.linalg.norm(v) for v in blk]),
+                block_sum=np.array([np.sum(v) for v in blk]),
+                agg_norm=np.array([np.linalg.norm(v) for v in agg]),
+                agg_sum=np.array([np.sum(v) for v in agg]),
+                norm=np.array([np.linalg.norm(x)]), stride=np.array([stride]),
+                sample=x[::stride].copy())
+
+
+def _large_precond(grid_n, nu, n_a, variant, sz, mode, stretched=False, stretch=1.056,
+                   anchored=False):
+    t = time.time()
+    P = refpy.Problem.oseen(grid_n, nu, n_a, stretched=stretched, stretch=stretch,
+                            anchored=anchored)
+    P.build_schur(variant, sz, mode, workers=0)
+    t_setup = time.time() - t
+    t = time.time()
+    P.build_precond_parallel(1e-4, 0, workers=0)
+    t_ilut = time.time() - t
+    s = problem_summary(P, with_factors=False)
+    s.pop("d_ranges")
+    s["stored_nnz"] = P.stored_nnz()
+    s["generate_partition_msc_seconds_ref"] = t_setup
+    s["ilut_seconds_ref_threads"] = t_ilut
+    s["threads"] = refpy.hardware_threads()
+    return P, s
+
+
+def cfg3p():
+    """BASELINE cfg3 with stretch 1.0313 (max aspect 50.1)."""
+    P, s = _large_precond(256, 0.002, 64, "lum", 795, 0, stretched=True, stretch=1.0313)
+    y = refpy.random_vector(P.n, 0)
+    t = time.time()
+    x = P.apply(y)
+    s["apply_seconds_ref"] = time.time() - t
+    s["apply_y_norm"] = float(np.linalg.norm(x))
+    np.savez_compressed(os.path.join(HERE, "cfg3p_apply.npz"), apply_y=x)
+    r = P.gmres(y, 50, 3000, 1e-8)
+    s["gmres"] = dict(restart=50, max_iters=3000, rel_tol=1e-8, iterations=r["iterations"],
+                      converged=r["converged"], seconds=r["seconds"],
+                      history=r["history"].tolist())
+    with open(os.path.join(HERE, "cfg3p.json"), "w") as f:
+        json.dump(s, f, indent=1)
+
+
+def cfg4_cycle():
+    """BASELINE cfg4: apply fingerprint + the first GMRES(100) cycle."""
+    P, s = _large_precond(1024, 0.001, 1024, "lum", 256, 1, anchored=True)
+    y = refpy.random_vector(P.n, 0)
+    t = time.time()
+    x = P.apply(y)
+    s["apply_seconds_ref"] = time.time() - t
+    fp = apply_fingerprint(x, P.d_ranges(), P.schur_ranges(), P.p)
+    np.savez_compressed(os.path.join(HERE, "cfg4_apply_fp.npz"), **fp)
+    r = P.gmres(y, 100, 100, 1e-8)
+    s["gmres_first_cycle"] = dict(restart=100, max_iters=100, rel_tol=1e-8,
+                                  iterations=r["iterations"], converged=r["converged"],
+                                  seconds=r["seconds"], history=r["history"].tolist())
+    old = os.path.join(HERE, "cfg4.json")
+    base = json.load(open(old)) if os.path.exists(old) else {}
+    base.update({k: v for k, v in s.items() if k not in base or k in (
+        "stored_nnz", "gmres_first_cycle", "apply_seconds_ref", "ilut_seconds_ref_threads",
+        "threads", "generate_partition_msc_seconds_ref")})
+    with open(old, "w") as f:
+        json.dump(base, f, indent=1)
+
+
+def cfg5_apply():
+    """BASELINE cfg5: apply fingerprint."""
+    P, s = _large_precond(2048, 0.01, 4096, "lum", 256, 1, anchored=True)
+    y = refpy.random_vector(P.n, 0)
+    t = time.time()
+    x = P.apply(y)
+    s["apply_seconds_ref"] = time.time() - t
+    fp = apply_fingerprint(x, P.d_ranges(), P.schur_ranges(), P.p)
+    np.savez_compressed(os.path.join(HERE, "cfg5_apply_fp.npz"), **fp)
+    old = os.path.join(HERE, "cfg5.json")
+    base = json.load(open(old)) if os.path.exists(old) else {}
+    for k in ("stored_nnz", "apply_seconds_ref", "ilut_seconds_ref_threads", "threads",
+              "generate_partition_msc_seconds_ref"):
+        base[k] = s[k]
+    with open(old, "w") as f:
+        json.dump(base, f, indent=1)
+
+
 def cfg_large(grid_n, nu, n_a, name):
     """Setup-only digests at cfg4/cfg5 (anchored LUM, sz 256)."""
     t = time.time()
@@ -184,8 +286,14 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true", help="also run the cfg2 GMRES (~3 min)")
     ap.add_argument("--large", action="store_true", help="cfg4/cfg5 setup digests (~5 min)")
+    ap.add_argument("--only", choices=["cfg2gmres", "cfg3p", "cfg4", "cfg5"])
     a = ap.parse_args()
     refpy.build()
+    if a.only:
+        {"cfg2gmres": lambda: cfg2(True), "cfg3p": cfg3p, "cfg4": cfg4_cycle,
+         "cfg5": cfg5_apply}[a.only]()
+        print("written", a.only)
+        sys.exit(0)
     cfg1()
     random_saddles()
     ilut_contracts()
