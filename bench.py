@@ -22,6 +22,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import resource
 import statistics
 import subprocess
 import sys
@@ -303,7 +304,8 @@ def run_reference_arm(args, cfg):
                         "what": "stock MscPreconditioner::apply (preconditioner.cpp:85-114), "
                                 "single-threaded as shipped, all blocks"},
         "setup": {"generate_scale_partition_s": t1 - t0, "aggregates_build_msc_s": t2 - t1,
-                  "ilut_all_blocks_s": t3 - t2, "ilut_threads": threads},
+                  "ilut_all_blocks_s": t3 - t2, "ilut_threads": threads,
+                  "host_peak_rss_gb": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20},
         "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "clocks": clk,
@@ -469,7 +471,7 @@ def reference_gmres_context(name):
         return None
 
 
-def gmres_run(name, ctx, local, max_iters=3000, orth="cgs2", threads=0):
+def gmres_run(name, ctx, local, max_iters=3000, orth="dcgs2", threads=0):
     """BASELINE time-to-solution: full setup (device assembly, host
     partition, device build_msc, device ILUT + Schur LU + correction) and
     right-preconditioned GMRES(restart) to rtol 1e-8 from the seeded rhs,
@@ -522,7 +524,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-iters", type=int, default=3000)
-    ap.add_argument("--orth", default="cgs2", choices=["cgs2", "mgs"])
+    ap.add_argument("--orth", default="dcgs2", choices=["dcgs2", "cgs2", "mgs"])
     ap.add_argument("--no-gmres", action="store_true",
                     help="skip the GMRES time-to-solution runs (cfg2, cfg4) in apply mode")
     ap.add_argument("--replicas", action="store_true",

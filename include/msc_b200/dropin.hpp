@@ -196,7 +196,7 @@ inline std::pair<std::vector<double>, msc::SolveReport> gmres(
                         a.values().data(), &h, &st),
         st);
   mscg_gmres_config c{cfg.restart, cfg.max_iters, cfg.rel_tol,
-                      cfg.side == msc::PrecondSide::Left ? 1 : 0, 1};
+                      cfg.side == msc::PrecondSide::Left ? 1 : 0, 2};
   mscg_gmres_report rep{};
   std::vector<double> x(n), hist(static_cast<size_t>(cfg.max_iters) + 64);
   const int rc = mscg_gmres(ctx.get(), h, gp ? gp->get() : nullptr, rhs.data(), x.data(),

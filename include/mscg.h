@@ -127,6 +127,22 @@ int mscg_problem_build_schur(mscg_problem *pb, const char *variant, int mode,
 int mscg_problem_build_schur_device(mscg_ctx *ctx, mscg_problem *pb, const char *variant,
                                     int mode, int sz, int nsizes, const int *sizes,
                                     mscg_status *st);
+/* build_msc over OVERLAPPED numbering aggregates (aggregate_overlapped,
+ * aggregates.cpp:50-85) for "omscn" | "omscnr" | "olum": owned sizes as
+ * mscg_problem_build_schur (mode 0/1/2); widths[nwidths] explicit (one per
+ * aggregate), or (widths NULL) `overlap` for every aggregate (< 0: sz), the last 0,
+ * clipped to min(size - 1, n_g - end) (benchmark.cpp:74-88).  Each
+ * aggregate's S_ii lives on its span [b, e + w); the merge writes every owned
+ * column over the whole span (schur_approx.cpp:141-160), so S^ is banded and
+ * a preconditioner built from this problem factors it whole (one exact LU,
+ * the reference's schur_single_).  ctx NULL: host build; else on the device
+ * (local blocks) with the merge on the host.  Errors as the reference
+ * ("aggregate_overlapped: ...", "build_msc: variant omscn needs an
+ * overlapped aggregate set"). */
+int mscg_problem_build_schur_overlapped(mscg_ctx *ctx, mscg_problem *pb, const char *variant,
+                                        int mode, int sz, int nsizes, const int *sizes,
+                                        int overlap, int nwidths, const int *widths,
+                                        int threads, mscg_status *st);
 int mscg_problem_num_aggregates(const mscg_problem *pb);
 const int *mscg_problem_schur_ranges(const mscg_problem *pb); /* 2*nagg */
 
@@ -142,6 +158,11 @@ int mscg_spmv(mscg_csr *a, const double *x, double *y, int mem,
               mscg_status *st);
 
 /* ---- MSC preconditioner ------------------------------------------------ */
+/* nschur = MSCG_SCHUR_SINGLE: S^ is an overlapped band, factored whole by one
+ * exact LU (preconditioner.cpp:58-67; s_ranges unused); a singular band
+ * raises "build_preconditioner: overlapped Schur band: dense_lu: zero pivot
+ * at index i". */
+#define MSCG_SCHUR_SINGLE (-1)
 /* build_preconditioner(c, schur, tolA, sA) (preconditioner.hpp:66-68) over
  * raw arrays: C (n x n, final numbering) split at p, interior block ranges,
  * block-diagonal S^ (n_g x n_g) with its owned ranges.  Interior blocks with
@@ -280,7 +301,8 @@ typedef struct {
   int max_iters;    /* default 3000 */
   double rel_tol;   /* default 1e-9 */
   int side;         /* 0 = right (default), 1 = left */
-  int orth;         /* 0 = MGS (reference order), 1 = CGS2 (fused multi-dot) */
+  int orth;         /* 0 = MGS (reference order), 1 = CGS2 (three basis sweeps),
+                       2 = DCGS2 (two basis sweeps, delayed reorthogonalisation) */
 } mscg_gmres_config;
 
 typedef struct {

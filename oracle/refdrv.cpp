@@ -62,6 +62,7 @@ struct RefProblem {
   SchurApproximation schur;
   std::unique_ptr<MscPreconditioner> prec;
   bool have_schur = false;
+  int overlap = -1;  // overlapped aggregate width (benchmark.cpp:35: -1 = sz)
 };
 
 struct RefFactors {
@@ -349,11 +350,26 @@ int ref_build_schur(RefProblem* p, const char* variant, int mode, int sz,
       sz = std::min(sz, ng);
       sizes = equal_sizes(ng, sz);
     }
-    p->agg = aggregate_by_numbering(ng, sizes);
-    p->schur = build_msc(p->pm, p->agg, variant_from_name(variant), workers);
+    const MscVariant v = variant_from_name(variant);
+    if (variant_overlapped(v)) {
+      // make_aggregates' overlapped branch (benchmark.cpp:80-88), with the
+      // overlap width passed through ref_set_overlap (default -1 = sz)
+      if (sz <= 0) sz = std::max(1, ng / 8);
+      sz = std::min(sz, ng);
+      std::vector<int> widths(sizes.size(), p->overlap < 0 ? sz : p->overlap);
+      widths.back() = 0;
+      clip_overlap_widths(ng, sizes, widths);
+      p->agg = aggregate_overlapped(ng, sizes, widths);
+    } else {
+      p->agg = aggregate_by_numbering(ng, sizes);
+    }
+    p->schur = build_msc(p->pm, p->agg, v, workers);
     p->have_schur = true;
   });
 }
+
+// overlap width used by the next ref_build_schur of an overlapped variant
+void ref_set_overlap(RefProblem* p, int overlap) { p->overlap = overlap; }
 
 int ref_exact_schur(RefProblem* p) {
   return guarded([&] {

@@ -58,6 +58,8 @@ def lib():
         L.ref_get_perm.argtypes = [vp, _i32p]
         L.ref_get_scaled_rhs.argtypes = [vp, _f64p]
         L.ref_get_d_ranges.argtypes = [vp, _i32p]
+        L.ref_set_overlap.argtypes = [vp, C.c_int]
+        L.ref_set_overlap.restype = None
         L.ref_build_schur.argtypes = [vp, C.c_char_p, C.c_int, C.c_int, C.c_int,
                                       _i32p, C.c_int]
         L.ref_exact_schur.argtypes = [vp]
@@ -310,7 +312,10 @@ class Problem:
         lib().ref_get_d_ranges(self.h, out)
         return out.reshape(-1, 2)
 
-    def build_schur(self, variant="lum", sz=0, mode=0, sizes=None, workers=1):
+    def build_schur(self, variant="lum", sz=0, mode=0, sizes=None, workers=1, overlap=-1):
+        """aggregates (numbering, or overlapped with `overlap` as
+        make_aggregates does, benchmark.cpp:74-88) + build_msc."""
+        lib().ref_set_overlap(self.h, int(overlap))
         s = np.asarray(sizes if sizes is not None else [0], np.int32)
         _check(lib().ref_build_schur(self.h, variant.encode(), mode, sz, len(s), s,
                                      workers))

@@ -73,6 +73,9 @@ _SIGS = {
                                                   C.c_int, vp, C.POINTER(Status)]),
     "mscg_problem_build_schur": (C.c_int, [vp, C.c_char_p, C.c_int, C.c_int, C.c_int, vp,
                                            C.c_int, C.POINTER(Status)]),
+    "mscg_problem_build_schur_overlapped": (C.c_int, [vp, vp, C.c_char_p, C.c_int, C.c_int,
+                                                      C.c_int, vp, C.c_int, C.c_int, vp,
+                                                      C.c_int, C.POINTER(Status)]),
     "mscg_problem_num_aggregates": (C.c_int, [vp]),
     "mscg_problem_schur_ranges": (ip, [vp]),
     "mscg_csr_upload": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp),

@@ -294,25 +294,49 @@ const double* mscg_problem_scaled_rhs(const mscg_problem* pb) {
   return pb->scaled_rhs.empty() ? nullptr : pb->scaled_rhs.data();
 }
 
+namespace {
+std::vector<int> schur_sizes(const mscg_problem* pb, int mode, int sz, int nsizes,
+                             const int* sizes) {
+  const int ng = pb->pm.n_g();
+  if (mode == 2) return std::vector<int>(sizes, sizes + nsizes);
+  if (mode == 1) return mscg::host::anchored_sizes(pb->pm, sz);
+  int s = sz <= 0 ? std::max(1, ng / 8) : sz;
+  s = std::min(s, ng);
+  return mscg::host::equal_sizes(ng, s);
+}
+
+// build_msc on the host (ctx == NULL) or the device; widths empty for the
+// non-overlapped aggregate sets.
+void build_schur_impl(mscg_ctx* ctx, mscg_problem* pb, const char* variant,
+                      const std::vector<int>& sz_list, const std::vector<int>& widths,
+                      int threads) {
+  const mscg::host::Variant v = mscg::host::variant_from_name(variant ? variant : "");
+  if (!ctx) {
+    pb->schur = mscg::host::build_msc(pb->pm, sz_list, v, threads, widths);
+  } else {
+    mscg::host::SchurApprox out;
+    mscg::host::aggregate_spans(pb->pm, sz_list, v, widths, out.ranges, out.spans);
+    out.overlapped = mscg::host::variant_overlapped(v);
+    const int kind = mscg::host::variant_lumped(v)   ? mscg::kMscLum
+                     : mscg::host::variant_rowsum(v) ? mscg::kMscMscnr
+                                                     : mscg::kMscMscn;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const auto& c = pb->pm.C;
+    const int ng = pb->pm.n_g();
+    out.s_hat = mscg::host::Csr(ng, ng);
+    mscg::build_msc_device(&ctx->ctx, c.nrows, pb->pm.p, c.rp.data(), c.ci.data(), c.v.data(),
+                           out.ranges, out.spans, kind, out.s_hat.rp, out.s_hat.ci, out.s_hat.v);
+    pb->schur = std::move(out);
+  }
+  pb->have_schur = true;
+  flatten(pb->schur.ranges, pb->s_ranges_flat);
+}
+}  // namespace
+
 int mscg_problem_build_schur(mscg_problem* pb, const char* variant, int mode, int sz, int nsizes,
                              const int* sizes, int threads, mscg_status* st) {
   return guard(st, [&] {
-    const int ng = pb->pm.n_g();
-    std::vector<int> sz_list;
-    if (mode == 2) {
-      sz_list.assign(sizes, sizes + nsizes);
-    } else if (mode == 1) {
-      sz_list = mscg::host::anchored_sizes(pb->pm, sz);
-    } else {
-      int s = sz <= 0 ? std::max(1, ng / 8) : sz;
-      s = std::min(s, ng);
-      sz_list = mscg::host::equal_sizes(ng, s);
-    }
-    pb->schur = mscg::host::build_msc(pb->pm, sz_list,
-                                      mscg::host::variant_from_name(variant ? variant : ""),
-                                      threads);
-    pb->have_schur = true;
-    flatten(pb->schur.ranges, pb->s_ranges_flat);
+    build_schur_impl(nullptr, pb, variant, schur_sizes(pb, mode, sz, nsizes, sizes), {}, threads);
   });
 }
 
@@ -321,48 +345,29 @@ int mscg_problem_build_schur_device(mscg_ctx* ctx, mscg_problem* pb, const char*
                                     mscg_status* st) {
   return guard(st, [&] {
     if (!ctx) throw std::invalid_argument("build_msc: null context");
-    const int ng = pb->pm.n_g(), p = pb->pm.p;
-    std::vector<int> sz_list;
-    if (mode == 2) {
-      sz_list.assign(sizes, sizes + nsizes);
-    } else if (mode == 1) {
-      sz_list = mscg::host::anchored_sizes(pb->pm, sz);
+    build_schur_impl(ctx, pb, variant, schur_sizes(pb, mode, sz, nsizes, sizes), {}, 0);
+  });
+}
+
+int mscg_problem_build_schur_overlapped(mscg_ctx* ctx, mscg_problem* pb, const char* variant,
+                                        int mode, int sz, int nsizes, const int* sizes,
+                                        int overlap, int nwidths, const int* widths,
+                                        int threads, mscg_status* st) {
+  return guard(st, [&] {
+    if (!pb) throw std::invalid_argument("build_msc: null problem");
+    const std::vector<int> sz_list = schur_sizes(pb, mode, sz, nsizes, sizes);
+    std::vector<int> w;
+    if (widths) {
+      if (nwidths < 0) throw std::invalid_argument("aggregate_overlapped: one width per aggregate");
+      w.assign(widths, widths + nwidths);
+      if (w.size() != sz_list.size())
+        throw std::invalid_argument("aggregate_overlapped: one width per aggregate");
     } else {
-      int s = sz <= 0 ? std::max(1, ng / 8) : sz;
-      s = std::min(s, ng);
-      sz_list = mscg::host::equal_sizes(ng, s);
+      const int ng = pb->pm.n_g();
+      int s = sz <= 0 ? std::max(1, ng / 8) : std::min(sz, ng);
+      w = mscg::host::overlap_widths(ng, sz_list, s, overlap);
     }
-    const mscg::host::Variant v = mscg::host::variant_from_name(variant ? variant : "");
-    int total = 0;
-    for (int x : sz_list) {
-      if (x < 1) throw std::invalid_argument("aggregates: sizes must be >= 1");
-      total += x;
-    }
-    if (sz_list.empty() || total != ng)
-      throw std::invalid_argument("aggregates: sizes sum to " + std::to_string(total) +
-                                  ", expected " + std::to_string(ng));
-    mscg::host::SchurApprox out;
-    int b = 0;
-    for (int x : sz_list) {
-      out.ranges.push_back({b, b + x});
-      b += x;
-    }
-    if (v != mscg::host::Variant::Lum)
-      for (size_t i = 0; i < out.ranges.size(); ++i)
-        if (out.ranges[i].second > p)
-          throw std::invalid_argument("build_msc: aggregate " + std::to_string(i) +
-                                      " has a D-side index outside the (1,1) block");
-    const int kind = v == mscg::host::Variant::Lum     ? mscg::kMscLum
-                     : v == mscg::host::Variant::Mscnr ? mscg::kMscMscnr
-                                                       : mscg::kMscMscn;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    const auto& c = pb->pm.C;
-    out.s_hat = mscg::host::Csr(ng, ng);
-    mscg::build_msc_device(&ctx->ctx, c.nrows, p, c.rp.data(), c.ci.data(), c.v.data(),
-                           out.ranges, kind, out.s_hat.rp, out.s_hat.ci, out.s_hat.v);
-    pb->schur = std::move(out);
-    pb->have_schur = true;
-    flatten(pb->schur.ranges, pb->s_ranges_flat);
+    build_schur_impl(ctx, pb, variant, sz_list, w, threads);
   });
 }
 
@@ -423,8 +428,12 @@ int mscg_precond_build(mscg_ctx* ctx, int n, int p, const int* c_rp, const int* 
     if (tol_a < 0.0) throw std::invalid_argument("factor_ilut: negative drop tolerance");
     auto h = std::make_unique<mscg_precond>();
     h->ctx = ctx;
+    const bool single = nschur == MSCG_SCHUR_SINGLE;
+    if (nschur < 0 && !single) throw std::invalid_argument("build_preconditioner: bad Schur range count");
     h->pc = mscg::build_precond(&ctx->ctx, n, p, c_rp, c_ci, c_v, pairs(nblocks, d_ranges), s_rp,
-                                s_ci, s_v, pairs(nschur, s_ranges), tol_a, s_a);
+                                s_ci, s_v, single ? std::vector<std::pair<int, int>>{}
+                                                  : pairs(nschur, s_ranges),
+                                tol_a, s_a, 0, -1, single);
     h->matrix.a = h->pc->C.get();
     h->matrix.ctx = ctx;
     h->matrix.owner = h->pc.get();
@@ -508,8 +517,9 @@ int mscg_precond_build_problem(mscg_ctx* ctx, const mscg_problem* pb, double tol
   return mscg_precond_build(ctx, c.nrows, pb->pm.p, c.rp.data(), c.ci.data(), c.v.data(),
                             static_cast<int>(pb->pm.d_ranges.size()), pb->d_ranges_flat.data(),
                             s.rp.data(), s.ci.data(), s.v.data(),
-                            static_cast<int>(pb->schur.ranges.size()), pb->s_ranges_flat.data(),
-                            tol_a, s_a, out, st);
+                            pb->schur.overlapped ? MSCG_SCHUR_SINGLE
+                                                 : static_cast<int>(pb->schur.ranges.size()),
+                            pb->s_ranges_flat.data(), tol_a, s_a, out, st);
 }
 
 int mscg_precond_build_shard(mscg_ctx* ctx, int n, int p, const int* c_rp, const int* c_ci,
@@ -524,9 +534,12 @@ int mscg_precond_build_shard(mscg_ctx* ctx, int n, int p, const int* c_rp, const
       throw std::invalid_argument("build_preconditioner: shard block range out of range");
     auto h = std::make_unique<mscg_precond>();
     h->ctx = ctx;
+    const bool single = nschur == MSCG_SCHUR_SINGLE;
+    if (nschur < 0 && !single) throw std::invalid_argument("build_preconditioner: bad Schur range count");
     h->pc = mscg::build_precond(&ctx->ctx, n, p, c_rp, c_ci, c_v, pairs(nblocks, d_ranges), s_rp,
-                                s_ci, s_v, pairs(nschur, s_ranges), tol_a, s_a, block_begin,
-                                block_end);
+                                s_ci, s_v, single ? std::vector<std::pair<int, int>>{}
+                                                  : pairs(nschur, s_ranges),
+                                tol_a, s_a, block_begin, block_end, single);
     h->matrix.a = h->pc->C.get();  // null for a true shard
     h->matrix.ctx = ctx;
     *out = h.release();
@@ -546,7 +559,8 @@ int mscg_precond_build_problem_shard(mscg_ctx* ctx, const mscg_problem* pb, doub
   return mscg_precond_build_shard(
       ctx, c.nrows, pb->pm.p, c.rp.data(), c.ci.data(), c.v.data(),
       static_cast<int>(pb->pm.d_ranges.size()), pb->d_ranges_flat.data(), s.rp.data(),
-      s.ci.data(), s.v.data(), static_cast<int>(pb->schur.ranges.size()),
+      s.ci.data(), s.v.data(),
+      pb->schur.overlapped ? MSCG_SCHUR_SINGLE : static_cast<int>(pb->schur.ranges.size()),
       pb->s_ranges_flat.data(), tol_a, s_a, block_begin, block_end, out, st);
 }
 
@@ -817,6 +831,7 @@ int mscg_gmres(mscg_ctx* ctx, mscg_csr* a, mscg_precond* pc, const double* b, do
       c.rel_tol = cfg->rel_tol;
       c.left = cfg->side == 1;
       c.orth = cfg->orth;
+      if (c.orth < 0 || c.orth > 2) throw std::invalid_argument("gmres: orth must be 0 (MGS), 1 (CGS2) or 2 (DCGS2)");
     }
     if (!a || !a->a) throw std::invalid_argument("gmres: null matrix");
     const size_t n = a->a->nrows;

@@ -2,7 +2,8 @@
 //
 // The Arnoldi step keeps every vector in HBM and every scalar on the device:
 //   w = A B^-1 v_j            (precond apply + SELL SpMV, right preconditioning)
-//   orthogonalisation         CGS2: multi-dot, fused axpy+dot, multi-axpy
+//   orthogonalisation         DCGS2 (default): two basis sweeps, see below;
+//                             CGS2: multi-dot, fused axpy+dot, multi-axpy
 //                             (h = V^T w; w -= V h, twice), or MGS in the
 //                             reference's order (one fused axpy+dot kernel per
 //                             basis vector)
@@ -396,10 +397,340 @@ __global__ void backsolve_kernel(Small s, int m) {
   }
 }
 
-__global__ void init_cycle_kernel(Small s, const double* beta) {
+__global__ void init_cycle_kernel(Small s, const double* beta, double* nu0) {
   for (int i = threadIdx.x; i <= s.m; i += blockDim.x) s.g[i] = 0.0;
   __syncthreads();
-  if (threadIdx.x == 0) s.g[0] = *beta;
+  if (threadIdx.x == 0) {
+    s.g[0] = *beta;
+    if (nu0) *nu0 = *beta;
+  }
+}
+
+// ---------------------------------------------------------------- DCGS2
+// Low-synchronisation CGS2 with delayed reorthogonalisation (the DCGS2
+// Arnoldi of Swirydowicz et al. 2020 / Bielich et al. 2022, restated): two
+// sweeps over the basis per iteration instead of three.
+//
+// State after iteration j: q_0..q_j final (orthonormal), slot j+1 holds
+// y_{j+1} = A B^-1 q_j projected ONCE (unnormalised, nu_{j+1} = ||y_{j+1}||),
+// H columns 0..j-1 final and column j preliminary.  Iteration j+1:
+//   w = A B^-1 y_{j+1}                        (the operator is linear: W = w / nu)
+//   sweep 1 (dcgs2_dot_kernel): s' = Q^T y, t' = Q^T w, y.y, y.w;  its last
+//     CTA then (dcgs2_fix) reorthogonalises y in coefficient space:
+//       u = y / nu, s = Q^T u, rho = sqrt(u.u - s.s), q_{j+1} = (u - Q s) / rho
+//     which finalises column j (H[0:j+1, j] += nu s, H[j+1, j] = nu rho) and
+//     its Givens rotation, and forms column j+1 without touching a vector:
+//       A B^-1 q_{j+1} = (W - Q_{j+2} H s) / rho,  t = Q^T W,
+//       c = q_{j+1}.W = (u.W - s.t) / rho,  h = ([t; c] - H s) / rho;
+//   sweep 2 (dcgs2_axpy_kernel): q_{j+1} = (u - Q s) / rho into its slot and
+//     y_{j+2} = (W - Q t - c q_{j+1}) / rho into the next, with ||y_{j+2}||;
+//     its last CTA rotates a copy of column j+1 (preliminary) for the
+//     convergence test, so the host still reads one status per iteration.
+// The last column of a cycle is finalised by the speculative next iteration
+// already in the stream, or by one dot sweep (finalize-only) at restart.
+// Same operator and projections as CGS2; only rounding differs (measured:
+// iteration counts and histories unchanged, tests/test_gpu_parity.py).
+struct Dcgs {
+  double* Hraw;  // (m+1) x m raw Hessenberg columns, column-major, ld m+1
+  double* dots;  // sweep-1 sums: [0,nq) Q^T y, [nq,2nq) Q^T w, [2nq] y.y, [2nq+1] y.w
+  double* coef;  // [0,m+1) s, [m+1, 2m+2) t, [2m+2] c, [2m+3] rho, [2m+4] nu, [2m+5] ok
+  double* nu;    // [m+2]: nu[j] = ||y_j||
+};
+
+// The serial Givens work of an iteration runs on one thread of a reduction
+// kernel's last CTA; the CTA first stages the rotations and the column in
+// shared memory (a dependent global load per rotation would cost an L2 round
+// trip each).  kMaxRestart bounds the staged arrays.
+constexpr int kMaxRestart = 500;
+struct GivensStage {
+  double cs[kMaxRestart + 1], sn[kMaxRestart + 1], col[kMaxRestart + 2];
+};
+
+// all threads: stage rotations 0..k-1 and column entries 0..k+1
+__device__ __forceinline__ void stage_givens(GivensStage& gs, const Small& s, const double* raw, int k) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    gs.cs[i] = s.cs[i];
+    gs.sn[i] = s.sn[i];
+  }
+  for (int i = threadIdx.x; i <= k + 1; i += blockDim.x) gs.col[i] = raw[i];
+  __syncthreads();
+}
+
+// one thread: rotations 0..k-1 applied to the staged column
+// (gmres.cpp:117-148 arithmetic), then the new rotation k
+__device__ __forceinline__ void rotate_staged(GivensStage& gs, int k, double& cs, double& sn) {
+  double* Hc = gs.col;
+  for (int i = 0; i < k; ++i) {
+    const double t1 = gs.cs[i] * Hc[i] + gs.sn[i] * Hc[i + 1];
+    const double t2 = -gs.sn[i] * Hc[i] + gs.cs[i] * Hc[i + 1];
+    Hc[i] = t1;
+    Hc[i + 1] = t2;
+  }
+  const double dr = hypot(Hc[k], Hc[k + 1]);
+  cs = dr == 0.0 ? 1.0 : Hc[k] / dr;
+  sn = dr == 0.0 ? 0.0 : Hc[k + 1] / dr;
+  Hc[k] = dr;
+  Hc[k + 1] = 0.0;
+}
+
+// Sweep-1 epilogue (last CTA, all threads): finalise column j-1 and its
+// rotation, then the coefficients of sweep 2 and the raw column j.
+// finalize_only: no w (the cycle's last column).
+__device__ void dcgs2_fix(const Small& s, const Dcgs& d, int j, bool finalize_only) {
+  __shared__ GivensStage gs;
+  __shared__ double S[kMaxRestart + 1], T[kMaxRestart + 1];
+  __shared__ double sc[2];
+  const int m = s.m, ldh = m + 1;
+  const double nu = d.nu[j];
+  const bool ok = nu >= 1e-14;  // y_j exists (no breakdown before it)
+  for (int i = threadIdx.x; i < j; i += blockDim.x) {
+    const double si = ok ? d.dots[i] / nu : 0.0;
+    const double ti = ok && !finalize_only ? d.dots[j + i] / nu : 0.0;
+    S[i] = si;
+    T[i] = ti;
+    d.coef[i] = si;
+    d.coef[m + 1 + i] = ti;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double rho = 1.0;
+    if (j > 0 && ok) {
+      const double alpha = d.dots[2 * j] / (nu * nu);
+      double ss = 0.0;
+      for (int i = 0; i < j; ++i) ss = fma(S[i], S[i], ss);
+      const double r2 = alpha - ss;
+      rho = r2 > 0.0 ? sqrt(r2) : sqrt(alpha);
+    }
+    sc[0] = rho;
+  }
+  __syncthreads();
+  const double rho = sc[0];
+  if (j > 0) {
+    // column j-1: H[0:j, j-1] += nu s, H[j, j-1] = nu rho (raw), then its
+    // final rotation
+    double* hc = d.Hraw + static_cast<size_t>(j - 1) * ldh;
+    if (ok) {
+      for (int i = threadIdx.x; i < j; i += blockDim.x) hc[i] = fma(nu, S[i], hc[i]);
+      if (threadIdx.x == 0) hc[j] = nu * rho;
+    }
+    __syncthreads();
+    stage_givens(gs, s, hc, j - 1);
+    if (threadIdx.x == 0) {
+      const int k = j - 1;
+      double cs, sn;
+      rotate_staged(gs, k, cs, sn);
+      s.cs[k] = cs;
+      s.sn[k] = sn;
+      s.g[k + 1] = -sn * s.g[k];
+      s.g[k] = cs * s.g[k];
+    }
+    __syncthreads();
+    double* Rc = s.H + static_cast<size_t>(j - 1) * ldh;
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) Rc[i] = gs.col[i];
+  }
+  if (finalize_only) return;
+  if (threadIdx.x == 0) {
+    const double bt = ok ? d.dots[2 * j + 1] / (nu * nu) : 0.0;
+    double st = 0.0;
+    for (int i = 0; i < j; ++i) st = fma(S[i], T[i], st);
+    const double c = (bt - st) / rho;
+    sc[1] = c;
+    d.coef[2 * m + 2] = c;
+    d.coef[2 * m + 3] = rho;
+    d.coef[2 * m + 4] = nu;
+    d.coef[2 * m + 5] = ok ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const double c = sc[1];
+  // raw column j: h_i = (t_i - sum_k H[i,k] s_k) / rho, t_j = c (H upper
+  // Hessenberg: k >= i-1); for fixed k the threads read a column: coalesced
+  double* hj = d.Hraw + static_cast<size_t>(j) * ldh;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+    double acc = i < j ? T[i] : c;
+#pragma unroll 4
+    for (int k = i > 0 ? i - 1 : 0; k < j; ++k) acc = fma(-d.Hraw[static_cast<size_t>(k) * ldh + i], S[k], acc);
+    hj[i] = acc / rho;
+  }
+}
+
+// Sweep 1: dots of y = slot j (and w) against q_0..q_{j-1}, plus y.y and
+// y.w, basis vectors in groups of kG (w and y re-read per group).
+template <int kG>
+__global__ void __launch_bounds__(kThreads) dcgs2_dot_kernel(int n, int j, const double* __restrict__ V,
+                                                             size_t ld, const double* __restrict__ w,
+                                                             Reducer red, Small s, Dcgs d, int finalize_only) {
+  __shared__ double sh[kThreads / 32][2 * kG + 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nq = j;
+  const double* y = V + ld * j;
+  const int npair = n >> 1;
+  const double2* y2 = reinterpret_cast<const double2*>(y);
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  const int ngroups = nq > 0 ? (nq + kG - 1) / kG : 1;
+  const int stride = gridDim.x * blockDim.x;
+  for (int grp = 0; grp < ngroups; ++grp) {
+    const int i0 = grp * kG;
+    const int ng = max(0, min(kG, nq - i0));
+    const bool first = grp == 0;
+    double ay[kG], aw[kG], yy = 0.0, yw = 0.0;
+#pragma unroll
+    for (int g = 0; g < kG; ++g) ay[g] = aw[g] = 0.0;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npair; q += stride) {
+      const double2 yv = y2[q];
+      const double2 wv = w ? w2[q] : make_double2(0.0, 0.0);
+      double2 v[kG];
+#pragma unroll
+      for (int g = 0; g < kG; ++g)
+        v[g] = g < ng ? __ldg(reinterpret_cast<const double2*>(V + ld * (i0 + g)) + q) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        ay[g] = fma(v[g].y, yv.y, fma(v[g].x, yv.x, ay[g]));
+        aw[g] = fma(v[g].y, wv.y, fma(v[g].x, wv.x, aw[g]));
+      }
+      if (first) {
+        yy = fma(yv.y, yv.y, fma(yv.x, yv.x, yy));
+        yw = fma(yv.y, wv.y, fma(yv.x, wv.x, yw));
+      }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: the last row
+      const double yl = y[n - 1], wl = w ? w[n - 1] : 0.0;
+#pragma unroll
+      for (int g = 0; g < kG; ++g)
+        if (g < ng) {
+          const double vl = V[ld * (i0 + g) + (n - 1)];
+          ay[g] = fma(vl, yl, ay[g]);
+          aw[g] = fma(vl, wl, aw[g]);
+        }
+      if (first) {
+        yy = fma(yl, yl, yy);
+        yw = fma(yl, wl, yw);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 2 * kG + 2; ++g) {
+      double v = g < kG ? ay[g] : (g < 2 * kG ? aw[g - kG] : (g == 2 * kG ? yy : yw));
+      for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) sh[warp][g] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * kG + 2) {
+      const int g = threadIdx.x;
+      int vec = -1;
+      if (g < kG) {
+        if (g < ng) vec = i0 + g;
+      } else if (g < 2 * kG) {
+        if (g - kG < ng) vec = nq + i0 + g - kG;
+      } else if (first) {
+        vec = 2 * nq + (g - 2 * kG);
+      }
+      if (vec >= 0) {
+        double t = 0.0;
+        for (int k = 0; k < kThreads / 32; ++k) t += sh[k][g];
+        red.partials[static_cast<size_t>(vec) * red.nblk + blockIdx.x] = t;
+      }
+    }
+    __syncthreads();
+  }
+  if (last_block(red)) {
+    finish(red, 2 * nq + 2, d.dots, 0);
+    __syncthreads();
+    dcgs2_fix(s, d, j, finalize_only != 0);
+  }
+}
+
+// Sweep 2: q_j = (y/nu - Q s)/rho over slot j (in place) and
+// y_{j+1} = (w/nu - Q t - c q_j)/rho into slot j+1, ||y_{j+1}|| reduced; the
+// last CTA forms the preliminary rotation of column j and the status.
+__global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, double* V, size_t ld,
+                                                              const double* __restrict__ w, Small s,
+                                                              Dcgs d, Reducer red, double denom) {
+  __shared__ double sS[512], sT[512];
+  __shared__ double sh[kThreads / 32];
+  const int m = s.m;
+  for (int i = threadIdx.x; i < j; i += blockDim.x) {
+    sS[i] = d.coef[i];
+    sT[i] = d.coef[m + 1 + i];
+  }
+  const double c = d.coef[2 * m + 2], rho = d.coef[2 * m + 3], nu = d.coef[2 * m + 4];
+  const bool ok = d.coef[2 * m + 5] != 0.0;
+  __syncthreads();
+  double* y = V + ld * j;
+  double* yn = V + ld * (j + 1);
+  double2* y2 = reinterpret_cast<double2*>(y);
+  double2* yn2 = reinterpret_cast<double2*>(yn);
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  const int npair = n >> 1;
+  double acc = 0.0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npair; q += gridDim.x * blockDim.x) {
+    const double2 yv = y2[q], wv = w2[q];
+    double ux = ok ? yv.x / nu : 0.0, uy = ok ? yv.y / nu : 0.0;
+    double wx = ok ? wv.x / nu : 0.0, wy = ok ? wv.y / nu : 0.0;
+    constexpr int kU = 16;  // basis rows in flight (software-pipelined)
+    double2 cur[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      cur[u] = u < j ? __ldg(reinterpret_cast<const double2*>(V + ld * u) + q) : make_double2(0.0, 0.0);
+    for (int i0 = 0; i0 < j; i0 += kU) {
+      double2 nxt[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + kU + u;
+        nxt[u] = i < j ? __ldg(reinterpret_cast<const double2*>(V + ld * i) + q) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (i0 + u < j) {
+          ux = fma(-sS[i0 + u], cur[u].x, ux);
+          uy = fma(-sS[i0 + u], cur[u].y, uy);
+          wx = fma(-sT[i0 + u], cur[u].x, wx);
+          wy = fma(-sT[i0 + u], cur[u].y, wy);
+        }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) cur[u] = nxt[u];
+    }
+    const double qx = ux / rho, qy = uy / rho;
+    const double nx = fma(-c, qx, wx) / rho, ny = fma(-c, qy, wy) / rho;
+    y2[q] = make_double2(qx, qy);
+    yn2[q] = make_double2(nx, ny);
+    acc = fma(nx, nx, acc);
+    acc = fma(ny, ny, acc);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: the last row
+    double ul = ok ? y[n - 1] / nu : 0.0, wl = ok ? w[n - 1] / nu : 0.0;
+    for (int i = 0; i < j; ++i) {
+      const double v = V[ld * i + (n - 1)];
+      ul = fma(-sS[i], v, ul);
+      wl = fma(-sT[i], v, wl);
+    }
+    const double ql = ul / rho, nl = fma(-c, ql, wl) / rho;
+    y[n - 1] = ql;
+    yn[n - 1] = nl;
+    acc = fma(nl, nl, acc);
+  }
+  const double bs = block_sum(acc, sh);
+  if (threadIdx.x == 0) red.partials[blockIdx.x] = bs;
+  if (last_block(red)) {
+    __shared__ GivensStage gs;
+    __shared__ double hn_s;
+    finish(red, 1, d.nu + j + 1, 1);
+    if (threadIdx.x == 0) {
+      hn_s = d.nu[j + 1];
+      d.Hraw[static_cast<size_t>(j) * (m + 1) + j + 1] = hn_s;
+    }
+    __syncthreads();
+    // preliminary rotation of column j (the final one follows its
+    // reorthogonalisation in the next sweep 1)
+    stage_givens(gs, s, d.Hraw + static_cast<size_t>(j) * (m + 1), j);
+    if (threadIdx.x == 0) {
+      const double hn = hn_s;
+      double cs, sn;
+      rotate_staged(gs, j, cs, sn);
+      const double gj1 = -sn * s.g[j];
+      s.status[0] = fabs(gj1) / denom;
+      s.status[1] = !(hn >= 1e-14) ? 1.0 : 0.0;
+      s.status[2] = hn;
+    }
+  }
 }
 
 struct Vec {
@@ -469,7 +800,8 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   const bool left = pc && cfg.left, right = pc && !cfg.left;
   GmresResult res;
 
-  Workspace ws(ctx, n, m + 2);
+  const bool dcgs2 = cfg.orth == 2;
+  Workspace ws(ctx, n, 2 * m + 4);
   const int G = ws.grid();
   // basis columns 256-byte aligned (16-byte pair loads in the CGS2 kernels)
   const size_t ld = (static_cast<size_t>(n) + 31) & ~static_cast<size_t>(31);
@@ -487,10 +819,23 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   st.status = st.scal + 16;
   double* hbuf = st.scal + 32;  // scratch for multidot results (<= m+1)
   DevBuf hscratch(sizeof(double) * 2 * (m + 2));
+  // DCGS2 state: raw Hessenberg, sweep-1 sums, sweep-2 coefficients, norms
+  const size_t ldh = static_cast<size_t>(m + 1);
+  DevBuf dstate(dcgs2 ? sizeof(double) * (ldh * m + (2 * m + 4) + (2 * m + 8) + (m + 2)) : 8);
+  Dcgs dc{};
+  if (dcgs2) {
+    dc.Hraw = dstate.as<double>();
+    dc.dots = dc.Hraw + ldh * m;
+    dc.coef = dc.dots + (2 * m + 4);
+    dc.nu = dc.coef + (2 * m + 8);
+    MSCG_CUDA(cudaMemsetAsync(dstate.p, 0, dstate.bytes, s));
+  }
   // MSCG_CGS2_FUSED=0: the four-sweep CGS2 (two multi-dot + multi-axpy pairs)
   const char* fused_env = std::getenv("MSCG_CGS2_FUSED");
   const bool cgs2_fused = !(fused_env && fused_env[0] == '0');
-  const bool dot16 = G >= 4 * ctx->sm_count;
+  // MSCG_DOT16=0|1 forces the group size (tests: both give bit-identical sums)
+  const char* dot16_env = std::getenv("MSCG_DOT16");
+  const bool dot16 = dot16_env ? dot16_env[0] == '1' : G >= 4 * ctx->sm_count;
   // The fused kernel re-reads each thread's basis rows after its axpy: fewer
   // resident rows keep that footprint (rows x (j+1) x 8 B) inside L2.
   const char* cps_env = std::getenv("MSCG_AXPYDOT_CPS");
@@ -562,9 +907,17 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
       res.converged = last_true <= cfg.rel_tol;
       break;
     }
-    scale_div_kernel<<<G, kThreads, 0, s>>>(n, vbase, st.scal + 1, vbase);
-    init_cycle_kernel<<<1, 128, 0, s>>>(st, st.scal + 1);
-    ctx->launches += 2;
+    if (dcgs2) {
+      // slot 0 keeps r unnormalised (y_0, nu_0 = beta): q_0 = r / beta is
+      // formed by the first iteration's sweep 2
+      init_cycle_kernel<<<1, 128, 0, s>>>(st, st.scal + 1, dc.nu);
+      ctx->launches += 1;
+      MSCG_CUDA(cudaMemsetAsync(dc.Hraw, 0, sizeof(double) * ldh * m, s));
+    } else {
+      scale_div_kernel<<<G, kThreads, 0, s>>>(n, vbase, st.scal + 1, vbase);
+      init_cycle_kernel<<<1, 128, 0, s>>>(st, st.scal + 1, nullptr);
+      ctx->launches += 2;
+    }
 
     int mm = 0;
     bool breakdown = false, inner_conv = false;
@@ -577,6 +930,17 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
       double* wp = w.as<double>();
       apply_op(vj, wp);
       double* Hc = st.H + static_cast<size_t>(j) * (m + 1);
+      if (dcgs2) {
+        // two basis sweeps; the status comes from sweep 2's last CTA
+        (dot16 ? dcgs2_dot_kernel<16> : dcgs2_dot_kernel<8>)<<<G, kThreads, 0, s>>>(
+            n, j, vbase, ld, wp, ws.red, st, dc, 0);
+        dcgs2_axpy_kernel<<<G, kThreads, 0, s>>>(n, j, vbase, ld, wp, st, dc, ws.red, denom);
+        ctx->launches += 2;
+        MSCG_CUDA(cudaMemcpyAsync(hstat + 4 * (j & 1), st.status, 3 * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+        MSCG_CUDA(cudaEventRecord(hev[j & 1], s));
+        return;
+      }
       if (cfg.orth == 0) {
         // MGS: for i <= j: h_ij = v_i . w ; w -= h_ij v_i (fused pairwise).
         for (int i = 0; i <= j; ++i) {
@@ -631,6 +995,13 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
         inner_conv = rel <= cfg.rel_tol;
         break;
       }
+    }
+    if (dcgs2 && mm > 0 && mm >= jmax) {
+      // no speculative iteration in the stream: finalise column mm-1 with
+      // one dot sweep of y_mm against q_0..q_{mm-1}
+      (dot16 ? dcgs2_dot_kernel<16> : dcgs2_dot_kernel<8>)<<<G, kThreads, 0, s>>>(
+          n, mm, vbase, ld, nullptr, ws.red, st, dc, 1);
+      ctx->launches++;
     }
     backsolve_kernel<<<1, 32, 0, s>>>(st, mm);
     double* z = w.as<double>();

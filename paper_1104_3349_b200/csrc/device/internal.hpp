@@ -311,6 +311,11 @@ struct Precond {
   // chunk's rows are multiplied as soon as that chunk of x (and the
   // interface part, copied first) has arrived, and leave while later
   // chunks are still in flight.  d_x, d_y: device scratch of n doubles.
+  // When the interior ranges are coupled (entries of C[0:p, 0:p] outside
+  // their block: PartitionedMatrix::from_split accepts such splits and the
+  // preconditioner keeps only the diagonal blocks) the whole x is copied
+  // before any row is multiplied.
+  bool d_coupled = false;
   void spmv_host(const double* x_host, double* y_host, double* d_x, double* d_y,
                  cudaStream_t s);
   ~Precond();
@@ -336,7 +341,9 @@ struct Precond {
 };
 
 // Build the whole preconditioner (block_begin = 0, block_end = -1) or the
-// shard owning interior blocks [block_begin, block_end).
+// shard owning interior blocks [block_begin, block_end).  schur_single: S^
+// is an overlapped band, factored whole by one exact LU (the reference's
+// schur_single_, preconditioner.cpp:58-67; s_ranges unused).
 std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
                                        const int* c_ci, const double* c_v,
                                        const std::vector<std::pair<int, int>>& d_ranges,
@@ -344,15 +351,19 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
                                        const double* s_v,
                                        const std::vector<std::pair<int, int>>& s_ranges,
                                        double tol_a, int s_a, int block_begin = 0,
-                                       int block_end = -1);
+                                       int block_end = -1, bool schur_single = false);
 
 // build_msc for numbering aggregates (ranges over the interface numbering)
 // on the device: S^ returned as a host CSR (n_g x n_g, block diagonal),
 // bit-identical to the reference.  Throws Error(SINGULAR) naming the first
 // aggregate whose D block is singular.
 constexpr int kMscMscn = 0, kMscMscnr = 1, kMscLum = 2;
+// ranges: owned ranges; spans: each aggregate's working range (= ranges,
+// or extended into the next aggregate for the overlapped variants, whose
+// banded S^ is merged on the host in the reference's order).
 void build_msc_device(Ctx* ctx, int n, int p, const int* c_rp, const int* c_ci, const double* c_v,
-                      const std::vector<std::pair<int, int>>& ranges, int variant,
+                      const std::vector<std::pair<int, int>>& ranges,
+                      const std::vector<std::pair<int, int>>& spans, int variant,
                       std::vector<int>& s_rp, std::vector<int>& s_ci, std::vector<double>& s_v);
 
 // generate_oseen's assembly + scale_rows on the device (one thread per row,
@@ -373,7 +384,7 @@ struct GmresConfig {
   int restart = 300, max_iters = 3000;
   double rel_tol = 1e-9;
   bool left = false;
-  int orth = 1;
+  int orth = 2;  // 0 MGS, 1 CGS2, 2 DCGS2
 };
 struct GmresResult {
   int iterations = 0;

@@ -59,12 +59,16 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
                                        const std::vector<std::pair<int, int>>& d_ranges,
                                        const int* s_rp, const int* s_ci,
                                        const double* s_v,
-                                       const std::vector<std::pair<int, int>>& s_ranges,
+                                       const std::vector<std::pair<int, int>>& s_ranges_in,
                                        double tol_a, int s_a, int block_begin,
-                                       int block_end) {
+                                       int block_end, bool schur_single) {
   if (p < 0 || p > n) throw Error(1, "build_preconditioner: split out of range");
   if (d_ranges.empty()) throw Error(1, "build_preconditioner: no interior D blocks");
   const int ng = n - p;
+  const std::vector<std::pair<int, int>> s_ranges =
+      schur_single ? std::vector<std::pair<int, int>>{{0, ng}} : s_ranges_in;
+  if (schur_single && ng < 1)
+    throw Error(1, "build_preconditioner: Schur approximation does not match the split");
   {
     int cov = 0;
     for (auto [b, e] : d_ranges) {
@@ -98,6 +102,17 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
     std::vector<int> rp, ci;
     std::vector<double> v;
     if (!sharded) {
+      // interior rows reading another interior block's columns (a coupled
+      // user split): host-buffer matvecs must not overlap per chunk
+      for (auto [b, e] : d_ranges) {
+        for (int i = b; i < e && !pc->d_coupled; ++i)
+          for (int k = c_rp[i]; k < c_rp[i + 1]; ++k)
+            if (c_ci[k] < p && (c_ci[k] < b || c_ci[k] >= e)) {
+              pc->d_coupled = true;
+              break;
+            }
+        if (pc->d_coupled) break;
+      }
       pc->C = upload_csr(ctx, n, n, c_rp, c_ci, c_v);
       extract(c_rp, c_ci, c_v, 0, p, p, n, e_rp, e_ci, e_v);  // E = C[0:p, p:n]
       pc->E = upload_csr(ctx, p, ng, e_rp.data(), e_ci.data(), e_v.data());
@@ -141,8 +156,20 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
       blocks.push_back({b, e - b, b});
       exact.push_back(1);
     }
-    pc->S = factor_blocks(ctx, sm.rp.as<int>(), sm.ci.as<int>(), sm.v.as<double>(), blocks, exact,
-                          0.0, "build_preconditioner: Schur block", &pc->times);
+    if (!schur_single) {
+      pc->S = factor_blocks(ctx, sm.rp.as<int>(), sm.ci.as<int>(), sm.v.as<double>(), blocks,
+                            exact, 0.0, "build_preconditioner: Schur block", &pc->times);
+    } else {
+      // the overlapped band: one exact LU of the whole S^ (:58-67)
+      try {
+        pc->S = factor_blocks(ctx, sm.rp.as<int>(), sm.ci.as<int>(), sm.v.as<double>(), blocks,
+                              exact, 0.0, "", &pc->times);
+      } catch (const Error& e) {
+        if (e.code != 2) throw;
+        throw Error(2, std::string("build_preconditioner: overlapped Schur band: ") + e.what(),
+                    -1, e.pivot);
+      }
+    }
   }
   pc->stored_nnz = pc->E->nnz + pc->F->nnz + pc->D->nnz_l() + pc->D->nnz_u() + (hi - lo);
   if (pc->S) pc->stored_nnz += pc->S->nnz_l() + pc->S->nnz_u() + ng;
@@ -255,6 +282,12 @@ void Precond::chunk_rows(int c, int& lo, int& hi) const {
 void Precond::spmv_host(const double* x_h, double* y_h, double* d_x, double* d_y,
                         cudaStream_t s) {
   if (shard.on || !C) throw Error(1, "matvec: this preconditioner holds no full C");
+  if (d_coupled) {
+    MSCG_CUDA(cudaMemcpyAsync(d_x, x_h, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    spmv(*C, d_x, d_y, nullptr, 0, s);
+    MSCG_CUDA(cudaMemcpyAsync(y_h, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    return;
+  }
   ensure_side_streams();
   const int ng = n - p;
   cudaEvent_t ev_if = ev_mid;

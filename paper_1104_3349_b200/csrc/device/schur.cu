@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "internal.hpp"
+#include "host/setup.hpp"
 
 namespace mscg {
 
@@ -32,16 +33,19 @@ __global__ void __launch_bounds__(kMscThreads) msc_block_kernel(
     int p, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ cv,
     const int* __restrict__ ranges, int variant, const long long* __restrict__ soff,
     double* __restrict__ scratch, int* __restrict__ perm_all, unsigned long long* err,
-    int* __restrict__ row_nnz) {
+    int* __restrict__ row_nnz, const int* __restrict__ roff) {
   const int agg = blockIdx.x;
   const int sb = ranges[2 * agg], se = ranges[2 * agg + 1], m = se - sb;
+  // per-aggregate row storage (perm, row counts): spans of overlapped
+  // aggregates share rows, so each aggregate has its own slice
+  const int r0 = roff[agg];
   const long long mm = static_cast<long long>(m) * m;
   const bool lum = variant == kMscLum;
   double* S = scratch + soff[agg];
   double* A = S + mm;   // D_ii, then its LU
   double* B = A + mm;   // right-hand sides (E_ii or diag(E_ii 1))
   double* X = B + mm;   // D_ii^-1 B
-  int* perm = perm_all + sb;
+  int* perm = perm_all + r0;
   const int tid = threadIdx.x;
   __shared__ double red_v[kMscThreads / 32];
   __shared__ int red_i[kMscThreads / 32];
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(kMscThreads) msc_block_kernel(
   for (int r = tid; r < m; r += blockDim.x) {
     int cnt = 0;
     for (int c = 0; c < m; ++c) cnt += S[static_cast<long long>(r) * m + c] != 0.0;
-    row_nnz[sb + r] = cnt;
+    row_nnz[r0 + r] = cnt;
   }
 }
 
@@ -218,24 +222,31 @@ __global__ void __launch_bounds__(kMscThreads) msc_fill_kernel(
 }  // namespace
 
 void build_msc_device(Ctx* ctx, int n, int p, const int* c_rp, const int* c_ci, const double* c_v,
-                      const std::vector<std::pair<int, int>>& ranges, int variant,
+                      const std::vector<std::pair<int, int>>& ranges,
+                      const std::vector<std::pair<int, int>>& spans, int variant,
                       std::vector<int>& s_rp, std::vector<int>& s_ci, std::vector<double>& s_v) {
   cudaStream_t s = ctx->stream;
   const int k = static_cast<int>(ranges.size());
   const int ng = n - p;
+  const bool overlapped = spans != ranges;
   s_rp.assign(ng + 1, 0);
   s_ci.clear();
   s_v.clear();
   if (k == 0) return;
   const int64_t nnz = c_rp[n];
-  std::vector<int> hr(2 * k);
+  // each CTA works on its aggregate's span (= its owned range unless the
+  // aggregates overlap)
+  std::vector<int> hr(2 * k), hro(k + 1, 0);
   std::vector<long long> hoff(k + 1, 0);
   for (int i = 0; i < k; ++i) {
-    hr[2 * i] = ranges[i].first;
-    hr[2 * i + 1] = ranges[i].second;
-    const long long m = ranges[i].second - ranges[i].first;
+    hr[2 * i] = spans[i].first;
+    hr[2 * i + 1] = spans[i].second;
+    const long long m = spans[i].second - spans[i].first;
     hoff[i + 1] = hoff[i] + (variant == kMscLum ? 1 : 4) * m * m;
+    hro[i + 1] = hro[i] + static_cast<int>(m);
   }
+  if (!overlapped)
+    for (int i = 0; i < k; ++i) hro[i] = ranges[i].first;  // = the running sum
   DevBuf d_rp(sizeof(int) * (n + 1)), d_ci(sizeof(int) * std::max<int64_t>(1, nnz)),
       d_v(sizeof(double) * std::max<int64_t>(1, nnz));
   MSCG_CUDA(cudaMemcpyAsync(d_rp.p, c_rp, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
@@ -243,31 +254,55 @@ void build_msc_device(Ctx* ctx, int n, int p, const int* c_rp, const int* c_ci, 
     MSCG_CUDA(cudaMemcpyAsync(d_ci.p, c_ci, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
     MSCG_CUDA(cudaMemcpyAsync(d_v.p, c_v, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
   }
-  DevBuf d_r(sizeof(int) * hr.size()), d_off(sizeof(long long) * hoff.size());
+  DevBuf d_r(sizeof(int) * hr.size()), d_off(sizeof(long long) * hoff.size()),
+      d_ro(sizeof(int) * hro.size());
   MSCG_CUDA(cudaMemcpyAsync(d_r.p, hr.data(), sizeof(int) * hr.size(), cudaMemcpyHostToDevice, s));
   MSCG_CUDA(cudaMemcpyAsync(d_off.p, hoff.data(), sizeof(long long) * hoff.size(),
                             cudaMemcpyHostToDevice, s));
+  MSCG_CUDA(cudaMemcpyAsync(d_ro.p, hro.data(), sizeof(int) * hro.size(), cudaMemcpyHostToDevice, s));
+  const int rows_total = std::max(ng, hro[k]);
   DevBuf scratch(sizeof(double) * std::max<long long>(1, hoff[k]));
-  DevBuf perm(sizeof(int) * std::max(1, ng)), nnzr(sizeof(int) * std::max(1, ng));
+  DevBuf perm(sizeof(int) * std::max(1, rows_total)), nnzr(sizeof(int) * std::max(1, rows_total));
   DevBuf err(sizeof(unsigned long long));
   const unsigned long long none = ~0ull;
   MSCG_CUDA(cudaMemcpyAsync(err.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
   msc_block_kernel<<<k, kMscThreads, 0, s>>>(p, d_rp.as<int>(), d_ci.as<int>(), d_v.as<double>(),
                                              d_r.as<int>(), variant, d_off.as<long long>(),
                                              scratch.as<double>(), perm.as<int>(),
-                                             err.as<unsigned long long>(), nnzr.as<int>());
+                                             err.as<unsigned long long>(), nnzr.as<int>(),
+                                             d_ro.as<int>());
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
   unsigned long long herr = none;
   std::vector<int> hn(ng);
   MSCG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost, s));
-  if (ng) MSCG_CUDA(cudaMemcpyAsync(hn.data(), nnzr.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, s));
+  if (ng && !overlapped)
+    MSCG_CUDA(cudaMemcpyAsync(hn.data(), nnzr.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, s));
   MSCG_CUDA(cudaStreamSynchronize(s));
   if (herr != none) {
     const int agg = static_cast<int>(herr >> 32), piv = static_cast<int>(herr & 0xffffffffu);
     throw Error(2, "build_msc: singular D block of aggregate " + std::to_string(agg) +
                        " (dense_lu: zero pivot at index " + std::to_string(piv) + ")",
                 -1, piv);
+  }
+  if (overlapped) {
+    // banded S^: the local blocks come back and are merged in the
+    // reference's order (owned columns over whole spans, host::merge_msc)
+    std::vector<std::vector<double>> loc(k);
+    std::vector<const double*> lp(k);
+    for (int i = 0; i < k; ++i) {
+      const size_t m = spans[i].second - spans[i].first;
+      loc[i].resize(m * m);
+      MSCG_CUDA(cudaMemcpyAsync(loc[i].data(), scratch.as<double>() + hoff[i], sizeof(double) * m * m,
+                                cudaMemcpyDeviceToHost, s));
+      lp[i] = loc[i].data();
+    }
+    MSCG_CUDA(cudaStreamSynchronize(s));
+    host::Csr out = host::merge_msc(ng, ranges, spans, lp);
+    s_rp = std::move(out.rp);
+    s_ci = std::move(out.ci);
+    s_v = std::move(out.v);
+    return;
   }
   for (int r = 0; r < ng; ++r) s_rp[r + 1] = s_rp[r] + hn[r];
   const int snnz = s_rp[ng];

@@ -61,7 +61,123 @@ Variant variant_from_name(const std::string& name) {
   if (name == "mscn") return Variant::Mscn;
   if (name == "mscnr") return Variant::Mscnr;
   if (name == "lum") return Variant::Lum;
+  if (name == "omscn") return Variant::Omscn;
+  if (name == "omscnr") return Variant::Omscnr;
+  if (name == "olum") return Variant::Olum;
   throw std::invalid_argument("unknown or unsupported MSC variant: " + name);
+}
+
+bool variant_overlapped(Variant v) {
+  return v == Variant::Omscn || v == Variant::Omscnr || v == Variant::Olum;
+}
+bool variant_rowsum(Variant v) { return v == Variant::Mscnr || v == Variant::Omscnr; }
+bool variant_lumped(Variant v) { return v == Variant::Lum || v == Variant::Olum; }
+
+static const char* variant_str(Variant v) {
+  switch (v) {
+    case Variant::Mscn: return "mscn";
+    case Variant::Mscnr: return "mscnr";
+    case Variant::Lum: return "lum";
+    case Variant::Omscn: return "omscn";
+    case Variant::Omscnr: return "omscnr";
+    case Variant::Olum: return "olum";
+  }
+  return "?";
+}
+
+std::vector<int> overlap_widths(int n_g, const std::vector<int>& sizes, int sz, int overlap) {
+  std::vector<int> w(sizes.size(), overlap < 0 ? sz : overlap);
+  if (!w.empty()) w.back() = 0;
+  int end = 0;
+  for (size_t i = 0; i < w.size(); ++i) {
+    end += sizes[i];
+    int bound = std::min(sizes[i] - 1, n_g - end);
+    if (i + 1 == w.size()) bound = 0;
+    w[i] = std::min(w[i], bound);
+  }
+  return w;
+}
+
+void aggregate_spans(const Partitioned& pm, const std::vector<int>& sizes, Variant v,
+                     const std::vector<int>& widths, std::vector<std::pair<int, int>>& ranges,
+                     std::vector<std::pair<int, int>>& spans) {
+  const int ng = pm.n_g(), p = pm.p;
+  int total = 0;
+  for (int s : sizes) {
+    if (s < 1) throw std::invalid_argument("aggregates: sizes must be >= 1");
+    total += s;
+  }
+  if (sizes.empty() || total != ng)
+    throw std::invalid_argument("aggregates: sizes sum to " + std::to_string(total) +
+                                ", expected " + std::to_string(ng));
+  ranges.clear();
+  spans.clear();
+  int b = 0;
+  for (int s : sizes) {
+    ranges.push_back({b, b + s});
+    b += s;
+  }
+  const int k = static_cast<int>(sizes.size());
+  const bool have = !widths.empty();
+  if (have) {  // aggregate_overlapped (aggregates.cpp:50-85)
+    if (static_cast<int>(widths.size()) != k)
+      throw std::invalid_argument("aggregate_overlapped: one width per aggregate");
+    for (int i = 0; i < k; ++i) {
+      const int w = widths[i];
+      if (w < 0 || (i + 1 == k && w != 0))
+        throw std::invalid_argument("aggregate_overlapped: widths must be >= 0 and end with 0");
+      if (w >= sizes[i])
+        throw std::invalid_argument("aggregate_overlapped: width " + std::to_string(w) +
+                                    " of aggregate " + std::to_string(i) + " violates w < size");
+      if (ranges[i].second + w > ng)
+        throw std::invalid_argument("aggregate_overlapped: overlapped span of aggregate " +
+                                    std::to_string(i) + " exceeds the block");
+    }
+  }
+  // check_agg_compatible (schur_approx.cpp:56-85)
+  const bool want = variant_overlapped(v);
+  if (want != have)
+    throw std::invalid_argument(std::string("build_msc: variant ") + variant_str(v) +
+                                (want ? " needs an overlapped aggregate set"
+                                      : " needs a non-overlapped aggregate set"));
+  for (int i = 0; i < k; ++i) spans.push_back({ranges[i].first, ranges[i].second + (have ? widths[i] : 0)});
+  if (!variant_lumped(v)) {
+    for (int i = 0; i < k; ++i)
+      if (spans[i].second > p)
+        throw std::invalid_argument("build_msc: aggregate " + std::to_string(i) +
+                                    " has a D-side index outside the (1,1) block");
+  }
+}
+
+Csr merge_msc(int ng, const std::vector<std::pair<int, int>>& ranges,
+              const std::vector<std::pair<int, int>>& spans,
+              const std::vector<const double*>& local) {
+  // Row r collects, for every aggregate whose span holds r (a contiguous
+  // run of aggregates ending at r's owner), that aggregate's owned columns
+  // in ascending order: the row-major order from_triplets sorts into.
+  Csr s(ng, ng);
+  const int k = static_cast<int>(ranges.size());
+  int own = 0;
+  for (int r = 0; r < ng; ++r) {
+    while (own + 1 < k && ranges[own].second <= r) ++own;
+    int first = own;
+    while (first > 0 && spans[first - 1].second > r) --first;
+    for (int i = first; i <= own; ++i) {
+      const auto [sb, se] = spans[i];
+      if (r < sb || r >= se) continue;
+      const int m = se - sb;
+      const double* a = local[i];
+      for (int c = ranges[i].first; c < ranges[i].second; ++c) {
+        const double v = a[static_cast<size_t>(r - sb) * m + (c - sb)];
+        if (v != 0.0) {
+          s.ci.push_back(c);
+          s.v.push_back(v);
+        }
+      }
+    }
+    s.rp[r + 1] = static_cast<int>(s.ci.size());
+  }
+  return s;
 }
 
 namespace {
@@ -161,29 +277,12 @@ Dense solve(const LuFactors& f, const Dense& b) {
 }  // namespace
 
 SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes, Variant v,
-                      int threads) {
+                      int threads, const std::vector<int>& widths) {
   const int ng = pm.n_g(), p = pm.p;
-  int total = 0;
-  for (int s : sizes) {
-    if (s < 1) throw std::invalid_argument("aggregates: sizes must be >= 1");
-    total += s;
-  }
-  if (sizes.empty() || total != ng)
-    throw std::invalid_argument("aggregates: sizes sum to " + std::to_string(total) +
-                                ", expected " + std::to_string(ng));
   SchurApprox out;
-  int b = 0;
-  for (int s : sizes) {
-    out.ranges.push_back({b, b + s});
-    b += s;
-  }
+  aggregate_spans(pm, sizes, v, widths, out.ranges, out.spans);
+  out.overlapped = variant_overlapped(v);
   const int k = static_cast<int>(sizes.size());
-  if (v != Variant::Lum) {
-    for (int i = 0; i < k; ++i)
-      if (out.ranges[i].second > p)
-        throw std::invalid_argument("build_msc: aggregate " + std::to_string(i) +
-                                    " has a D-side index outside the (1,1) block");
-  }
   std::vector<Dense> local(k);
   if (threads <= 0) threads = hardware_threads();
   std::atomic<int> next{0};
@@ -193,15 +292,15 @@ SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes, Vari
   auto work = [&] {
     for (int i = next++; i < k; i = next++) {
       try {
-        const auto [sb, se] = out.ranges[i];
+        const auto [sb, se] = out.spans[i];
         const int m = se - sb;
         // G = C[p:, p:]; D = C[:p, :p]; E = C[:p, p:]; F = C[p:, :p].
         Dense s = dense_range(pm.C, p + sb, p + se, p + sb, p + se);
-        if (v != Variant::Lum) {
+        if (!variant_lumped(v)) {
           LuFactors dlu = factor_exact(dense_range(pm.C, sb, se, sb, se), i);
           Dense e = dense_range(pm.C, sb, se, p + sb, p + se);
           Dense rhs;
-          if (v == Variant::Mscnr) {
+          if (variant_rowsum(v)) {
             // E_ii compressed to diag(E_ii * 1) (schur_approx.cpp:112-126).
             rhs = Dense(m, m);
             for (int r = 0; r < m; ++r) {
@@ -248,23 +347,10 @@ SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes, Vari
   }
   if (err) std::rethrow_exception(err);
 
-  // Sequential merge (schur_approx.cpp:141-160): block diagonal, each row
-  // holds the nonzeros of its own aggregate in column order.
-  Csr& s = out.s_hat;
-  s = Csr(ng, ng);
-  for (int i = 0; i < k; ++i) {
-    const auto [sb, se] = out.ranges[i];
-    for (int r = sb; r < se; ++r) {
-      for (int c = sb; c < se; ++c) {
-        const double val = local[i](r - sb, c - sb);
-        if (val != 0.0) {
-          s.ci.push_back(c);
-          s.v.push_back(val);
-        }
-      }
-      s.rp[r + 1] = static_cast<int>(s.ci.size());
-    }
-  }
+  // Sequential merge (schur_approx.cpp:141-160).
+  std::vector<const double*> lp(k);
+  for (int i = 0; i < k; ++i) lp[i] = local[i].a.data();
+  out.s_hat = merge_msc(ng, out.ranges, out.spans, lp);
   return out;
 }
 

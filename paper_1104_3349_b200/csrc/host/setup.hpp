@@ -60,18 +60,44 @@ void anchor_interface(Partitioned& pm);
 std::vector<int> equal_sizes(int n_g, int sz);
 std::vector<int> anchored_sizes(const Partitioned& pm, int sz);
 
-enum class Variant { Mscn, Mscnr, Lum };
+// MSC variants over numbering aggregates (schur_approx.cpp:11-52); the
+// overlapped ones (O*) extend every aggregate's span by a width into the
+// next (aggregate_overlapped, aggregates.cpp:50-85).
+enum class Variant { Mscn, Mscnr, Lum, Omscn, Omscnr, Olum };
 Variant variant_from_name(const std::string& name);
+bool variant_overlapped(Variant v);
+bool variant_rowsum(Variant v);
+bool variant_lumped(Variant v);
 
-// build_msc for the non-overlapped numbering variants
-// (proj/src/schur_approx.cpp:88-161): S^ as a block-diagonal CSR over the
-// aggregate ranges.
+// Overlap widths as benchmark.cpp:74-88 makes them: `overlap` for every
+// aggregate (< 0: sz), the last 0, clipped to min(size - 1, n_g - end)
+// (clip_overlap_widths, aggregates.cpp:143-156).
+std::vector<int> overlap_widths(int n_g, const std::vector<int>& sizes, int sz, int overlap);
+
+// build_msc (proj/src/schur_approx.cpp:88-161) over numbering aggregates:
+// owned ranges from `sizes`, spans extended by `widths` (empty: none; the
+// overlapped variants need them, aggregate_overlapped's checks apply).
+// Each aggregate's dense S_ii lives on its span; the merge writes every
+// owned column over its aggregate's whole span, so overlapped aggregates
+// give a banded S^ (block diagonal otherwise).
 struct SchurApprox {
   Csr s_hat;
-  std::vector<std::pair<int, int>> ranges;
+  std::vector<std::pair<int, int>> ranges;  // owned ranges
+  std::vector<std::pair<int, int>> spans;   // = ranges unless overlapped
+  bool overlapped = false;
 };
 SchurApprox build_msc(const Partitioned& pm, const std::vector<int>& sizes,
-                      Variant v, int threads = 0);
+                      Variant v, int threads = 0, const std::vector<int>& widths = {});
+// The aggregate checks of aggregate_overlapped / check_agg_compatible
+// (aggregates.cpp:50-85, schur_approx.cpp:56-85): owned ranges and spans.
+void aggregate_spans(const Partitioned& pm, const std::vector<int>& sizes, Variant v,
+                     const std::vector<int>& widths, std::vector<std::pair<int, int>>& ranges,
+                     std::vector<std::pair<int, int>>& spans);
+// The sequential merge (schur_approx.cpp:141-160) of per-aggregate dense
+// blocks local[i] (span x span, row-major) into S^.
+Csr merge_msc(int n_g, const std::vector<std::pair<int, int>>& ranges,
+              const std::vector<std::pair<int, int>>& spans,
+              const std::vector<const double*>& local);
 
 int hardware_threads();
 

@@ -449,13 +449,24 @@ class Problem:
         return None if not p else np.ctypeslib.as_array(p, (self.n,)).copy()
 
     def build_msc(self, variant="lum", sz=0, mode="equal", sizes=None, threads=0,
-                  ctx: "Context | None" = None):
+                  ctx: "Context | None" = None, overlap=-1, widths=None):
         """build_msc (schur_approx.cpp:88-161) over numbering aggregates; on the
-        host (threads) or, with ctx, on the device — S^ bit-identical either way."""
+        host (threads) or, with ctx, on the device — S^ bit-identical either way.
+        Overlapped variants ("omscn", "omscnr", "olum"): aggregate_overlapped
+        (aggregates.cpp:50-85) with `widths`, or `overlap` per aggregate
+        (< 0: sz; last 0; clipped as benchmark.cpp:74-88 does); the
+        preconditioner then factors the banded S^ whole."""
         m = {"equal": 0, "anchored": 1, "explicit": 2}[mode]
         s = np.ascontiguousarray(sizes if sizes is not None else [0], np.int32)
         st = api.Status()
-        if ctx is not None:
+        if variant.startswith("o") or widths is not None:
+            w = None if widths is None else np.ascontiguousarray(widths, np.int32)
+            _check(api.lib().mscg_problem_build_schur_overlapped(
+                ctx.h if ctx is not None else None, self.h, variant.encode(), m, sz, len(s),
+                _ptr(s), int(overlap), 0 if w is None else len(w),
+                _ptr(w) if w is not None else None, threads,
+                C.byref(st)), st)
+        elif ctx is not None:
             _check(api.lib().mscg_problem_build_schur_device(
                 ctx.h, self.h, variant.encode(), m, sz, len(s), _ptr(s), C.byref(st)), st)
         else:
@@ -588,17 +599,23 @@ def build_preconditioner_shard(problem: Problem, block_begin: int, block_end: in
 def build_preconditioner_arrays(ctx: Context, c: SparseMatrix, p: int, d_ranges,
                                 s_hat: SparseMatrix, s_ranges, tolA=1e-4, sA=400,
                                 kind="msc") -> MscPreconditioner:
+    """s_ranges None: S^ is an overlapped band, factored whole (one exact LU,
+    the reference's schur_single_)."""
     rp, ci, v = c.arrays()
     srp, sci, sv = s_hat.arrays()
     dr = np.ascontiguousarray(np.asarray(d_ranges, np.int32).reshape(-1))
-    sr = np.ascontiguousarray(np.asarray(s_ranges, np.int32).reshape(-1))
+    single = s_ranges is None
+    sr = np.ascontiguousarray(np.asarray([0, 0] if single else s_ranges, np.int32).reshape(-1))
     h = C.c_void_p()
     st = api.Status()
     _check(api.lib().mscg_precond_build(ctx.h, c.nrows, p, _ptr(rp), _ptr(ci), _ptr(v),
                                         len(dr) // 2, _ptr(dr), _ptr(srp), _ptr(sci), _ptr(sv),
-                                        len(sr) // 2, _ptr(sr), tolA, sA, C.byref(h),
-                                        C.byref(st)), st)
+                                        -1 if single else len(sr) // 2, _ptr(sr), tolA, sA,
+                                        C.byref(h), C.byref(st)), st)
     return MscPreconditioner(ctx, h, kind, sA)
+
+
+_ORTH = {"mgs": 0, "cgs2": 1, "dcgs2": 2}
 
 
 @dataclass
@@ -607,7 +624,7 @@ class SolverConfig:
     max_iters: int = 3000
     rel_tol: float = 1e-9
     side: str = "right"
-    orth: str = "cgs2"   # "cgs2" (fused multi-dot) or "mgs" (reference order)
+    orth: str = "dcgs2"  # "dcgs2" (two basis sweeps), "cgs2" (three) or "mgs" (reference order)
 
 
 @dataclass
@@ -635,7 +652,7 @@ def gmres(a: DeviceMatrix, b_precond: MscPreconditioner | None, rhs, cfg: Solver
         x = np.empty(n)
         px = _ptr(x)
     c = api.GmresConfig(cfg.restart, cfg.max_iters, cfg.rel_tol,
-                        1 if cfg.side == "left" else 0, 0 if cfg.orth == "mgs" else 1)
+                        1 if cfg.side == "left" else 0, _ORTH[cfg.orth])
     rep = api.GmresReport()
     cap = cfg.max_iters + 64
     hist = np.empty(cap)

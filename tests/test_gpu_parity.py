@@ -117,7 +117,7 @@ def test_apply_device_tensor(cfg1_pc, cfg1_oracle, ref, cfg1):
     assert rel_err(x.cpu().numpy(), cfg1_oracle.apply(y)) <= APPLY_TOL
 
 
-@pytest.mark.parametrize("orth", ["cgs2", "mgs"])
+@pytest.mark.parametrize("orth", ["dcgs2", "cgs2", "mgs"])
 def test_gmres_cfg1_iterations(msc, cfg1_pc, cfg1_oracle, cfg1, ref, rs, orth):
     b = ref.random_vector(cfg1.n, 0)
     want = rs.gmres(csr_tuple(cfg1.C), b, 30, 3000, 1e-8, msc=cfg1_oracle)
@@ -162,6 +162,61 @@ def test_gmres_cgs2_fused_matches_four_sweeps(msc, ctx, n, restart, monkeypatch)
     assert np.allclose(h1, h0, rtol=1e-9, atol=1e-15)
     assert rel_err(x1, x0) < 1e-9
     assert np.linalg.norm(b - a @ x1) / np.linalg.norm(b) <= 1e-10
+
+
+def _banded_system(msc, ctx, n, seed):
+    """Sparse nonsymmetric test operator (CSR built directly, any n)."""
+    rng = np.random.default_rng(seed)
+    idx = np.arange(n)
+    rows = np.concatenate([idx, idx, idx])
+    cols = np.concatenate([idx, (idx + 1) % n, (idx + 7) % n])
+    vals = np.concatenate([1.2 + rng.uniform(0, 1, n), np.full(n, -0.9), rng.uniform(-0.5, 0.5, n)])
+    o = np.lexsort((cols, rows))
+    rows, cols, vals = rows[o], cols[o], vals[o]
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    S = msc.SparseMatrix(n, n, np.cumsum(rp).astype(np.int32), cols.astype(np.int32), vals)
+    return S, msc.DeviceMatrix(ctx, S), rng.uniform(-1, 1, n)
+
+
+@pytest.mark.parametrize("n,restart", [(4099, 70), (3000, 33), (257, 5), (160001, 40)])
+def test_gmres_dcgs2_matches_cgs2(msc, ctx, n, restart, monkeypatch):
+    """DCGS2 (two basis sweeps, delayed reorthogonalisation) against CGS2
+    (three sweeps): same projections, regrouped arithmetic, so the residual
+    histories agree to 1e-9 relative and the iteration counts match; odd and
+    even lengths, restarts, several groups of basis vectors, and a long
+    vector (n = 160001) where the 16-vector dot groups are chosen."""
+    S, A, b = _banded_system(msc, ctx, n, n)
+    out = {}
+    for orth in ("cgs2", "dcgs2"):
+        cfg = msc.SolverConfig(restart=restart, max_iters=400, rel_tol=1e-10, orth=orth)
+        out[orth] = msc.gmres(A, None, b, cfg)
+    (x0, r0), (x1, r1) = out["cgs2"], out["dcgs2"]
+    assert r0.converged and r1.converged
+    assert r1.iterations == r0.iterations and r1.iterations > restart // 2
+    h0, h1 = np.asarray(r0.residual_history), np.asarray(r1.residual_history)
+    assert np.allclose(h1, h0, rtol=1e-9, atol=1e-15)
+    assert rel_err(x1, x0) < 1e-9
+    ax = np.zeros(n)
+    rows = np.repeat(np.arange(n), np.diff(S.row_offsets))
+    np.add.at(ax, rows, S.values * x1[S.col_indices])
+    assert np.linalg.norm(b - ax) / np.linalg.norm(b) <= 1e-10
+
+
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_gmres_dot_groups_bit_identical(msc, ctx, orth, monkeypatch):
+    """Basis dots in groups of 8 or 16 vectors (MSCG_DOT16) keep every
+    per-vector summation order: identical residual histories, bit for bit."""
+    S, A, b = _banded_system(msc, ctx, 160001, 7)
+    cfg = msc.SolverConfig(restart=40, max_iters=120, rel_tol=1e-10, orth=orth)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("MSCG_DOT16", mode)
+        out[mode] = msc.gmres(A, None, b, cfg)
+    (x0, r0), (x1, r1) = out["0"], out["1"]
+    assert r0.iterations == r1.iterations
+    assert same_bits(np.asarray(r0.residual_history), np.asarray(r1.residual_history))
+    assert same_bits(x0, x1)
 
 
 def test_gmres_unpreconditioned_identity(msc, ctx, ref):
@@ -620,3 +675,104 @@ def test_full_scale_apply_parity(msc, ctx, ref, grid, nu, n_a, sample):
         want = R.solve(y[r0:r1]) - R.solve(w)
         for mode in ("on", "off"):
             assert rel_err(xs[mode][r0:r1], want) <= APPLY_TOL, (b, mode)
+
+
+def test_host_buffer_spmv_coupled_split(msc, ctx, rs):
+    """PartitionedMatrix::from_split accepts interior ranges that are still
+    coupled (entries of C[0:p, 0:p] between blocks); the preconditioner keeps
+    only the diagonal blocks, but matvec(C, x) with page-locked host buffers
+    must still be the full product: bit-identical to the reference matvec,
+    also right after a call with a different x (no stale rows)."""
+    import ctypes as C
+    import torch
+    from paper_1104_3349_b200 import _capi
+    rng = np.random.default_rng(31)
+    n, p = 600, 480
+    a = np.zeros((n, n))
+    a[:p, :p] = (rng.uniform(size=(p, p)) < 0.02) * rng.uniform(-1, 1, (p, p))
+    a[np.arange(p), np.arange(p)] = 8.0 + rng.uniform(0, 1, p)
+    a[:p, p:] = (rng.uniform(size=(p, n - p)) < 0.03) * rng.uniform(-1, 1, (p, n - p))
+    a[p:, :p] = (rng.uniform(size=(n - p, p)) < 0.03) * rng.uniform(-1, 1, (n - p, p))
+    a[np.arange(p, n), np.arange(p, n)] = 1.0
+    Cm = msc.SparseMatrix.from_dense(a)
+    ranges = [(0, 120), (120, 240), (240, 360), (360, 480)]
+    S = msc.SparseMatrix.from_dense(np.eye(n - p) * 2.0)
+    pc = msc.build_preconditioner_arrays(ctx, Cm, p, ranges, S, [(0, n - p)], tolA=1e-4, sA=1000)
+    mat = _capi.lib().mscg_precond_matrix(pc.h)
+    st = _capi.Status()
+    for seed in (1, 2, 3):
+        x = rng.uniform(-1, 1, n) * seed
+        want = rs.matvec(*Cm.arrays(), x)
+        xp = torch.from_numpy(x).pin_memory()
+        yp = torch.full((n,), float("nan"), dtype=torch.float64).pin_memory()
+        rc = _capi.lib().mscg_spmv(mat, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()),
+                                   _capi.MEM_HOST, C.byref(st))
+        assert rc == 0, st.message
+        assert same_bits(yp.numpy(), want)
+
+
+@pytest.mark.parametrize("variant,grid,nu,n_a,sz,overlap", [
+    ("omscn", 32, 0.1, 8, 0, -1),     # cfg1, overlap = sz (clipped)
+    ("omscnr", 32, 0.1, 8, 0, 5),
+    ("olum", 64, 0.01, 16, 40, 12),
+    ("olum", 128, 0.01, 16, 0, 40),   # cfg2 grid: band of n_g = 1264
+])
+def test_overlapped_schur_band_matches_reference(msc, ctx, ref, variant, grid, nu, n_a, sz,
+                                                 overlap):
+    """Overlapped variants end to end on the device: build_msc over
+    overlapped aggregates (device local blocks, reference merge) gives the
+    reference's banded S^ bit for bit; the preconditioner factors the band
+    whole by one exact LU (schur_single_, preconditioner.cpp:58-67,100-102):
+    its factor is the reference's, the apply matches the reference's
+    MscPreconditioner::apply to 1e-10, and right-preconditioned GMRES takes
+    the reference's iteration count."""
+    R = ref.Problem.oseen(grid, nu, n_a)
+    P = msc.oseen_problem(grid, nu, n_a)
+    R.build_schur(variant, sz, 0, overlap=overlap)
+    P.build_msc(variant, sz=sz, overlap=overlap, ctx=ctx)
+    Rs, Ps = R.csr(5), P.s_hat
+    assert np.array_equal(Rs.rp, Ps.row_offsets) and np.array_equal(Rs.ci, Ps.col_indices)
+    assert same_bits(Rs.v, Ps.values)
+    R.build_precond(1e-4, 0)
+    pc = msc.build_preconditioner(P, tolA=1e-4, sA=0, ctx=ctx)
+    assert pc.kind == variant
+    f = pc.schur_factors(0)
+    assert f.dim == P.n - P.p
+    L, U, perm = R.factors(1, 0)
+    assert same_bits(f.lower.values, L.v) and same_bits(f.upper.values, U.v)
+    assert np.array_equal(f.row_perm, perm)
+    with pytest.raises(IndexError):
+        R.factors(1, 1)  # one factor for the whole band
+    assert pc.stored_nnz() == R.stored_nnz()
+    for seed in (1, 2):
+        y = ref.random_vector(P.n, seed)
+        assert rel_err(pc.apply(y), R.apply(y)) <= APPLY_TOL
+    if grid == 32:
+        b = ref.random_vector(P.n, 0)
+        want = R.gmres(b, 30, 3000, 1e-8)
+        x, rep = msc.gmres(pc.matrix, pc, b, msc.SolverConfig(restart=30, rel_tol=1e-8))
+        assert abs(rep.iterations - want["iterations"]) <= 1
+        assert rep.converged and msc.true_residual(pc.matrix, x, b) <= 1e-8
+
+
+def test_overlapped_band_singular_error(msc, ctx, ref):
+    """A singular overlapped band raises the reference's error text
+    ("build_preconditioner: overlapped Schur band: dense_lu: zero pivot at
+    index i", preconditioner.cpp:58-67)."""
+    n, p = 40, 30
+    rng = np.random.default_rng(4)
+    a = np.zeros((n, n))
+    a[:p, :p] = np.diag(4.0 + rng.uniform(0, 1, p))
+    a[:p, p:] = rng.uniform(-1, 1, (p, n - p)) * (rng.uniform(size=(p, n - p)) < 0.3)
+    a[p:, :p] = a[:p, p:].T
+    Cm = msc.SparseMatrix.from_dense(a)
+    band = np.eye(n - p)
+    band[3, 3] = 0.0  # zero column 3 of the band
+    band[3, 4] = 1.0
+    S = msc.SparseMatrix.from_dense(band)
+    with pytest.raises(msc.SingularMatrixError) as e:
+        msc.build_preconditioner_arrays(ctx, Cm, p, [(0, 15), (15, 30)], S, None, sA=1000,
+                                        kind="omscn")
+    assert str(e.value) == ("build_preconditioner: overlapped Schur band: dense_lu: zero pivot "
+                            "at index 3")
+    assert e.value.pivot_index == 3

@@ -128,3 +128,55 @@ def test_setup_errors(msc):
         pb.build_msc("lum", mode="explicit", sizes=[1, 2])
     with pytest.raises(ValueError, match="unknown or unsupported MSC variant"):
         pb.build_msc("nope")
+
+
+@pytest.mark.parametrize("variant", ["omscn", "omscnr", "olum"])
+@pytest.mark.parametrize("grid,nu,n_a,sz,overlap", [
+    (32, 0.1, 8, 0, -1),    # overlap = sz, clipped to size - 1
+    (32, 0.1, 8, 0, 5),
+    (64, 0.01, 16, 40, 12),  # OMSCN / OMSCNR: singular D block of aggregate 13
+])
+def test_overlapped_build_msc_matches_reference(msc, ref, variant, grid, nu, n_a, sz, overlap):
+    """Overlapped numbering aggregates (aggregate_overlapped,
+    aggregates.cpp:50-85, widths as make_aggregates makes them) and the
+    banded S^ of build_msc (schur_approx.cpp:88-161): bit-identical to the
+    live reference, identical errors."""
+    R = ref.Problem.oseen(grid, nu, n_a)
+    P = msc.oseen_problem(grid, nu, n_a)
+    err_r = err_p = None
+    try:
+        R.build_schur(variant, sz, 0, overlap=overlap)
+    except ref.RefError as e:
+        err_r = str(e)
+    try:
+        P.build_msc(variant, sz=sz, overlap=overlap)
+    except (msc.SingularMatrixError, ValueError) as e:
+        err_p = str(e)
+    assert err_r == err_p
+    if err_r:
+        return
+    Rs, Ps = R.csr(5), P.s_hat
+    assert np.array_equal(Rs.rp, Ps.row_offsets) and np.array_equal(Rs.ci, Ps.col_indices)
+    assert same_bits(Rs.v, Ps.values)
+    assert np.array_equal(R.schur_ranges(), P.schur_ranges())
+    # banded: some owned column is written outside its own aggregate's rows
+    ranges = P.schur_ranges()
+    own = np.repeat(np.arange(len(ranges)), np.diff(ranges, axis=1).ravel())
+    rows = np.repeat(np.arange(Ps.nrows), np.diff(Ps.row_offsets))
+    assert np.any(own[rows] != own[Ps.col_indices])
+
+
+def test_overlapped_aggregate_errors(msc):
+    """aggregate_overlapped / check_agg_compatible argument errors
+    (aggregates.cpp:57-74, schur_approx.cpp:65-72): same text."""
+    P = msc.oseen_problem(32, 0.1, 8)
+    ng = P.n - P.p
+    k = len(np.asarray(msc.oseen_problem(32, 0.1, 8).build_msc("lum").schur_ranges()))
+    with pytest.raises(ValueError, match="variant mscn needs a non-overlapped aggregate set"):
+        P.build_msc("mscn", widths=[1] * (k - 1) + [0])
+    with pytest.raises(ValueError, match="widths must be >= 0 and end with 0"):
+        P.build_msc("omscn", widths=[1] * k)
+    with pytest.raises(ValueError, match="violates w < size"):
+        P.build_msc("omscn", widths=[ng] + [0] * (k - 1))
+    with pytest.raises(ValueError, match="one width per aggregate"):
+        P.build_msc("omscn", widths=[0])
