@@ -127,8 +127,9 @@ class GpuPreconditioner : public msc::Preconditioner {
   int n_;
 };
 
-// build_preconditioner (preconditioner.hpp:66-68) for the block-diagonal
-// (non-overlapped) Schur approximations.
+// build_preconditioner (preconditioner.hpp:66-68): block-diagonal Schur
+// approximations factor per owned range, overlapped (banded) ones whole by
+// one exact LU (schur_single_, preconditioner.cpp:58-67).
 inline GpuPreconditioner build_preconditioner(const msc::PartitionedMatrix& c,
                                               const msc::SchurApproximation& schur,
                                               double tolA, int sA,
@@ -136,8 +137,6 @@ inline GpuPreconditioner build_preconditioner(const msc::PartitionedMatrix& c,
   if (schur.s_hat.rows() != c.n_g())
     throw std::invalid_argument(
         "build_preconditioner: Schur approximation does not match the split");
-  if (schur.overlapped)
-    throw std::invalid_argument("build_preconditioner: overlapped Schur bands are not supported");
   std::vector<int> dr, sr;
   for (auto [b, e] : c.d_block_ranges) {
     dr.push_back(b);
@@ -153,7 +152,9 @@ inline GpuPreconditioner build_preconditioner(const msc::PartitionedMatrix& c,
                            c.C.col_indices().data(), c.C.values().data(),
                            static_cast<int>(c.d_block_ranges.size()), dr.data(),
                            schur.s_hat.row_offsets().data(), schur.s_hat.col_indices().data(),
-                           schur.s_hat.values().data(), static_cast<int>(schur.owned_ranges.size()),
+                           schur.s_hat.values().data(),
+                           schur.overlapped ? MSCG_SCHUR_SINGLE
+                                            : static_cast<int>(schur.owned_ranges.size()),
                            sr.data(), tolA, sA, &h, &st),
         st);
   return GpuPreconditioner(h, schur.exact ? "exact-schur" : msc::variant_name(schur.variant),
@@ -180,7 +181,10 @@ inline std::vector<double> matvec(const msc::SparseMatrix& a, std::span<const do
 
 // gmres (gmres.hpp:44-47): right/left-preconditioned restarted GMRES with
 // the reference's convergence rules; `prec` must be a GpuPreconditioner or
-// null (no CPU fallback for other preconditioners).
+// null (no CPU fallback for other preconditioners).  Orthogonalisation is
+// DCGS2 (two basis sweeps; same projections as the reference's MGS, rounding
+// regrouped).  cfg.restart <= 500 (std::invalid_argument above: the Givens
+// state is staged in shared memory).
 inline std::pair<std::vector<double>, msc::SolveReport> gmres(
     const msc::SparseMatrix& a, const msc::Preconditioner* prec, const std::vector<double>& rhs,
     const msc::SolverConfig& cfg, Context& ctx = Context::instance()) {

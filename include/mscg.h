@@ -21,6 +21,19 @@
  *     pinned staging); MSCG_MEM_DEVICE are device pointers on the handle's
  *     device and stream.  There is no CPU fallback: without a CUDA device the
  *     device entry points fail with MSCG_ERR_CUDA.
+ *
+ * Limits the reference does not have (each fails with
+ * MSCG_ERR_INVALID_ARGUMENT and a message naming it, never silently):
+ *   - a factored block (interior block, Schur block, or the whole overlapped
+ *     band) holds at most 65535 rows: factor columns are stored block-local
+ *     as uint16;
+ *   - the ILUT working row (8 B per block row) and the triangular solve's
+ *     solution vector plus far-sum slots live in shared memory (227 KB per
+ *     CTA): about 27 000 rows per ILUT block and 25 000 per solved block
+ *     (BASELINE blocks are <= 3 400 rows; cfg3's whole S^ band is 6 360);
+ *   - GMRES restart <= 500 (the Givens state is staged in shared memory);
+ *   - a context drives one device; contexts on several devices may coexist
+ *     in one process.
  */
 #ifndef MSCG_H
 #define MSCG_H

@@ -32,6 +32,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cstdio>
+
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -200,13 +202,23 @@ std::unique_ptr<Correction> build_correction(Ctx* ctx, const FactorSet& D, const
     return nullptr;
   }
   if (mode == kCorrAuto) {
-    // worth it when the panels move fewer bytes than a pass over the factors
-    // (12 B per stored entry incl. the U diagonal), and they fit with room
+    // decided by the byte counts alone: worth it when the panels move fewer
+    // bytes than a pass over the factors (12 B per stored entry incl. the U
+    // diagonal).  Free memory is only an out-of-memory guard, and a skip for
+    // that reason is logged (the apply path, and so its rounding, is then
+    // the reference's two interior passes; mscg_precond_correction reports
+    // which path a preconditioner uses).
     const int64_t factor_bytes = 12 * (D.nnz_l() + D.nnz_u() + D.total_rows);
+    if (w_bytes > factor_bytes) return nullptr;
     size_t free_b = 0, total_b = 0;
     MSCG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (w_bytes > factor_bytes || static_cast<size_t>(w_bytes) + (size_t(4) << 30) > free_b)
+    if (static_cast<size_t>(w_bytes) + (size_t(4) << 30) > free_b) {
+      fprintf(stderr,
+              "mscg: interior correction skipped: its %.2f GB of panels do not fit in %.2f GB "
+              "of free device memory (applies use the two interior passes)\n",
+              w_bytes / 1e9, free_b / 1e9);
       return nullptr;
+    }
   }
   cudaStream_t s = ctx->stream;
   c->row0 = D.row0.as<int>();

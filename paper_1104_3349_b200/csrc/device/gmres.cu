@@ -554,18 +554,20 @@ __device__ void dcgs2_fix(const Small& s, const Dcgs& d, int j, bool finalize_on
 }
 
 // Sweep 1: dots of y = slot j (and w) against q_0..q_{j-1}, plus y.y and
-// y.w, basis vectors in groups of kG (w and y re-read per group).
-template <int kG>
-__global__ void __launch_bounds__(kThreads) dcgs2_dot_kernel(int n, int j, const double* __restrict__ V,
+// y.w, basis vectors in groups of kG (w and y re-read per group).  kW = false:
+// the cycle's finalize-only sweep (no w).  The inner loop is branch-free so
+// that every load of a row pair is in flight at once.
+template <int kG, bool kW>
+__global__ void __launch_bounds__(kThreads, 1) dcgs2_dot_kernel(int n, int j, const double* __restrict__ V,
                                                              size_t ld, const double* __restrict__ w,
-                                                             Reducer red, Small s, Dcgs d, int finalize_only) {
+                                                             Reducer red, Small s, Dcgs d) {
   __shared__ double sh[kThreads / 32][2 * kG + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nq = j;
   const double* y = V + ld * j;
   const int npair = n >> 1;
   const double2* y2 = reinterpret_cast<const double2*>(y);
-  const double2* w2 = reinterpret_cast<const double2*>(w);
+  const double2* w2 = reinterpret_cast<const double2*>(kW ? w : y);
   const int ngroups = nq > 0 ? (nq + kG - 1) / kG : 1;
   const int stride = gridDim.x * blockDim.x;
   for (int grp = 0; grp < ngroups; ++grp) {
@@ -575,25 +577,47 @@ __global__ void __launch_bounds__(kThreads) dcgs2_dot_kernel(int n, int j, const
     double ay[kG], aw[kG], yy = 0.0, yw = 0.0;
 #pragma unroll
     for (int g = 0; g < kG; ++g) ay[g] = aw[g] = 0.0;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npair; q += stride) {
-      const double2 yv = y2[q];
-      const double2 wv = w ? w2[q] : make_double2(0.0, 0.0);
-      double2 v[kG];
+    // basis rows past the group's end read a valid vector (clamped index)
+    // into accumulators that are never stored
+    const double2* vg[kG];
 #pragma unroll
-      for (int g = 0; g < kG; ++g)
-        v[g] = g < ng ? __ldg(reinterpret_cast<const double2*>(V + ld * (i0 + g)) + q) : make_double2(0.0, 0.0);
+    for (int g = 0; g < kG; ++g)
+      vg[g] = reinterpret_cast<const double2*>(V + ld * min(i0 + g, max(nq - 1, 0)));
+    // two row pairs per trip (q, q + stride), like multidot_kernel: 2 kG
+    // basis loads in flight per thread
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + stride < npair; q += 2 * stride) {
+      const double2 ya = y2[q], yb = y2[q + stride];
+      const double2 wa = w2[q], wb = w2[q + stride];
+      double2 va[kG], vb[kG];
 #pragma unroll
       for (int g = 0; g < kG; ++g) {
-        ay[g] = fma(v[g].y, yv.y, fma(v[g].x, yv.x, ay[g]));
-        aw[g] = fma(v[g].y, wv.y, fma(v[g].x, wv.x, aw[g]));
+        va[g] = __ldg(vg[g] + q);
+        vb[g] = __ldg(vg[g] + q + stride);
       }
-      if (first) {
-        yy = fma(yv.y, yv.y, fma(yv.x, yv.x, yy));
-        yw = fma(yv.y, wv.y, fma(yv.x, wv.x, yw));
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        ay[g] = fma(vb[g].y, yb.y, fma(vb[g].x, yb.x, fma(va[g].y, ya.y, fma(va[g].x, ya.x, ay[g]))));
+        if (kW)
+          aw[g] = fma(vb[g].y, wb.y, fma(vb[g].x, wb.x, fma(va[g].y, wa.y, fma(va[g].x, wa.x, aw[g]))));
       }
+      yy = fma(yb.y, yb.y, fma(yb.x, yb.x, fma(ya.y, ya.y, fma(ya.x, ya.x, yy))));
+      if (kW) yw = fma(yb.y, wb.y, fma(yb.x, wb.x, fma(ya.y, wa.y, fma(ya.x, wa.x, yw))));
+    }
+    if (q < npair) {
+      const double2 yv = y2[q];
+      const double2 wv = w2[q];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        const double2 v = __ldg(vg[g] + q);
+        ay[g] = fma(v.y, yv.y, fma(v.x, yv.x, ay[g]));
+        if (kW) aw[g] = fma(v.y, wv.y, fma(v.x, wv.x, aw[g]));
+      }
+      yy = fma(yv.y, yv.y, fma(yv.x, yv.x, yy));
+      if (kW) yw = fma(yv.y, wv.y, fma(yv.x, wv.x, yw));
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: the last row
-      const double yl = y[n - 1], wl = w ? w[n - 1] : 0.0;
+      const double yl = y[n - 1], wl = kW ? w[n - 1] : 0.0;
 #pragma unroll
       for (int g = 0; g < kG; ++g)
         if (g < ng) {
@@ -601,10 +625,8 @@ __global__ void __launch_bounds__(kThreads) dcgs2_dot_kernel(int n, int j, const
           ay[g] = fma(vl, yl, ay[g]);
           aw[g] = fma(vl, wl, aw[g]);
         }
-      if (first) {
-        yy = fma(yl, yl, yy);
-        yw = fma(yl, wl, yw);
-      }
+      yy = fma(yl, yl, yy);
+      yw = fma(yl, wl, yw);
     }
 #pragma unroll
     for (int g = 0; g < 2 * kG + 2; ++g) {
@@ -626,7 +648,7 @@ __global__ void __launch_bounds__(kThreads) dcgs2_dot_kernel(int n, int j, const
       if (vec >= 0) {
         double t = 0.0;
         for (int k = 0; k < kThreads / 32; ++k) t += sh[k][g];
-        red.partials[static_cast<size_t>(vec) * red.nblk + blockIdx.x] = t;
+        red.partials[static_cast<size_t>(vec) * red.nblk + blockIdx.x] = (kW || g < kG || g == 2 * kG) ? t : 0.0;
       }
     }
     __syncthreads();
@@ -634,7 +656,7 @@ __global__ void __launch_bounds__(kThreads) dcgs2_dot_kernel(int n, int j, const
   if (last_block(red)) {
     finish(red, 2 * nq + 2, d.dots, 0);
     __syncthreads();
-    dcgs2_fix(s, d, j, finalize_only != 0);
+    dcgs2_fix(s, d, j, !kW);
   }
 }
 
@@ -644,7 +666,13 @@ __global__ void __launch_bounds__(kThreads) dcgs2_dot_kernel(int n, int j, const
 __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, double* V, size_t ld,
                                                               const double* __restrict__ w, Small s,
                                                               Dcgs d, Reducer red, double denom) {
-  __shared__ double sS[512], sT[512];
+  // the coefficients and (last CTA, after the sweep) the Givens stage share
+  // one shared-memory buffer: more CTAs per SM for the sweep
+  constexpr int kCoef = 2 * (kMaxRestart + 12);
+  constexpr int kStage = (sizeof(GivensStage) + sizeof(double) - 1) / sizeof(double);
+  __shared__ __align__(16) double sbuf[kCoef > kStage ? kCoef : kStage];
+  double* sS = sbuf;
+  double* sT = sbuf + kMaxRestart + 12;
   __shared__ double sh[kThreads / 32];
   const int m = s.m;
   for (int i = threadIdx.x; i < j; i += blockDim.x) {
@@ -665,28 +693,15 @@ __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, doub
     const double2 yv = y2[q], wv = w2[q];
     double ux = ok ? yv.x / nu : 0.0, uy = ok ? yv.y / nu : 0.0;
     double wx = ok ? wv.x / nu : 0.0, wy = ok ? wv.y / nu : 0.0;
-    constexpr int kU = 16;  // basis rows in flight (software-pipelined)
-    double2 cur[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-      cur[u] = u < j ? __ldg(reinterpret_cast<const double2*>(V + ld * u) + q) : make_double2(0.0, 0.0);
-    for (int i0 = 0; i0 < j; i0 += kU) {
-      double2 nxt[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + kU + u;
-        nxt[u] = i < j ? __ldg(reinterpret_cast<const double2*>(V + ld * i) + q) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (i0 + u < j) {
-          ux = fma(-sS[i0 + u], cur[u].x, ux);
-          uy = fma(-sS[i0 + u], cur[u].y, uy);
-          wx = fma(-sT[i0 + u], cur[u].x, wx);
-          wy = fma(-sT[i0 + u], cur[u].y, wy);
-        }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) cur[u] = nxt[u];
+    // multiaxpy-style: a short unrolled loop per thread, many warps per SM
+    // keep the basis stream in flight
+#pragma unroll 8
+    for (int i = 0; i < j; ++i) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(V + ld * i) + q);
+      ux = fma(-sS[i], v.x, ux);
+      uy = fma(-sS[i], v.y, uy);
+      wx = fma(-sT[i], v.x, wx);
+      wy = fma(-sT[i], v.y, wy);
     }
     const double qx = ux / rho, qy = uy / rho;
     const double nx = fma(-c, qx, wx) / rho, ny = fma(-c, qy, wy) / rho;
@@ -710,7 +725,7 @@ __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, doub
   const double bs = block_sum(acc, sh);
   if (threadIdx.x == 0) red.partials[blockIdx.x] = bs;
   if (last_block(red)) {
-    __shared__ GivensStage gs;
+    GivensStage& gs = *reinterpret_cast<GivensStage*>(sbuf);  // coefficients no longer read
     __shared__ double hn_s;
     finish(red, 1, d.nu + j + 1, 1);
     if (threadIdx.x == 0) {
@@ -932,8 +947,8 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
       double* Hc = st.H + static_cast<size_t>(j) * (m + 1);
       if (dcgs2) {
         // two basis sweeps; the status comes from sweep 2's last CTA
-        (dot16 ? dcgs2_dot_kernel<16> : dcgs2_dot_kernel<8>)<<<G, kThreads, 0, s>>>(
-            n, j, vbase, ld, wp, ws.red, st, dc, 0);
+        (dot16 ? dcgs2_dot_kernel<16, true> : dcgs2_dot_kernel<8, true>)<<<G, kThreads, 0, s>>>(
+            n, j, vbase, ld, wp, ws.red, st, dc);
         dcgs2_axpy_kernel<<<G, kThreads, 0, s>>>(n, j, vbase, ld, wp, st, dc, ws.red, denom);
         ctx->launches += 2;
         MSCG_CUDA(cudaMemcpyAsync(hstat + 4 * (j & 1), st.status, 3 * sizeof(double),
@@ -999,8 +1014,8 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
     if (dcgs2 && mm > 0 && mm >= jmax) {
       // no speculative iteration in the stream: finalise column mm-1 with
       // one dot sweep of y_mm against q_0..q_{mm-1}
-      (dot16 ? dcgs2_dot_kernel<16> : dcgs2_dot_kernel<8>)<<<G, kThreads, 0, s>>>(
-          n, mm, vbase, ld, nullptr, ws.red, st, dc, 1);
+      (dot16 ? dcgs2_dot_kernel<16, false> : dcgs2_dot_kernel<8, false>)<<<G, kThreads, 0, s>>>(
+          n, mm, vbase, ld, nullptr, ws.red, st, dc);
       ctx->launches++;
     }
     backsolve_kernel<<<1, 32, 0, s>>>(st, mm);

@@ -673,22 +673,30 @@ size_t smem_bytes(int dim_max, int workers, int slots) {
 }  // namespace
 
 void ensure_smem(const void* kern, size_t smem) {
+  // the attribute is per device: cache it per (device, kernel)
   static std::mutex mu;
-  static std::vector<std::pair<const void*, size_t>> set;  // kernel -> attribute value
+  struct Entry {
+    int dev;
+    const void* kern;
+    size_t smem;
+  };
+  static std::vector<Entry> set;
+  int dev = 0;
+  MSCG_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
   for (auto& e : set)
-    if (e.first == kern) {
-      if (smem > e.second) {
+    if (e.dev == dev && e.kern == kern) {
+      if (smem > e.smem) {
         MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
-        e.second = smem;
+        e.smem = smem;
       }
       return;
     }
   if (smem > 48 * 1024)
     MSCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-  set.push_back({kern, std::max<size_t>(smem, 48 * 1024)});
+  set.push_back({dev, kern, std::max<size_t>(smem, 48 * 1024)});
 }
 
 void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const double* sub,
@@ -752,10 +760,13 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const char* e = getenv("MSCG_TRI_VARIANT");
     return e ? atoi(e) : 0;
   }();
-  auto launch = [&](auto kern, int warps, size_t smem) {
+  auto check_smem = [&](size_t smem) {
     if (smem > 227 * 1024)
       throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
                          " rows exceeds the shared-memory solution vector");
+  };
+  auto launch = [&](auto kern, int warps, size_t smem) {
+    check_smem(smem);
     // the attribute is raised once per kernel and size (a driver call on
     // every launch costs the stream its back-to-back launches)
     ensure_smem(reinterpret_cast<const void*>(kern), smem);
@@ -769,12 +780,12 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   // Fewer blocks than SMs (cfg2/cfg3): each block has an SM to itself, so
   // large blocks get 31 workers (1024 threads) instead of 15 (cfg2 D-solve
   // 0.645 -> 0.417 ms); small ones (cfg1, ~400 rows) are faster without.
-  static const int sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
+  int sms = 148;
+  {
+    int dev = 0;
+    MSCG_CUDA(cudaGetDevice(&dev));
+    MSCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   if (variant == 0 && npos <= sms && d > 1024) {
     launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
     MSCG_CUDA(cudaGetLastError());
@@ -797,6 +808,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     MSCG_CUDA(cudaEventRecord(fs.tail_ev[0], s));
     MSCG_CUDA(cudaStreamWaitEvent(fs.tail_stream, fs.tail_ev[0], 0));
     const int head = npos - tail;
+    check_smem(smem_bytes<true>(d, 31, ns));
     {
       auto k16 = trisolve_kernel<16, 4, 2, true, false>;
       const size_t sm16 = smem_bytes<true>(d, 15, ns);

@@ -113,6 +113,28 @@ int main() {
     std::vector<double> mv = msc_b200::matvec(c.pm.C, y);
     report(mv == matvec(c.pm.C, y), "matvec_bit_identical");
   }
+  // --- cfg1 with an overlapped Schur band (OMSCN): the drop-in factors the
+  // band whole like the reference's schur_single_ (preconditioner.cpp:58-67)
+  {
+    Cfg c = oseen(32, 0.1, 8);
+    const int ng = c.pm.n_g(), sz = ng / 8;
+    std::vector<int> sizes = equal_sizes(ng, sz), widths(sizes.size(), sz);
+    widths.back() = 0;
+    clip_overlap_widths(ng, sizes, widths);
+    SchurApproximation s =
+        build_msc(c.pm, aggregate_overlapped(ng, sizes, widths), MscVariant::Omscn);
+    MscPreconditioner ref = build_preconditioner(c.pm, s, 1e-4, 0);
+    auto gpu = msc_b200::build_preconditioner(c.pm, s, 1e-4, 0);
+    std::mt19937 rng(1);
+    std::vector<double> y = oracle::random_vector(c.pm.n(), rng);
+    const double err = oracle::rel_err(gpu.apply(y), ref.apply(y));
+    report(s.overlapped && err < 1e-10, "omscn_band_apply_vs_reference", std::to_string(err));
+    TriangularFactors f = gpu.factors(1, 0);
+    report(ref.schur_factors().size() == 1 && f.dim() == ng &&
+               f.upper.same_pattern_and_values(ref.schur_factors()[0].upper) &&
+               f.lower.same_pattern_and_values(ref.schur_factors()[0].lower),
+           "omscn_band_factor_bit_identical");
+  }
   // --- cfg3 as written: identical SingularMatrixError ---
   {
     Cfg c = oseen(256, 0.002, 64, true, 1.1);
