@@ -13,9 +13,12 @@ than L2, so no flush is needed between steps.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
                     [--mode apply|gmres] [--impl ours|reference]
 
-For N > 1 (torchrun) every rank runs an independent replica of the
-single-GPU workload ("replicas only": BASELINE runs the path on one GPU;
-see DESIGN.md §Multi-GPU); value = total steps of all ranks / max time.
+For N > 1 (torchrun) the interior blocks are sharded over the ranks (one
+process per GPU): one step = one distributed
+apply + one distributed SpMV, two n_g all-reduces over NCCL; strong scaling,
+value = whole-job applies/s over the max-over-ranks device time.
+`--replicas` runs N independent single-GPU replicas instead.  The
+distributed GMRES (mscg_gmres_shard) is exercised by tests/test_gpu_dist.py.
 """
 from __future__ import annotations
 

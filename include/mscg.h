@@ -333,6 +333,24 @@ int mscg_gmres(mscg_ctx *ctx, mscg_csr *a, mscg_precond *pc, const double *b,
                double *x, int mem, const mscg_gmres_config *cfg,
                mscg_gmres_report *rep, double *history, int hist_cap,
                mscg_status *st);
+
+/* Distributed right-preconditioned GMRES (DCGS2) over preconditioner shards
+ * (no reference counterpart): one process per GPU, each with its
+ * shard (mscg_precond_build_shard).  b, x are global-length vectors (x gets
+ * the rank's interior rows and the interface, other rows zero).  Krylov
+ * vectors are compact per rank ([own interior rows | interface], the
+ * interface replicated); the exchanges per iteration are two n_g all-reduces
+ * (preconditioner, matvec) and two short ones (the 2j+2 sweep-1 dots and one
+ * norm).  allreduce(count, user) must replace comm_buf[0:count] (device,
+ * comm_cap >= max(2*restart+4, n_g) doubles) by its sum over the ranks, in
+ * stream order on the context stream (NCCL on that stream, or gloo on CUDA
+ * tensors).  cfg->side must be right and cfg->orth DCGS2. */
+typedef void (*mscg_allreduce_fn)(int count, void *user);
+int mscg_gmres_shard(mscg_ctx *ctx, mscg_precond *shard, int rank, int world,
+                     const double *b, double *x, int mem, const mscg_gmres_config *cfg,
+                     double *comm_buf, int comm_cap, mscg_allreduce_fn allreduce,
+                     void *user, mscg_gmres_report *rep, double *history, int hist_cap,
+                     mscg_status *st);
 /* true_residual (gmres.cpp:26-33). */
 int mscg_true_residual(mscg_ctx *ctx, mscg_csr *a, const double *x,
                        const double *b, int mem, double *out, mscg_status *st);

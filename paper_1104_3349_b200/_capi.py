@@ -35,6 +35,9 @@ class GmresConfig(C.Structure):
                 ("side", C.c_int), ("orth", C.c_int)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_int, C.c_void_p)
+
+
 class GmresReport(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("history_len", C.c_int),
                 ("history_total", C.c_int), ("solve_seconds", C.c_double),
@@ -113,6 +116,9 @@ _SIGS = {
     "mscg_precond_matrix": (vp, [vp]),
     "mscg_gmres": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(GmresConfig),
                              C.POINTER(GmresReport), vp, C.c_int, C.POINTER(Status)]),
+    "mscg_gmres_shard": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_int,
+                                   C.POINTER(GmresConfig), vp, C.c_int, vp, vp,
+                                   C.POINTER(GmresReport), vp, C.c_int, C.POINTER(Status)]),
     "mscg_precond_nnz": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "mscg_precond_use_correction": (C.c_int, [vp, C.c_int]),
     "mscg_precond_layout_bytes": (C.c_int, [vp, C.POINTER(C.c_int64)]),

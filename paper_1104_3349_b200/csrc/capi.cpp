@@ -855,6 +855,50 @@ int mscg_gmres(mscg_ctx* ctx, mscg_csr* a, mscg_precond* pc, const double* b, do
   });
 }
 
+int mscg_gmres_shard(mscg_ctx* ctx, mscg_precond* shard, int rank, int world, const double* b,
+                     double* x, int mem, const mscg_gmres_config* cfg, double* comm_buf,
+                     int comm_cap, mscg_allreduce_fn allreduce, void* user,
+                     mscg_gmres_report* rep, double* history, int hist_cap, mscg_status* st) {
+  return guard(st, [&] {
+    if (!ctx || !shard || !shard->pc->shard.on)
+      throw std::invalid_argument("gmres_shard: null context or not a shard preconditioner");
+    if (world > 1 && (!allreduce || !comm_buf))
+      throw std::invalid_argument("gmres_shard: an all-reduce callback and buffer are needed");
+    if (rank < 0 || rank >= std::max(world, 1)) throw std::invalid_argument("gmres_shard: bad rank");
+    mscg::GmresConfig c;
+    if (cfg) {
+      c.restart = cfg->restart;
+      c.max_iters = cfg->max_iters;
+      c.rel_tol = cfg->rel_tol;
+      c.left = cfg->side == 1;
+      c.orth = cfg->orth;
+    }
+    mscg::DistComm comm;
+    comm.rank = rank;
+    comm.size = std::max(world, 1);
+    comm.buf = comm_buf;
+    comm.cap = comm_cap;
+    comm.allreduce = allreduce;
+    comm.user = user;
+    const size_t n = shard->pc->n;
+    mscg::GmresResult r;
+    with_vectors(ctx, b, n, x, n, mem, [&](const double* db, double* dx) {
+      r = mscg::gmres_shard(&ctx->ctx, shard->pc.get(), db, dx, c, comm);
+    });
+    if (rep) {
+      rep->iterations = r.iterations;
+      rep->converged = r.converged ? 1 : 0;
+      rep->history_total = static_cast<int>(r.history.size());
+      rep->history_len = std::min<int>(hist_cap, rep->history_total);
+      rep->solve_seconds = r.seconds;
+      rep->final_true_residual = r.final_true;
+    }
+    if (history)
+      for (int i = 0; i < std::min<int>(hist_cap, static_cast<int>(r.history.size())); ++i)
+        history[i] = r.history[i];
+  });
+}
+
 int mscg_true_residual(mscg_ctx* ctx, mscg_csr* a, const double* x, const double* b, int mem,
                        double* out, mscg_status* st) {
   return guard(st, [&] {
@@ -866,8 +910,12 @@ int mscg_true_residual(mscg_ctx* ctx, mscg_csr* a, const double* x, const double
     }
     mscg::DevBuf dx(sizeof(double) * std::max<size_t>(1, a->a->ncols)),
         db(sizeof(double) * std::max<size_t>(1, n));
-    MSCG_CUDA(cudaMemcpy(dx.p, x, sizeof(double) * a->a->ncols, cudaMemcpyHostToDevice));
-    MSCG_CUDA(cudaMemcpy(db.p, b, sizeof(double) * n, cudaMemcpyHostToDevice));
+    // on the context stream (a non-blocking stream: a legacy-stream
+    // cudaMemcpy from pageable memory may still be in flight when the
+    // residual kernels start)
+    cudaStream_t s = ctx->ctx.stream;
+    MSCG_CUDA(cudaMemcpyAsync(dx.p, x, sizeof(double) * a->a->ncols, cudaMemcpyHostToDevice, s));
+    MSCG_CUDA(cudaMemcpyAsync(db.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     *out = mscg::true_residual(&ctx->ctx, *a->a, dx.as<double>(), db.as<double>());
   });
 }

@@ -106,6 +106,27 @@ __global__ void __launch_bounds__(kThreads) nrm2_kernel(int n, const double* __r
   if (last_block(red)) finish(red, 1, out, 1);
 }
 
+// sum of squares of x[0:n) -> *out (a distributed rank's local part)
+__global__ void __launch_bounds__(kThreads) sumsq_kernel(int n, const double* __restrict__ x,
+                                                         Reducer red, double* out) {
+  __shared__ double sh[kThreads / 32];
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    acc = fma(x[i], x[i], acc);
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) red.partials[blockIdx.x] = s;
+  if (last_block(red)) finish(red, 1, out, 0);
+}
+
+__global__ void sqrt_kernel(double* v) { *v = sqrt(*v); }
+
+// y = a - b (elementwise)
+__global__ void sub2_kernel(int n, const double* __restrict__ a, const double* __restrict__ b,
+                            double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = a[i] - b[i];
+}
+
 // h[i] = V_i . w for i < nv: basis vectors in groups of kDotGroup, so w is
 // read once per group and each CTA reduces kDotGroup sums per pass.  Rows
 // go in 16-byte pairs (the basis is stored with a 32-element-aligned
@@ -560,7 +581,7 @@ __device__ void dcgs2_fix(const Small& s, const Dcgs& d, int j, bool finalize_on
 template <int kG, bool kW>
 __global__ void __launch_bounds__(kThreads, 1) dcgs2_dot_kernel(int n, int j, const double* __restrict__ V,
                                                              size_t ld, const double* __restrict__ w,
-                                                             Reducer red, Small s, Dcgs d) {
+                                                             Reducer red, Small s, Dcgs d, int local) {
   __shared__ double sh[kThreads / 32][2 * kG + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nq = j;
@@ -655,17 +676,57 @@ __global__ void __launch_bounds__(kThreads, 1) dcgs2_dot_kernel(int n, int j, co
   }
   if (last_block(red)) {
     finish(red, 2 * nq + 2, d.dots, 0);
+    if (local) return;  // distributed: the sums are all-reduced first (dcgs2_fix_kernel)
     __syncthreads();
     dcgs2_fix(s, d, j, !kW);
   }
 }
 
+__global__ void __launch_bounds__(kThreads) dcgs2_fix_kernel(Small s, Dcgs d, int j, int finalize_only) {
+  dcgs2_fix(s, d, j, finalize_only != 0);
+}
+
+// Preliminary rotation of column j once nu[j+1] = ||y_{j+1}|| is final, and
+// the iteration's status (one CTA; gs aliases free shared memory).
+__device__ void dcgs2_prelim(const Small& s, const Dcgs& d, int j, double denom, GivensStage& gs) {
+  __shared__ double hn_s;
+  const int m = s.m;
+  if (threadIdx.x == 0) {
+    hn_s = d.nu[j + 1];
+    d.Hraw[static_cast<size_t>(j) * (m + 1) + j + 1] = hn_s;
+  }
+  __syncthreads();
+  // preliminary rotation of column j (the final one follows its
+  // reorthogonalisation in the next sweep 1)
+  stage_givens(gs, s, d.Hraw + static_cast<size_t>(j) * (m + 1), j);
+  if (threadIdx.x == 0) {
+    const double hn = hn_s;
+    double cs, sn;
+    rotate_staged(gs, j, cs, sn);
+    const double gj1 = -sn * s.g[j];
+    s.status[0] = fabs(gj1) / denom;
+    s.status[1] = !(hn >= 1e-14) ? 1.0 : 0.0;
+    s.status[2] = hn;
+  }
+}
+
+// distributed: nu[j+1] holds the all-reduced sum of squares
+__global__ void __launch_bounds__(kThreads) dcgs2_prelim_kernel(Small s, Dcgs d, int j, double denom) {
+  __shared__ GivensStage gs;
+  if (threadIdx.x == 0) d.nu[j + 1] = sqrt(d.nu[j + 1]);
+  __syncthreads();
+  dcgs2_prelim(s, d, j, denom, gs);
+}
+
 // Sweep 2: q_j = (y/nu - Q s)/rho over slot j (in place) and
 // y_{j+1} = (w/nu - Q t - c q_j)/rho into slot j+1, ||y_{j+1}|| reduced; the
 // last CTA forms the preliminary rotation of column j and the status.
+// n_dot <= n: rows counted in the norm (a distributed rank's own rows);
+// local: leave the sum of squares in nu[j+1] for the all-reduce.
 __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, double* V, size_t ld,
                                                               const double* __restrict__ w, Small s,
-                                                              Dcgs d, Reducer red, double denom) {
+                                                              Dcgs d, Reducer red, double denom,
+                                                              int n_dot, int local) {
   // the coefficients and (last CTA, after the sweep) the Givens stage share
   // one shared-memory buffer: more CTAs per SM for the sweep
   constexpr int kCoef = 2 * (kMaxRestart + 12);
@@ -707,8 +768,8 @@ __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, doub
     const double nx = fma(-c, qx, wx) / rho, ny = fma(-c, qy, wy) / rho;
     y2[q] = make_double2(qx, qy);
     yn2[q] = make_double2(nx, ny);
-    acc = fma(nx, nx, acc);
-    acc = fma(ny, ny, acc);
+    if (2 * q < n_dot) acc = fma(nx, nx, acc);
+    if (2 * q + 1 < n_dot) acc = fma(ny, ny, acc);
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: the last row
     double ul = ok ? y[n - 1] / nu : 0.0, wl = ok ? w[n - 1] / nu : 0.0;
@@ -720,31 +781,18 @@ __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, doub
     const double ql = ul / rho, nl = fma(-c, ql, wl) / rho;
     y[n - 1] = ql;
     yn[n - 1] = nl;
-    acc = fma(nl, nl, acc);
+    if (n - 1 < n_dot) acc = fma(nl, nl, acc);
   }
   const double bs = block_sum(acc, sh);
   if (threadIdx.x == 0) red.partials[blockIdx.x] = bs;
   if (last_block(red)) {
-    GivensStage& gs = *reinterpret_cast<GivensStage*>(sbuf);  // coefficients no longer read
-    __shared__ double hn_s;
+    if (local) {
+      finish(red, 1, d.nu + j + 1, 0);
+      return;
+    }
     finish(red, 1, d.nu + j + 1, 1);
-    if (threadIdx.x == 0) {
-      hn_s = d.nu[j + 1];
-      d.Hraw[static_cast<size_t>(j) * (m + 1) + j + 1] = hn_s;
-    }
-    __syncthreads();
-    // preliminary rotation of column j (the final one follows its
-    // reorthogonalisation in the next sweep 1)
-    stage_givens(gs, s, d.Hraw + static_cast<size_t>(j) * (m + 1), j);
-    if (threadIdx.x == 0) {
-      const double hn = hn_s;
-      double cs, sn;
-      rotate_staged(gs, j, cs, sn);
-      const double gj1 = -sn * s.g[j];
-      s.status[0] = fabs(gj1) / denom;
-      s.status[1] = !(hn >= 1e-14) ? 1.0 : 0.0;
-      s.status[2] = hn;
-    }
+    GivensStage& gs = *reinterpret_cast<GivensStage*>(sbuf);  // coefficients no longer read
+    dcgs2_prelim(s, d, j, denom, gs);
   }
 }
 
@@ -948,8 +996,8 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
       if (dcgs2) {
         // two basis sweeps; the status comes from sweep 2's last CTA
         (dot16 ? dcgs2_dot_kernel<16, true> : dcgs2_dot_kernel<8, true>)<<<G, kThreads, 0, s>>>(
-            n, j, vbase, ld, wp, ws.red, st, dc);
-        dcgs2_axpy_kernel<<<G, kThreads, 0, s>>>(n, j, vbase, ld, wp, st, dc, ws.red, denom);
+            n, j, vbase, ld, wp, ws.red, st, dc, 0);
+        dcgs2_axpy_kernel<<<G, kThreads, 0, s>>>(n, j, vbase, ld, wp, st, dc, ws.red, denom, n, 0);
         ctx->launches += 2;
         MSCG_CUDA(cudaMemcpyAsync(hstat + 4 * (j & 1), st.status, 3 * sizeof(double),
                                   cudaMemcpyDeviceToHost, s));
@@ -1015,7 +1063,7 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
       // no speculative iteration in the stream: finalise column mm-1 with
       // one dot sweep of y_mm against q_0..q_{mm-1}
       (dot16 ? dcgs2_dot_kernel<16, false> : dcgs2_dot_kernel<8, false>)<<<G, kThreads, 0, s>>>(
-          n, mm, vbase, ld, nullptr, ws.red, st, dc);
+          n, mm, vbase, ld, nullptr, ws.red, st, dc, 0);
       ctx->launches++;
     }
     backsolve_kernel<<<1, 32, 0, s>>>(st, mm);
@@ -1052,6 +1100,232 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   }
   res.history.push_back(last_true);
   res.final_true = last_true;
+  MSCG_CUDA(cudaStreamSynchronize(s));
+  res.seconds = std::chrono::duration<double>(clk::now() - t0).count();
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// Distributed right-preconditioned GMRES over preconditioner shards (SURVEY
+// 8(e)): rank r owns the interior rows [lo, hi) of its blocks; every Krylov
+// vector is stored compact, [own interior rows | interface], the interface
+// part replicated (every rank computes it from the same all-reduced
+// numbers, so the copies stay bit-identical).  Per iteration:
+//   operator   apply_shard_begin -> all-reduce t (n_g) -> apply_shard_end;
+//              spmv_shard -> all-reduce the interface rows (n_g)
+//   DCGS2      sweep 1 local dots -> all-reduce (2j+2) -> fix (one CTA);
+//              sweep 2 local sum of squares -> all-reduce (1) -> rotation
+// Dots and norms count the interface rows on rank 0 only.  `comm.sum`
+// reduces in stream order (the caller's all-reduce runs on the context
+// stream: NCCL, or gloo on CUDA tensors).
+GmresResult gmres_shard(Ctx* ctx, Precond* sh, const double* b_glob, double* x_glob,
+                        const GmresConfig& cfg, const DistComm& comm) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  if (!sh || !sh->shard.on) throw Error(1, "gmres_shard: not a shard preconditioner");
+  if (cfg.left) throw Error(1, "gmres_shard: right preconditioning only");
+  if (cfg.orth != 2) throw Error(1, "gmres_shard: DCGS2 orthogonalisation only");
+  if (cfg.restart < 1 || !(cfg.rel_tol > 0.0) || cfg.max_iters < 1)
+    throw Error(1, "gmres: bad solver configuration");
+  if (cfg.restart > kMaxRestart) throw Error(1, "gmres: restart above 500 is not supported");
+  const int n = sh->n, p = sh->p, ng = n - p;
+  const int lo = sh->shard.row_lo, hi = sh->shard.row_hi, own = hi - lo;
+  const int nl = own + ng, n_dot = own + (comm.rank == 0 ? ng : 0);
+  const int m = cfg.restart;
+  if (comm.cap < std::max(2 * m + 4, std::max(ng, 1)))
+    throw Error(1, "gmres_shard: communication buffer too small");
+  cudaStream_t s = ctx->stream;
+  GmresResult res;
+  Workspace ws(ctx, std::max(nl, 1), 2 * m + 4);
+  const int G = ws.grid();
+  const size_t ld = (static_cast<size_t>(nl) + 31) & ~static_cast<size_t>(31);
+  DevBuf V(sizeof(double) * ld * (m + 1)), w(sizeof(double) * ld), tmp(sizeof(double) * ld),
+      bc(sizeof(double) * ld), xc(sizeof(double) * ld);
+  DevBuf gy(sizeof(double) * n), gx(sizeof(double) * n), gw(sizeof(double) * n),
+      tpart(sizeof(double) * std::max(1, ng)), y2p(sizeof(double) * std::max(1, ng));
+  DevBuf small(sizeof(double) * (static_cast<size_t>(m + 1) * m + 4 * (m + 1) + 64));
+  double* sp = small.as<double>();
+  Small st;
+  st.m = m;
+  st.H = sp;
+  st.cs = st.H + static_cast<size_t>(m + 1) * m;
+  st.sn = st.cs + (m + 1);
+  st.g = st.sn + (m + 1);
+  st.y = st.g + (m + 1);
+  st.scal = st.y + (m + 1);
+  st.status = st.scal + 16;
+  const size_t ldh = static_cast<size_t>(m + 1);
+  DevBuf dstate(sizeof(double) * (ldh * m + (2 * m + 4) + (2 * m + 8) + (m + 2)));
+  Dcgs dc{};
+  dc.Hraw = dstate.as<double>();
+  dc.dots = dc.Hraw + ldh * m;
+  dc.coef = dc.dots + (2 * m + 4);
+  dc.nu = dc.coef + (2 * m + 8);
+  MSCG_CUDA(cudaMemsetAsync(dstate.p, 0, dstate.bytes, s));
+  MSCG_CUDA(cudaMemsetAsync(small.p, 0, small.bytes, s));
+  MSCG_CUDA(cudaMemsetAsync(gy.p, 0, gy.bytes, s));
+  MSCG_CUDA(cudaMemsetAsync(gx.p, 0, gx.bytes, s));
+  MSCG_CUDA(cudaMemsetAsync(gw.p, 0, gw.bytes, s));
+  const char* dot16_env = std::getenv("MSCG_DOT16");
+  const bool dot16 = dot16_env ? dot16_env[0] == '1' : G >= 4 * ctx->sm_count;
+
+  auto sum = [&](double* d, int count) {  // all-reduce in stream order
+    if (comm.size <= 1 || count <= 0) return;
+    MSCG_CUDA(cudaMemcpyAsync(comm.buf, d, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+    comm.allreduce(count, comm.user);
+    MSCG_CUDA(cudaMemcpyAsync(d, comm.buf, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+  };
+  auto to_global = [&](const double* c, double* g) {
+    if (own) MSCG_CUDA(cudaMemcpyAsync(g + lo, c, sizeof(double) * own, cudaMemcpyDeviceToDevice, s));
+    if (ng) MSCG_CUDA(cudaMemcpyAsync(g + p, c + own, sizeof(double) * ng, cudaMemcpyDeviceToDevice, s));
+  };
+  auto from_global = [&](const double* g, double* c) {
+    if (own) MSCG_CUDA(cudaMemcpyAsync(c, g + lo, sizeof(double) * own, cudaMemcpyDeviceToDevice, s));
+    if (ng) MSCG_CUDA(cudaMemcpyAsync(c + own, g + p, sizeof(double) * ng, cudaMemcpyDeviceToDevice, s));
+  };
+  auto op_a = [&](const double* xin, double* yout) {  // yout = C xin (compact)
+    to_global(xin, gx.as<double>());
+    sh->spmv_shard(gx.as<double>(), gw.as<double>(), y2p.as<double>(), comm.rank == 0, s);
+    sum(y2p.as<double>(), ng);
+    if (own) MSCG_CUDA(cudaMemcpyAsync(yout, gw.as<double>() + lo, sizeof(double) * own, cudaMemcpyDeviceToDevice, s));
+    if (ng) MSCG_CUDA(cudaMemcpyAsync(yout + own, y2p.p, sizeof(double) * ng, cudaMemcpyDeviceToDevice, s));
+  };
+  auto op_minv = [&](const double* yin, double* xout) {  // xout = B^-1 yin (compact)
+    to_global(yin, gy.as<double>());
+    sh->apply_shard_begin(gy.as<double>(), tpart.as<double>(), s);
+    sum(tpart.as<double>(), ng);
+    sh->apply_shard_end(gy.as<double>(), tpart.as<double>(), gx.as<double>(), s);
+    from_global(gx.as<double>(), xout);
+  };
+  auto norm = [&](const double* x, double* slot) {  // global 2-norm, device slot + host value
+    sumsq_kernel<<<G, kThreads, 0, s>>>(n_dot, x, ws.red, slot);
+    ctx->launches++;
+    sum(slot, 1);
+    sqrt_kernel<<<1, 1, 0, s>>>(slot);
+    double h = 0;
+    MSCG_CUDA(cudaMemcpyAsync(&h, slot, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MSCG_CUDA(cudaStreamSynchronize(s));
+    return h;
+  };
+  struct HostStatus {
+    double* p = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~HostStatus() {
+      if (p) cudaFreeHost(p);
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+    }
+  } hs;
+  MSCG_CUDA(cudaMallocHost(&hs.p, 8 * sizeof(double)));
+  for (auto& e : hs.ev) MSCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+  from_global(b_glob, bc.as<double>());
+  fill_kernel<<<G, kThreads, 0, s>>>(nl, 0.0, xc.as<double>());
+  ctx->launches++;
+  const double norm_b = norm(bc.as<double>(), st.scal + 2);
+  auto finish_x = [&] {
+    MSCG_CUDA(cudaMemsetAsync(x_glob, 0, sizeof(double) * n, s));
+    to_global(xc.as<double>(), x_glob);
+  };
+  if (norm_b == 0.0) {
+    res.converged = true;
+    res.history.push_back(0.0);
+    finish_x();
+    MSCG_CUDA(cudaStreamSynchronize(s));
+    res.seconds = std::chrono::duration<double>(clk::now() - t0).count();
+    return res;
+  }
+  const double denom = norm_b;
+  auto true_res = [&]() {
+    op_a(xc.as<double>(), w.as<double>());
+    sub2_kernel<<<G, kThreads, 0, s>>>(nl, bc.as<double>(), w.as<double>(), tmp.as<double>());
+    ctx->launches++;
+    return norm(tmp.as<double>(), st.scal + 4) / norm_b;
+  };
+  double last_true = 1.0, prev_cycle_true = -1.0;
+  bool done = false;
+  double* vbase = V.as<double>();
+  while (!done) {
+    op_a(xc.as<double>(), w.as<double>());  // r = b - A x into slot 0 (unnormalised y_0)
+    sub2_kernel<<<G, kThreads, 0, s>>>(nl, bc.as<double>(), w.as<double>(), vbase);
+    ctx->launches++;
+    const double beta = norm(vbase, st.scal + 1);
+    const double rel0 = beta / denom;
+    if (res.history.empty()) res.history.push_back(rel0);
+    if (rel0 <= cfg.rel_tol) {
+      last_true = true_res();
+      res.converged = last_true <= cfg.rel_tol;
+      break;
+    }
+    init_cycle_kernel<<<1, 128, 0, s>>>(st, st.scal + 1, dc.nu);
+    MSCG_CUDA(cudaMemsetAsync(dc.Hraw, 0, sizeof(double) * ldh * m, s));
+    ctx->launches++;
+    int mm = 0;
+    bool breakdown = false, inner_conv = false;
+    auto enqueue_iteration = [&](int j) {
+      double* vj = vbase + ld * j;
+      op_minv(vj, tmp.as<double>());
+      op_a(tmp.as<double>(), w.as<double>());
+      (dot16 ? dcgs2_dot_kernel<16, true> : dcgs2_dot_kernel<8, true>)<<<G, kThreads, 0, s>>>(
+          n_dot, j, vbase, ld, w.as<double>(), ws.red, st, dc, 1);
+      sum(dc.dots, 2 * j + 2);
+      dcgs2_fix_kernel<<<1, kThreads, 0, s>>>(st, dc, j, 0);
+      dcgs2_axpy_kernel<<<G, kThreads, 0, s>>>(nl, j, vbase, ld, w.as<double>(), st, dc, ws.red,
+                                               denom, n_dot, 1);
+      sum(dc.nu + j + 1, 1);
+      dcgs2_prelim_kernel<<<1, kThreads, 0, s>>>(st, dc, j, denom);
+      ctx->launches += 4;
+      MSCG_CUDA(cudaMemcpyAsync(hs.p + 4 * (j & 1), st.status, 3 * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+      MSCG_CUDA(cudaEventRecord(hs.ev[j & 1], s));
+    };
+    const int jmax = std::min(m, cfg.max_iters - res.iterations);
+    if (jmax > 0) enqueue_iteration(0);
+    for (int j = 0; j < jmax; ++j) {
+      if (j + 1 < jmax) enqueue_iteration(j + 1);
+      MSCG_CUDA(cudaEventSynchronize(hs.ev[j & 1]));
+      const double* status = hs.p + 4 * (j & 1);
+      breakdown = status[1] != 0.0;
+      ++res.iterations;
+      mm = j + 1;
+      const double rel = status[0];
+      res.history.push_back(rel);
+      if (breakdown || rel <= cfg.rel_tol) {
+        inner_conv = rel <= cfg.rel_tol;
+        break;
+      }
+    }
+    if (mm > 0 && mm >= jmax) {
+      (dot16 ? dcgs2_dot_kernel<16, false> : dcgs2_dot_kernel<8, false>)<<<G, kThreads, 0, s>>>(
+          n_dot, mm, vbase, ld, nullptr, ws.red, st, dc, 1);
+      sum(dc.dots, 2 * mm + 2);
+      dcgs2_fix_kernel<<<1, kThreads, 0, s>>>(st, dc, mm, 1);
+      ctx->launches += 2;
+    }
+    backsolve_kernel<<<1, 32, 0, s>>>(st, mm);
+    combine_kernel<<<G, kThreads, 0, s>>>(nl, mm, vbase, ld, st.y, w.as<double>());
+    ctx->launches += 2;
+    op_minv(w.as<double>(), tmp.as<double>());
+    axpy1_kernel<<<G, kThreads, 0, s>>>(nl, tmp.as<double>(), xc.as<double>());
+    ctx->launches++;
+    last_true = true_res();
+    if (last_true <= cfg.rel_tol) {
+      res.converged = true;
+      done = true;
+    } else if (breakdown || res.iterations >= cfg.max_iters) {
+      res.converged = false;
+      done = true;
+    } else if (inner_conv) {
+      if (prev_cycle_true >= 0.0 && last_true >= 0.999 * prev_cycle_true) {
+        res.converged = false;
+        done = true;
+      }
+    }
+    prev_cycle_true = last_true;
+  }
+  res.history.push_back(last_true);
+  res.final_true = last_true;
+  finish_x();
   MSCG_CUDA(cudaStreamSynchronize(s));
   res.seconds = std::chrono::duration<double>(clk::now() - t0).count();
   return res;

@@ -395,5 +395,18 @@ struct GmresResult {
 GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b_dev,
                   double* x_dev, const GmresConfig& cfg);
 double true_residual(Ctx* ctx, const DevCsr& a, const double* x_dev, const double* b_dev);
+// Distributed GMRES over preconditioner shards (one rank per process):
+// comm.allreduce(count, user) must sum buf[0:count] over the ranks in stream
+// order on the context stream.  b, x: global-length device vectors (x gets
+// the rank's own interior rows and the interface; other rows zero).
+struct DistComm {
+  int rank = 0, size = 1;
+  double* buf = nullptr;
+  int cap = 0;
+  void (*allreduce)(int count, void* user) = nullptr;
+  void* user = nullptr;
+};
+GmresResult gmres_shard(Ctx* ctx, Precond* shard, const double* b_dev, double* x_dev,
+                        const GmresConfig& cfg, const DistComm& comm);
 
 }  // namespace mscg

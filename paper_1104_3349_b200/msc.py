@@ -577,6 +577,50 @@ class PreconditionerShard:
                                                  C.c_void_p(y2part.data_ptr()),
                                                  int(with_interface_block), C.byref(st)), st)
 
+    def gmres(self, b, cfg: "SolverConfig", rank: int, world: int, group=None):
+        """Distributed right-preconditioned GMRES (DCGS2) across the ranks'
+        shards; every rank calls it with the same global-length b (numpy or a
+        CUDA float64 tensor).  Returns (x, SolveReport): x global-length with
+        this rank's interior rows and the interface filled (others zero).
+        The exchanges run through torch.distributed.all_reduce on `group`,
+        ordered on the context stream (bound to torch's current stream)."""
+        import torch
+        import torch.distributed as dist
+        if cfg.side != "right" or cfg.orth != "dcgs2":
+            raise ValueError("gmres_shard: right preconditioning with DCGS2 only")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        cap = max(2 * cfg.restart + 4, self.n_g, 8)
+        buf = torch.zeros(cap, dtype=torch.float64, device=dev)
+        prev = self.ctx.stream_handle
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+
+        def _reduce(count, _user):
+            dist.all_reduce(buf[:count], group=group)
+
+        cb = api.ALLREDUCE_FN(_reduce)
+        pb, mem, keep, is_t = _vec_args(b, self.n)
+        if is_t:
+            x = torch.zeros(self.n, dtype=torch.float64, device=b.device)
+            px = C.c_void_p(x.data_ptr())
+        else:
+            x = np.zeros(self.n)
+            px = _ptr(x)
+        c = api.GmresConfig(cfg.restart, cfg.max_iters, cfg.rel_tol, 0, _ORTH[cfg.orth])
+        rep = api.GmresReport()
+        hcap = cfg.max_iters + 64
+        hist = np.empty(hcap)
+        st = api.Status()
+        try:
+            _check(api.lib().mscg_gmres_shard(self.ctx.h, self.h, rank, world, pb, px, mem,
+                                              C.byref(c), C.c_void_p(buf.data_ptr()), cap, cb,
+                                              None, C.byref(rep), _ptr(hist), hcap,
+                                              C.byref(st)), st)
+        finally:
+            self.ctx.set_stream(prev if prev else None)
+        return x, SolveReport(iterations=rep.iterations, converged=bool(rep.converged),
+                              residual_history=hist[: rep.history_len].tolist(),
+                              solve_seconds=rep.solve_seconds)
+
     def __del__(self):
         if getattr(self, "h", None):
             api.lib().mscg_precond_destroy(self.h)
