@@ -117,6 +117,16 @@ int mscg_problem_from_csr(int n, const int *rp, const int *ci, const double *v,
                           int p, int nranges, const int *ranges,
                           mscg_problem **out, mscg_status *st);
 void mscg_problem_destroy(mscg_problem *pb);
+/* nested_dissection(build_graph(A), target) (graph.cpp:8-30,178-230) of the
+ * pattern of a square CSR matrix, on the device (ctx) or the host (ctx NULL,
+ * `threads` workers): perm[n] = forward permutation (blocks in depth-first
+ * leaf order, each ascending, then the ascending separator), *nblocks, and
+ * ranges[2*cap] the block ranges.  Identical to the reference.  (The Oseen
+ * problem builders use it inside partition_saddle; mscg_problem_oseen_device
+ * runs it on the device.) */
+int mscg_nested_dissection(mscg_ctx *ctx, int n, const int *rp, const int *ci, int target,
+                           int threads, int *perm, int *nblocks, int *ranges, int cap,
+                           mscg_status *st);
 void mscg_problem_dims(const mscg_problem *pb, int *n, int *p, int *nblocks,
                        int64_t *nnz_c, int *separator_size);
 /* which: 0 = C (final numbering), 5 = S^ (after mscg_problem_build_schur).

@@ -35,6 +35,7 @@
 
 #include "msc/aggregates.hpp"
 #include "msc/factorization.hpp"
+#include "msc/graph.hpp"
 #include "msc/gmres.hpp"
 #include "msc/matrix_market.hpp"
 #include "msc/oseen.hpp"
@@ -366,6 +367,27 @@ int ref_build_schur(RefProblem* p, const char* variant, int mode, int sz,
     p->schur = build_msc(p->pm, p->agg, v, workers);
     p->have_schur = true;
   });
+}
+
+// nested_dissection(build_graph(A), target) (graph.cpp:8-30,178-230) of the
+// pattern of a CSR matrix: forward permutation (blocks, then separator) and
+// the block ranges (ranges[2*cap]); returns the block count or -1.
+int ref_nested_dissection(int n, const int* rp, const int* ci, int target, int* perm,
+                          int* ranges, int cap) {
+  int nb = -1;
+  if (guarded([&] {
+    std::vector<double> v(rp[n], 1.0);
+    AdjacencyGraph g = build_graph(csr_from_arrays(n, n, rp, ci, v.data()));
+    SeparatorPartition part = nested_dissection(g, target);
+    for (int i = 0; i < n; ++i) perm[i] = part.permutation.forward[i];
+    nb = static_cast<int>(part.block_ranges.size());
+    for (int b = 0; b < nb && b < cap; ++b) {
+      ranges[2 * b] = part.block_ranges[b].first;
+      ranges[2 * b + 1] = part.block_ranges[b].second;
+    }
+  }))
+    return -1;
+  return nb;
 }
 
 // overlap width used by the next ref_build_schur of an overlapped variant

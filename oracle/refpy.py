@@ -58,6 +58,8 @@ def lib():
         L.ref_get_perm.argtypes = [vp, _i32p]
         L.ref_get_scaled_rhs.argtypes = [vp, _f64p]
         L.ref_get_d_ranges.argtypes = [vp, _i32p]
+        L.ref_nested_dissection.argtypes = [C.c_int, _i32p, _i32p, C.c_int, _i32p, _i32p, C.c_int]
+        L.ref_nested_dissection.restype = C.c_int
         L.ref_set_overlap.argtypes = [vp, C.c_int]
         L.ref_set_overlap.restype = None
         L.ref_build_schur.argtypes = [vp, C.c_char_p, C.c_int, C.c_int, C.c_int,
@@ -415,6 +417,19 @@ class Problem:
                                C.byref(secs)))
         return dict(x=x, iterations=its.value, converged=bool(conv.value),
                     history=hist[: nh.value].copy(), seconds=secs.value)
+
+
+def nested_dissection(rp, ci, target):
+    """The reference's nested_dissection(build_graph(A), target) of a CSR
+    pattern: (forward permutation, block ranges)."""
+    n = len(rp) - 1
+    perm = np.empty(n, np.int32)
+    cap = max(1, 2 * target + 2)
+    ranges = np.empty(2 * cap, np.int32)
+    nb = lib().ref_nested_dissection(n, np.ascontiguousarray(rp, np.int32),
+                                     np.ascontiguousarray(ci, np.int32), target, perm, ranges, cap)
+    _check(0 if nb >= 0 else -1)
+    return perm, ranges[: 2 * nb].reshape(-1, 2)
 
 
 def time_block_solves(factors, rhs, reps, workers):

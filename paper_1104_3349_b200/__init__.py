@@ -27,6 +27,7 @@ from .msc import (  # noqa: F401
     load_matrix_market,
     load_vector_market,
     matvec,
+    nested_dissection,
     oseen_problem,
     partitioned_problem,
     true_residual,

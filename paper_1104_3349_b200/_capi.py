@@ -119,6 +119,8 @@ _SIGS = {
     "mscg_gmres_shard": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_int,
                                    C.POINTER(GmresConfig), vp, C.c_int, vp, vp,
                                    C.POINTER(GmresReport), vp, C.c_int, C.POINTER(Status)]),
+    "mscg_nested_dissection": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, C.c_int, vp,
+                                         C.POINTER(C.c_int), vp, C.c_int, C.POINTER(Status)]),
     "mscg_precond_nnz": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "mscg_precond_use_correction": (C.c_int, [vp, C.c_int]),
     "mscg_precond_layout_bytes": (C.c_int, [vp, C.POINTER(C.c_int64)]),

@@ -233,12 +233,57 @@ int mscg_problem_oseen_device(mscg_ctx* ctx, int grid_n, double nu, int stretche
                                   sys.C.v, sys.rhs, sys.p);
     }
     sys.C.nrows = sys.C.ncols = static_cast<int>(sys.C.rp.size()) - 1;
-    pb->pm = mscg::host::partition_saddle(sys.C, sys.p, n_a, threads);
+    // nested dissection on the device too;
+    // MSCG_DISSECT=host keeps the host version (comparisons)
+    static const bool host_nd = [] {
+      const char* e = getenv("MSCG_DISSECT");
+      return e && std::string(e) == "host";
+    }();
+    mscg::host::Dissector nd;
+    if (!host_nd)
+      nd = [&](int gn, const int64_t* off, const int* adj, int target,
+               std::vector<std::vector<int>>& blocks, std::vector<int>& sep) {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        mscg::nested_dissection_device(&ctx->ctx, gn, off, adj, target, blocks, sep);
+      };
+    pb->pm = mscg::host::partition_saddle(sys.C, sys.p, n_a, threads, nd);
     if (anchored) mscg::host::anchor_interface(pb->pm);
     pb->scaled_rhs.resize(sys.rhs.size());
     for (size_t k = 0; k < sys.rhs.size(); ++k) pb->scaled_rhs[k] = sys.rhs[pb->pm.perm[k]];
     flatten(pb->pm.d_ranges, pb->d_ranges_flat);
     *out = pb.release();
+  });
+}
+
+int mscg_nested_dissection(mscg_ctx* ctx, int n, const int* rp, const int* ci, int target,
+                           int threads, int* perm, int* nblocks, int* ranges, int cap,
+                           mscg_status* st) {
+  return guard(st, [&] {
+    if (n < 0 || !rp || !perm || !nblocks) throw std::invalid_argument("nested_dissection: bad arguments");
+    std::vector<int64_t> off;
+    std::vector<int> adj;
+    mscg::host::undirected_graph(n, rp, ci, off, adj);
+    std::vector<std::vector<int>> blocks;
+    std::vector<int> sep;
+    if (ctx) {
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      mscg::nested_dissection_device(&ctx->ctx, n, off.data(), adj.data(), target, blocks, sep);
+    } else {
+      if (target < 1 || target > std::max(n, 1))
+        throw std::invalid_argument("nested_dissection: target_blocks out of range");
+      mscg::host::nested_dissection_host(n, off.data(), adj.data(), target, threads, blocks, sep);
+    }
+    int w = 0, b = 0;
+    for (const auto& blk : blocks) {
+      if (ranges && b < cap) {
+        ranges[2 * b] = w;
+        ranges[2 * b + 1] = w + static_cast<int>(blk.size());
+      }
+      for (int u : blk) perm[w++] = u;
+      ++b;
+    }
+    for (int u : sep) perm[w++] = u;
+    *nblocks = b;
   });
 }
 

@@ -358,6 +358,14 @@ std::unique_ptr<Precond> build_precond(Ctx* ctx, int n, int p, const int* c_rp,
 // bit-identical to the reference.  Throws Error(SINGULAR) naming the first
 // aggregate whose D block is singular.
 constexpr int kMscMscn = 0, kMscMscnr = 1, kMscLum = 2;
+// nested_dissection (proj/src/graph.cpp:178-230) of an undirected graph
+// (CSR, sorted adjacency, no self loops) on the device: blocks in the
+// reference's depth-first leaf order (each ascending) and the sorted
+// separator, identical to the reference (csrc/device/dissect.cu).
+void nested_dissection_device(Ctx* ctx, int n, const int64_t* off, const int* adj,
+                              int target_blocks, std::vector<std::vector<int>>& blocks,
+                              std::vector<int>& separator);
+
 // ranges: owned ranges; spans: each aggregate's working range (= ranges,
 // or extended into the next aggregate for the overlapped variants, whose
 // banded S^ is merged on the host in the reference's order).

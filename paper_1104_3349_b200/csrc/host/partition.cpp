@@ -282,7 +282,53 @@ void nested_dissection(const Graph& g, int target_blocks, int threads,
 
 }  // namespace
 
-Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads) {
+void nested_dissection_host(int n, const int64_t* off, const int* adj, int target_blocks,
+                            int threads, std::vector<std::vector<int>>& blocks,
+                            std::vector<int>& separator) {
+  Graph g;
+  g.n = n;
+  g.off.assign(off, off + n + 1);
+  g.adj.assign(adj, adj + off[n]);
+  nested_dissection(g, target_blocks, threads <= 0 ? hardware_threads() : threads, blocks,
+                    separator);
+}
+
+void undirected_graph(int n, const int* rp, const int* ci, std::vector<int64_t>& off,
+                      std::vector<int>& adj) {
+  // build_graph (graph.cpp:8-30) as the reference computes it: node i's list
+  // is its own off-diagonal row pattern plus the rows j > i that list i.
+  // (The reference assigns undirected[i] = out[i] at step i, overwriting the
+  // entries earlier rows pushed, so the "undirected" lists are symmetric only
+  // for structurally symmetric patterns — such as the saddle systems here.)
+  std::vector<int64_t> cnt(n + 1, 0);
+  for (int i = 0; i < n; ++i)
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] != i) {
+        ++cnt[i + 1];
+        if (ci[k] < i) ++cnt[ci[k] + 1];
+      }
+  for (int i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int> raw(cnt[n]);
+  std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+  for (int i = 0; i < n; ++i)
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] != i) {
+        raw[pos[i]++] = ci[k];
+        if (ci[k] < i) raw[pos[ci[k]]++] = i;
+      }
+  off.assign(n + 1, 0);
+  adj.clear();
+  for (int i = 0; i < n; ++i) {
+    auto b = raw.begin() + cnt[i], e = raw.begin() + cnt[i + 1];
+    std::sort(b, e);
+    e = std::unique(b, e);
+    adj.insert(adj.end(), b, e);
+    off[i + 1] = static_cast<int64_t>(adj.size());
+  }
+}
+
+Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads,
+                             const Dissector& dissect) {
   if (c.nrows != c.ncols || p < 1 || p > c.nrows)
     throw std::invalid_argument("partition_saddle: bad split");
   if (threads <= 0) threads = hardware_threads();
@@ -378,7 +424,10 @@ Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads
             std::chrono::duration<double>(tg - t_start).count());
   std::vector<std::vector<int>> blocks;
   std::vector<int> separator;
-  nested_dissection(g, target_blocks, threads, blocks, separator);
+  if (dissect)
+    dissect(g.n, g.off.data(), g.adj.data(), target_blocks, blocks, separator);
+  else
+    nested_dissection(g, target_blocks, threads, blocks, separator);
   const auto tn = std::chrono::steady_clock::now();
 
   // Second-block unknowns follow their interior couplings

@@ -4,6 +4,8 @@
 // reproduced bit-identically so that GPU and CPU see the same matrix").
 #pragma once
 
+#include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -47,7 +49,24 @@ struct Partitioned {
 // proj/src/partitioned_matrix.cpp:71-203 with nested_dissection
 // (proj/src/graph.cpp:136-230).  `threads` <= 0 picks the hardware count;
 // the result does not depend on it.
-Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads = 0);
+// `dissect` (optional) replaces the host nested dissection of the enriched
+// graph (CSR with sorted adjacency): the device version
+// (csrc/device/dissect.cu) plugs in here; the result must be the reference's
+// blocks (depth-first order, each ascending) and sorted separator.
+using Dissector = std::function<void(int n, const int64_t* off, const int* adj, int target,
+                                     std::vector<std::vector<int>>& blocks,
+                                     std::vector<int>& separator)>;
+Partitioned partition_saddle(const Csr& c, int p, int target_blocks, int threads = 0,
+                             const Dissector& dissect = {});
+
+// nested_dissection (graph.cpp:178-230) on the host (level-parallel) of an
+// undirected graph in CSR (sorted adjacency, no self loops), and build_graph
+// (graph.cpp:8-30) of a square CSR pattern.
+void nested_dissection_host(int n, const int64_t* off, const int* adj, int target_blocks,
+                            int threads, std::vector<std::vector<int>>& blocks,
+                            std::vector<int>& separator);
+void undirected_graph(int n, const int* rp, const int* ci, std::vector<int64_t>& off,
+                      std::vector<int>& adj);
 
 // SURVEY.md §8(d) interface anchoring: each interface pressure with an
 // interface-velocity neighbour is moved directly after its smallest-index

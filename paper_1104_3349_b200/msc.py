@@ -504,6 +504,24 @@ def oseen_problem(grid_n, nu, n_a, stretched=False, stretch=1.056, anchored=Fals
     return Problem(h)
 
 
+def nested_dissection(a: SparseMatrix, target_blocks: int, ctx: "Context | None" = None,
+                      threads: int = 0):
+    """nested_dissection(build_graph(a), target_blocks) (graph.cpp:178-230):
+    (forward permutation, block ranges) — on the device with a context, else
+    on the host; identical to the reference either way."""
+    rp, ci, _ = a.arrays()
+    n = a.nrows
+    perm = np.empty(max(n, 1), np.int32)
+    cap = 2 * max(1, target_blocks) + 2
+    ranges = np.empty(2 * cap, np.int32)
+    nb = C.c_int()
+    st = api.Status()
+    _check(api.lib().mscg_nested_dissection(ctx.h if ctx is not None else None, n, _ptr(rp),
+                                            _ptr(ci), target_blocks, threads, _ptr(perm),
+                                            C.byref(nb), _ptr(ranges), cap, C.byref(st)), st)
+    return perm[:n], ranges[: 2 * min(nb.value, cap)].reshape(-1, 2)
+
+
 def partitioned_problem(c: SparseMatrix, p: int, d_ranges=()) -> Problem:
     """PartitionedMatrix::from_split(C, p, d_ranges)."""
     rp, ci, v = c.arrays()

@@ -776,3 +776,44 @@ def test_overlapped_band_singular_error(msc, ctx, ref):
     assert str(e.value) == ("build_preconditioner: overlapped Schur band: dense_lu: zero pivot "
                             "at index 3")
     assert e.value.pivot_index == 3
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_nested_dissection_device_matches_reference(msc, ctx, ref, seed):
+    """Nested dissection on the device (csrc/device/dissect.cu, SURVEY 8(f)
+    row 2): random patterns with disconnected pieces, isolated nodes and
+    nonsymmetric rows, plus grid graphs — the reference's permutation and
+    block ranges exactly."""
+    from test_host_setup import _random_pattern
+    rng = np.random.default_rng(100 + seed)
+    cases = []
+    for _ in range(12):
+        n = int(rng.integers(3, 2000))
+        cases.append((_random_pattern(msc, rng, n, int(rng.integers(1, 4)),
+                                      int(rng.integers(1, 6)), bool(rng.integers(0, 2))),
+                      int(rng.integers(1, min(n, 256) + 1))))
+    m = 40 + seed
+    g = np.zeros((m * m, m * m))
+    for i in range(m):
+        for j in range(m):
+            u = i * m + j
+            if i + 1 < m:
+                g[u, u + m] = g[u + m, u] = 1
+            if j + 1 < m:
+                g[u, u + 1] = g[u + 1, u] = 1
+    cases.append((msc.SparseMatrix.from_dense(g), 64))
+    for A, target in cases:
+        p_ref, r_ref = ref.nested_dissection(A.row_offsets, A.col_indices, target)
+        p, r = msc.nested_dissection(A, target, ctx=ctx)
+        assert np.array_equal(p, p_ref) and np.array_equal(r, r_ref), (A.nrows, target)
+
+
+def test_device_partition_cfg4_digest(msc, ctx):
+    """cfg4 (1024^2, 1024 blocks, anchored) through the device problem path
+    (device assembly + device nested dissection): C and the permutation
+    equal the reference's digests (tests/golden/cfg4.json)."""
+    js = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg4.json")))
+    P = msc.oseen_problem(1024, 0.001, 1024, anchored=True, ctx=ctx)
+    from test_host_setup import csr_digest, digest
+    assert csr_digest(P.C) == js["c_sha"]
+    assert digest(P.perm().astype("<i4")) == js["perm_sha"]

@@ -180,3 +180,35 @@ def test_overlapped_aggregate_errors(msc):
         P.build_msc("omscn", widths=[ng] + [0] * (k - 1))
     with pytest.raises(ValueError, match="one width per aggregate"):
         P.build_msc("omscn", widths=[0])
+
+
+def _random_pattern(msc, rng, n, deg, comps, symmetric):
+    """Random sparse pattern with `comps` groups (disconnected pieces) and
+    isolated nodes; nonsymmetric unless asked."""
+    a = np.zeros((n, n))
+    lab = rng.integers(0, comps, n)
+    for i in range(n):
+        for _ in range(deg):
+            j = rng.integers(0, n)
+            if lab[j] == lab[i]:
+                a[i, j] = 1.0
+    if symmetric:
+        a = a + a.T
+    return msc.SparseMatrix.from_dense(a + np.eye(n))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_nested_dissection_host_matches_reference(msc, ref, seed):
+    """nested_dissection(build_graph(A), target) (graph.cpp:8-30,178-230) on
+    random patterns — disconnected pieces, isolated nodes, nonsymmetric rows
+    (the reference's build_graph keeps only later rows' in-edges) —
+    identical permutation and block ranges."""
+    rng = np.random.default_rng(seed)
+    for _ in range(25):
+        n = int(rng.integers(3, 400))
+        A = _random_pattern(msc, rng, n, int(rng.integers(1, 4)), int(rng.integers(1, 5)),
+                            bool(rng.integers(0, 2)))
+        target = int(rng.integers(1, min(n, 128) + 1))
+        p_ref, r_ref = ref.nested_dissection(A.row_offsets, A.col_indices, target)
+        p, r = msc.nested_dissection(A, target)
+        assert np.array_equal(p, p_ref) and np.array_equal(r, r_ref), (n, target)
