@@ -157,9 +157,35 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 }
 // Pass counter read: acquire when the solution is overwritten in place (the
 // U pass reuses z's slots, so a value's presence cannot mark readiness).
-template <bool kAcquire>
+// Cluster solves read the home CTA's counter through a generic (distributed
+// shared memory) address with cluster-scope acquire.
+__device__ __forceinline__ int ld_acquire_cluster(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cluster(int* p, int v) {
+  asm volatile("st.release.cluster.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <bool kAcquire, bool kRemote = false>
 __device__ __forceinline__ int poll(const int* p) {
-  return kAcquire ? ld_acquire(p) : vload(p);
+  return kAcquire ? (kRemote ? ld_acquire_cluster(p) : ld_acquire(p)) : vload(p);
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// generic address of `p` (a shared-memory location of this CTA) in CTA
+// `rank` of the cluster
+template <class T>
+__device__ __forceinline__ T* map_rank(T* p, unsigned rank) {
+  T* out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
+  return out;
 }
 
 // A vector slice [p, p + 32) copied by TMA needs 16-byte aligned ends:
@@ -182,7 +208,7 @@ __device__ __forceinline__ Slice aligned_slice(const double* p, int len) {
 // instead of per-lane loop bounds) so the final reduction runs converged.
 // The first round's loads are issued before the readiness wait (one poll
 // per warp on the tile counter).
-template <int kUnroll, bool kInPlace>
+template <int kUnroll, bool kInPlace, bool kRemote = false>
 __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
@@ -208,7 +234,7 @@ __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
       // their fast path)
       // exponential back-off: the solver finishes a tile every few
       // microseconds and short polls would steal its issue slots
-      for (unsigned s = ns; poll<kInPlace>(done) < need; s = min(2 * s, ns_max)) __nanosleep(s);
+      for (unsigned s = ns; poll<kInPlace, kRemote>(done) < need; s = min(2 * s, ns_max)) __nanosleep(s);
     }
     // Gather operands (independent shared loads); poll only if one is still
     // pending (the counter is a hint, the sentinel is the guarantee).
@@ -242,7 +268,7 @@ __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
 // (at most 32 * kUnroll).  One round of loads for all rows; each product goes
 // to the warp's shared scratch and lane r sums row r's run in entry order.
 // Returns lane r's row sum (and whether row r has entries).
-template <int kUnroll, bool kInPlace>
+template <int kUnroll, bool kInPlace, bool kRemote = false>
 __device__ __noinline__ double group_dot(const double* __restrict__ vals,
                                             const uint16_t* __restrict__ cols, int s, int e,
                                             const int* rp, int row0, int span,
@@ -260,7 +286,7 @@ __device__ __noinline__ double group_dot(const double* __restrict__ vals,
   const bool mine = lane < span;
   const int rb = mine ? __ldg(rp + row0 + lane) : 0;
   const int re = mine ? __ldg(rp + row0 + lane + 1) : 0;
-  for (unsigned sl = ns; poll<kInPlace>(done) < need; sl = min(2 * sl, ns_max)) __nanosleep(sl);
+  for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max)) __nanosleep(sl);
   const volatile double* vs = sol;
   double xv[kUnroll];
   bool pending = false;
@@ -379,12 +405,24 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
 // instead of two).  kProducer:
 // warp 1 issues the near-tile copies (the solver's issue of a bulk copy costs
 // ~400 cycles of its chain per tile) and warps 2.. are the workers.
-template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer>
+// kCluster > 1: a cluster of kCluster CTAs solves one block.  CTA 0 (home)
+// is the single-CTA kernel (solver + workers, solution and far-sum slots in
+// its shared memory); CTAs 1.. are all workers: they read the solution from
+// the home CTA's shared memory and publish their partial sums into its slots
+// through distributed shared memory (generic addresses from mapa), and poll
+// its pass counters with cluster-scope acquire.  Used when the blocks are
+// too few to fill the GPU (cfg1 / cfg2): a block's far entries then stream
+// through kCluster SMs instead of one.
+template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer,
+          int kCluster = 1>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
   constexpr int kFirstWorker = kProducer ? 2 : 1;
   constexpr int kWorkers = kWarps - kFirstWorker;
+  constexpr bool kCl = kCluster > 1;
+  // workers of the whole cluster: the home CTA's, then every warp of the others
+  constexpr int kAllWorkers = kWorkers + (kCluster - 1) * kWarps;
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                        // kRing slots: tile | meta | rhs slice
   double* part = ring + kRing * kSlotElems; // far sums, one slot per work item
@@ -397,7 +435,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   __shared__ __align__(8) uint64_t empty[kRing];  // near item consumed (producer variant)
   __shared__ int done_l, done_u;
 
-  const int b = a.order[a.pos0 + blockIdx.x];  // heaviest blocks first (LPT)
+  const unsigned crank = kCl ? cluster_rank() : 0u;
+  const bool home = crank == 0;
+  const int b = a.order[a.pos0 + blockIdx.x / kCluster];  // heaviest blocks first (LPT)
   const int n = a.dim[b], r0 = a.row0[b];
   const int nt = (n + kTile - 1) / kTile;
   const double* lt = a.ltile + a.toff[b] * kTileStride;
@@ -405,6 +445,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const double pend = pending_value();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  // Cluster: every CTA keeps its own copy of the solution and pass counters
+  // (the home solver pushes each solved tile and counter to the others over
+  // DSMEM, so workers gather locally); far sums go to the home CTA's slots.
+  double* const zh = z;
+  double* const xh = x;
+  double* parth = kCl && !home ? map_rank(part, 0) : part;
+  int* const done_lh = &done_l;
+  int* const done_uh = &done_u;
   for (int i = threadIdx.x; i < nt * kTile; i += blockDim.x) {
     // rows past the block's end read as zero by the neighbour products
     z[i] = i < n ? pend : 0.0;
@@ -421,6 +469,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if constexpr (kCl) cluster_sync_all();  // the home's sentinels are in place
 
   // Near item q: q < nt -> L tile q (+ rhs slice), else U tile 2nt-1-q.
   // Item q lives in slot q % kRing, phase (q / kRing) & 1.
@@ -459,11 +508,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
     }
   };
-  long long* tr = (a.trace && b == 0) ? a.trace : nullptr;
+  long long* tr = (a.trace && b == 0 && home) ? a.trace : nullptr;
   const int j = lane;
 
   // ================================================================ L pass
-  if (warp == 0) {
+  if (home && warp == 0) {
     if (lane == 0) {
       for (int q = 0; q < kRing && q < 2 * nt; ++q) issue(q, first_bytes(q));
       // the block's work-item lists go to L2 once
@@ -502,38 +551,47 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       double zj = valid ? tile_inverse_dot<true>(T, rbuf, j) : 0.0;
       __syncwarp();  // rbuf is rewritten by the next tile
-      if (valid) *reinterpret_cast<volatile double*>(z + i) = zj;
+      if (valid) {
+        *reinterpret_cast<volatile double*>(z + i) = zj;
+        if constexpr (kCl)
+          for (unsigned r = 1; r < kCluster; ++r)
+            *reinterpret_cast<volatile double*>(map_rank(z + i, r)) = zj;
+      }
       __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
         *reinterpret_cast<volatile int*>(&done_l) = t + 1;
+        if constexpr (kCl)
+          for (unsigned r = 1; r < kCluster; ++r)
+            *reinterpret_cast<volatile int*>(map_rank(&done_l, r)) = t + 1;
         if (tr) tr[4 * t + 2] = clock64();
         if (!kProducer && t + kRing < 2 * nt) issue(t + kRing, next_bytes(t));
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 3] = clock64();
     }
-  } else if (kProducer && warp == 1) {
+  } else if (kProducer && home && warp == 1) {
     produce(kRing, min(nt + kRing, 2 * nt));
   } else {
     // workers: far items of L rows, rows ascending
-    const int w = warp - kFirstWorker;
+    const int lw = home ? warp - kFirstWorker : warp;  // scratch slot in this CTA
+    const int w = home ? lw : kWorkers + static_cast<int>(crank - 1) * kWarps + warp;
     const double* fv = a.lval + a.loff[b];
     const uint16_t* fc = a.lcol + a.loff[b];
     const int4* items = a.litems + a.lioff[b];
     const int nitems = a.lnum[b];
     const int* rp = a.lrp + r0 + b;
-    double* scr = scratch + w * kGroupEntries;
+    double* scr = scratch + lw * kGroupEntries;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
-    if (lane < a.pf_items && w + kWorkers * lane < nitems) {  // warm the first items
-      const int4 d = items[w + kWorkers * lane];
+    if (lane < a.pf_items && w + kAllWorkers * lane < nitems) {  // warm the first items
+      const int4 d = items[w + kAllWorkers * lane];
       prefetch_far(fv, fc, d.z, d.w);
     }
-    for (int it = w; it < nitems; it += kWorkers) {
+    for (int it = w; it < nitems; it += kAllWorkers) {
       const int4 d = nxt;
-      if (it + kWorkers < nitems) nxt = items[it + kWorkers];
-      if (lane == 0 && a.pf_items && it + kWorkers * a.pf_items < nitems) {
-        const int4 f = items[it + kWorkers * a.pf_items];
+      if (it + kAllWorkers < nitems) nxt = items[it + kAllWorkers];
+      if (lane == 0 && a.pf_items && it + kAllWorkers * a.pf_items < nitems) {
+        const int4 f = items[it + kAllWorkers * a.pf_items];
         prefetch_far(fv, fc, f.z, f.w);
       }
       const int i = d.x & 0xffff, k = d.y & 0xff;
@@ -545,15 +603,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int my = lane < span ? a.lslot[r0 + i + lane] : 0;
         bool has;
         const double acc =
-            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, span, z, scr, lane,
-                                                 a.sleep_ns, &done_l, d.y >> 8, a.sleep_max, has);
+            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, span, zh, scr, lane,
+                                                 a.sleep_ns, done_lh, d.y >> 8, a.sleep_max, has);
         if (rt) rt[1] = clock64();
-        if (has) *reinterpret_cast<volatile double*>(part + my) = acc;
+        if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, z, lane, a.sleep_ns,
-                                                   &done_l, d.y >> 8, a.sleep_max);
+        const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
+                                                   done_lh, d.y >> 8, a.sleep_max);
         if (rt) rt[1] = clock64();
-        if (lane == 0) *reinterpret_cast<volatile double*>(part + slot) = acc;
+        if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
       if (rt) {
         rt[2] = clock64();
@@ -562,9 +620,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     }
   }
   __syncthreads();  // every L far sum consumed (slots pending again) before the U pass
+  if constexpr (kCl) cluster_sync_all();
 
   // ================================================================ U pass
-  if (warp == 0) {
+  if (home && warp == 0) {
     for (int tt = 0; tt < nt; ++tt) {
       const int t = nt - 1 - tt;
       const int q = nt + tt;
@@ -592,42 +651,59 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       double xj = valid ? tile_inverse_dot<false>(T, rbuf, j) : 0.0;
       __syncwarp();
-      if (valid) *reinterpret_cast<volatile double*>(x + i) = xj;
+      if (valid) {
+        *reinterpret_cast<volatile double*>(x + i) = xj;
+        if constexpr (kCl)
+          for (unsigned r = 1; r < kCluster; ++r)
+            *reinterpret_cast<volatile double*>(map_rank(x + i, r)) = xj;
+      }
       __syncwarp();
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
-        if (kInPlace)
-          st_release(&done_u, tt + 1);
-        else
+        if (kInPlace) {
+          if constexpr (kCl) {
+            // one cluster-scope fence orders the tile's pushes before every
+            // CTA's counter (its workers acquire before reading x)
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            for (unsigned r = 0; r < kCluster; ++r) {
+              int* c = r ? map_rank(&done_u, r) : &done_u;
+              asm volatile("st.relaxed.cluster.b32 [%0], %1;" ::"l"(c), "r"(tt + 1) : "memory");
+            }
+          } else {
+            st_release(&done_u, tt + 1);
+          }
+        } else {
           *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
+        }
         if (tr) tr[4 * q + 2] = clock64();
         if (!kProducer && q + kRing < 2 * nt) issue(q + kRing, next_bytes(q));
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 3] = clock64();
     }
-  } else if (kProducer && warp == 1) {
+  } else if (kProducer && home && warp == 1) {
     produce(nt + kRing, 2 * nt);
   } else {
     // workers: far items of U rows, rows descending
-    const int w = warp - kFirstWorker;
+    const int lw = home ? warp - kFirstWorker : warp;
+    const int w = home ? lw : kWorkers + static_cast<int>(crank - 1) * kWarps + warp;
     const double* fv = a.uval + a.uoff[b];
     const uint16_t* fc = a.ucol + a.uoff[b];
     const int4* items = a.uitems + a.uioff[b];
     const int nitems = a.unum[b];
     const long long lit = a.lnum[b];
     const int* rp = a.urp + r0 + b;
-    double* scr = scratch + w * kGroupEntries;
+    double* scr = scratch + lw * kGroupEntries;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
-    if (lane < a.pf_u && w + kWorkers * lane < nitems) {  // warm the first items
-      const int4 d = items[w + kWorkers * lane];
+    if (lane < a.pf_u && w + kAllWorkers * lane < nitems) {  // warm the first items
+      const int4 d = items[w + kAllWorkers * lane];
       prefetch_far(fv, fc, d.z, d.w);
     }
-    for (int it = w; it < nitems; it += kWorkers) {
+    for (int it = w; it < nitems; it += kAllWorkers) {
       const int4 d = nxt;
-      if (it + kWorkers < nitems) nxt = items[it + kWorkers];
-      if (lane == 0 && a.pf_u && it + kWorkers * a.pf_u < nitems) {
-        const int4 f = items[it + kWorkers * a.pf_u];
+      if (it + kAllWorkers < nitems) nxt = items[it + kAllWorkers];
+      if (lane == 0 && a.pf_u && it + kAllWorkers * a.pf_u < nitems) {
+        const int4 f = items[it + kAllWorkers * a.pf_u];
         prefetch_far(fv, fc, f.z, f.w);
       }
       const int i = d.x & 0xffff, k = d.y & 0xff;
@@ -638,16 +714,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int span = (k & 0x7f) + 1;
         const int my = lane < span ? a.uslot[r0 + i + lane] : 0;
         bool has;
-        const double acc =
-            group_dot<kGroupEntries / 32, kInPlace>(fv, fc, d.z, d.w, rp, i, span, x, scr, lane,
-                                                    a.sleep_ns, &done_u, d.y >> 8, a.sleep_max, has);
+        const double acc = group_dot<kGroupEntries / 32, kInPlace, kCl>(
+            fv, fc, d.z, d.w, rp, i, span, xh, scr, lane, a.sleep_ns, done_uh, d.y >> 8,
+            a.sleep_max, has);
         if (rt) rt[1] = clock64();
-        if (has) *reinterpret_cast<volatile double*>(part + my) = acc;
+        if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, x, lane, a.sleep_ns,
-                                                      &done_u, d.y >> 8, a.sleep_max);
+        const double acc = seg_dot<kUnroll, kInPlace, kCl>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
+                                                           done_uh, d.y >> 8, a.sleep_max);
         if (rt) rt[1] = clock64();
-        if (lane == 0) *reinterpret_cast<volatile double*>(part + slot) = acc;
+        if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
       if (rt) {
         rt[2] = clock64();
@@ -656,6 +732,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     }
   }
   __syncthreads();
+  // the home CTA's shared memory stays alive until every remote worker is done
+  if constexpr (kCl) cluster_sync_all();
+  if (!home) return;
   // epilogue: the block's solution leaves in one coalesced sweep
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     out[r0 + i] = sub ? sub[r0 + i] - x[i] : x[i];
@@ -785,6 +864,54 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     int dev = 0;
     MSCG_CUDA(cudaGetDevice(&dev));
     MSCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  // Fewer blocks than fill the GPU: a thread-block cluster of C CTAs (C SMs)
+  // per block — the home CTA solves, the others stream far entries into its
+  // shared memory over DSMEM (MSCG_TRI_CLUSTER=0 off, =C forces the size).
+  static const int cl_env = [] {
+    const char* e = getenv("MSCG_TRI_CLUSTER");
+    return e ? atoi(e) : -1;
+  }();
+  int ccl = 1;
+  if (variant == 0 && d > 1024 && cl_env != 0) {
+    const int fit = sms / std::max(1, npos);
+    // measured at cfg2 (16 blocks): 4 CTAs per block 0.305 ms, 8: 0.487 ms
+    // (pushes to more CTAs lengthen the chain), 1: 0.420 ms
+    for (int c : {6, 4, 3, 2})
+      if ((cl_env < 0 ? c <= std::min(fit, 4) : c == cl_env)) {
+        ccl = c;
+        break;
+      }
+  }
+  if (ccl > 1) {
+    const size_t smc = smem_bytes<true>(d, 32, ns);  // remote CTAs: 32 worker scratches
+    check_smem(smc);
+    auto go = [&](auto kern) {
+      ensure_smem(reinterpret_cast<const void*>(kern), smc);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(npos * ccl);
+      cfg.blockDim = dim3(32 * 32);
+      cfg.dynamicSmemBytes = smc;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = ccl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      MSCG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, rhs, out, sub));
+    };
+    if (ccl == 6)
+      go(trisolve_kernel<32, 4, 1, true, false, 6>);
+    else if (ccl == 4)
+      go(trisolve_kernel<32, 4, 1, true, false, 4>);
+    else if (ccl == 3)
+      go(trisolve_kernel<32, 4, 1, true, false, 3>);
+    else
+      go(trisolve_kernel<32, 4, 1, true, false, 2>);
+    MSCG_CUDA(cudaGetLastError());
+    return;
   }
   if (variant == 0 && npos <= sms && d > 1024) {
     launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
