@@ -22,7 +22,12 @@ for g, nu, na, anch in cases:
     t1 = time.perf_counter()
     pd = msc.oseen_problem(g, nu, na, anchored=anch, ctx=ctx)
     t2 = time.perf_counter()
-    same = (np.array_equal(ph.perm(), pd.perm()) and np.array_equal(ph.d_ranges(), pd.d_ranges()))
+    Ch, Cd = ph.C, pd.C
+    same = (np.array_equal(ph.perm(), pd.perm()) and np.array_equal(ph.d_ranges(), pd.d_ranges())
+            and np.array_equal(Ch.row_offsets, Cd.row_offsets)
+            and np.array_equal(Ch.col_indices, Cd.col_indices)
+            and np.array_equal(Ch.values.view(np.int64), Cd.values.view(np.int64))
+            and ph.p == pd.p)
     print(f"grid {g} n_a {na}: host {t1 - t0:.3f} s, device {t2 - t1:.3f} s, identical {same}",
           flush=True)
     if not same:
