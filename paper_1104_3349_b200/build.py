@@ -37,7 +37,7 @@ SOURCES = [
     "host/oseen.cpp", "host/partition.cpp", "host/schur.cpp", "host/mmio.cpp", "capi.cpp",
     "device/runtime.cu", "device/spmv.cu", "device/factor.cu", "device/trisolve.cu",
     "device/precond.cu", "device/correct.cu", "device/gmres.cu", "device/schur.cu", "device/oseen.cu",
-    "device/dissect.cu",
+    "device/dissect.cu", "device/partition.cu",
 ]
 HEADERS = ["host/csr.hpp", "host/setup.hpp", "device/common.cuh", "device/internal.hpp"]
 

@@ -239,15 +239,14 @@ int mscg_problem_oseen_device(mscg_ctx* ctx, int grid_n, double nu, int stretche
       const char* e = getenv("MSCG_DISSECT");
       return e && std::string(e) == "host";
     }();
-    mscg::host::Dissector nd;
-    if (!host_nd)
-      nd = [&](int gn, const int64_t* off, const int* adj, int target,
-               std::vector<std::vector<int>>& blocks, std::vector<int>& sep) {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        mscg::nested_dissection_device(&ctx->ctx, gn, off, adj, target, blocks, sep);
-      };
-    pb->pm = mscg::host::partition_saddle(sys.C, sys.p, n_a, threads, nd);
-    if (anchored) mscg::host::anchor_interface(pb->pm);
+    if (host_nd) {
+      pb->pm = mscg::host::partition_saddle(sys.C, sys.p, n_a, threads);
+      if (anchored) mscg::host::anchor_interface(pb->pm);
+    } else {
+      // the whole partition (and anchoring) on the device
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      pb->pm = mscg::partition_saddle_device(&ctx->ctx, sys.C, sys.p, n_a, anchored != 0);
+    }
     pb->scaled_rhs.resize(sys.rhs.size());
     for (size_t k = 0; k < sys.rhs.size(); ++k) pb->scaled_rhs[k] = sys.rhs[pb->pm.perm[k]];
     flatten(pb->pm.d_ranges, pb->d_ranges_flat);

@@ -601,36 +601,34 @@ __global__ void bounds_kernel(int n, const unsigned* skey, int K, int* pstart) {
   }
 }
 
+// a borrowed device array with DevBuf's accessor
+struct Borrowed {
+  const void* p;
+  template <class T> T* as() const { return static_cast<T*>(const_cast<void*>(p)); }
+};
+
 }  // namespace
 
-void nested_dissection_device(Ctx* ctx, int n, const int64_t* h_off, const int* h_adj,
-                              int target_blocks, std::vector<std::vector<int>>& blocks,
-                              std::vector<int>& separator) {
+// Core on device arrays: piece (n ints, out) = final piece id of every node
+// in depth-first leaf order, -1 for the separator; returns the piece count.
+int nested_dissection_core(Ctx* ctx, int n, const long long* d_off_p, const int* d_adj_p,
+                           int target_blocks, int* piece_out) {
+  cudaStream_t s = ctx->stream;
   if (target_blocks < 1 || target_blocks > std::max(n, 1))
     throw Error(1, "nested_dissection: target_blocks out of range");
-  blocks.clear();
-  separator.clear();
-  if (target_blocks == 1 || n <= 1) {
-    std::vector<int> all(n);
-    for (int i = 0; i < n; ++i) all[i] = i;
-    blocks.push_back(std::move(all));
-    return;
-  }
+  MSCG_CUDA(cudaMemsetAsync(piece_out, 0, sizeof(int) * std::max(n, 1), s));
+  if (target_blocks == 1 || n <= 1) return 1;
   int depth = 0;
   while ((1 << depth) < target_blocks) ++depth;
   static const bool verbose = getenv("MSCG_VERBOSE") != nullptr;
   using clk = std::chrono::steady_clock;
   auto tl = clk::now();
-  cudaStream_t s = ctx->stream;
-  const long long ne = h_off[n];
-  DevBuf d_off(sizeof(long long) * (n + 1)), d_adj(sizeof(int) * std::max<long long>(1, ne));
-  MSCG_CUDA(cudaMemcpyAsync(d_off.p, h_off, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, s));
-  if (ne) MSCG_CUDA(cudaMemcpyAsync(d_adj.p, h_adj, sizeof(int) * ne, cudaMemcpyHostToDevice, s));
-  DevBuf piece(sizeof(int) * n), dist(sizeof(int) * n), disc(sizeof(int) * n),
+  const Borrowed d_off{d_off_p}, d_adj{d_adj_p};
+  const Borrowed piece{piece_out};
+  DevBuf dist(sizeof(int) * n), disc(sizeof(int) * n),
       fa(sizeof(int) * n), fb(sizeof(int) * n), offs(sizeof(int) * n), lab(n),
       plist(sizeof(int) * n), ids(sizeof(int) * n), key(sizeof(unsigned) * n),
       skey(sizeof(unsigned) * n);
-  MSCG_CUDA(cudaMemsetAsync(piece.p, 0, sizeof(int) * n, s));
   const int G = 2 * ctx->sm_count;  // entry-chunk grid of the round kernels
   // the cooperative search: as many CTAs as are co-resident (<= kCoopMaxG)
   int Gc = 0;
@@ -797,16 +795,37 @@ void nested_dissection_device(Ctx* ctx, int n, const int64_t* h_off, const int* 
       tl = now;
     }
   }
-  // blocks: pieces in order, each ascending; separator ascending
-  DevBuf pstart(sizeof(int) * (K + 1));
-  sort_by_piece(K, pstart.as<int>());
-  std::vector<int> order(n), ps(K + 1);
-  MSCG_CUDA(cudaMemcpyAsync(order.data(), plist.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
-  MSCG_CUDA(cudaMemcpyAsync(ps.data(), pstart.p, sizeof(int) * (K + 1), cudaMemcpyDeviceToHost, s));
   MSCG_CUDA(cudaStreamSynchronize(s));
+  return K;
+}
+
+void nested_dissection_device(Ctx* ctx, int n, const int64_t* h_off, const int* h_adj,
+                              int target_blocks, std::vector<std::vector<int>>& blocks,
+                              std::vector<int>& separator) {
+  if (target_blocks < 1 || target_blocks > std::max(n, 1))
+    throw Error(1, "nested_dissection: target_blocks out of range");
+  blocks.clear();
+  separator.clear();
+  if (target_blocks == 1 || n <= 1) {
+    std::vector<int> all(n);
+    for (int i = 0; i < n; ++i) all[i] = i;
+    blocks.push_back(std::move(all));
+    return;
+  }
+  cudaStream_t s = ctx->stream;
+  const long long ne = h_off[n];
+  DevBuf d_off(sizeof(long long) * (n + 1)), d_adj(sizeof(int) * std::max<long long>(1, ne));
+  MSCG_CUDA(cudaMemcpyAsync(d_off.p, h_off, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, s));
+  if (ne) MSCG_CUDA(cudaMemcpyAsync(d_adj.p, h_adj, sizeof(int) * ne, cudaMemcpyHostToDevice, s));
+  DevBuf piece(sizeof(int) * n);
+  const int K = nested_dissection_core(ctx, n, d_off.as<long long>(), d_adj.as<int>(),
+                                       target_blocks, piece.as<int>());
+  std::vector<int> hp(n);
+  MSCG_CUDA(cudaMemcpyAsync(hp.data(), piece.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+  MSCG_CUDA(cudaStreamSynchronize(s));
+  // blocks: pieces in order, each ascending; separator ascending
   blocks.resize(K);
-  for (int k = 0; k < K; ++k) blocks[k].assign(order.begin() + ps[k], order.begin() + ps[k + 1]);
-  separator.assign(order.begin() + ps[K], order.end());
+  for (int u = 0; u < n; ++u) (hp[u] < 0 ? separator : blocks[hp[u]]).push_back(u);
 }
 
 }  // namespace mscg

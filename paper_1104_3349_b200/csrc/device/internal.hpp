@@ -41,9 +41,9 @@ struct Ctx {
   ~Ctx();
 };
 
-// Device CSR kept in SELL-32 (slices of 32 rows, column-major inside a slice)
-// so that a warp reads 32 consecutive entries per step while each lane keeps
-// the reference's row-sequential accumulation order.
+// Device CSR kept in SELL-64 (slices of 64 rows, column-major inside a
+// slice): lane r of a warp owns rows 2r, 2r+1 and reads entry k of both as one
+// 16-byte load, keeping the reference's row-sequential accumulation order.
 struct DevCsr {
   Ctx* ctx = nullptr;
   int nrows = 0, ncols = 0;

@@ -132,3 +132,14 @@ std::vector<double> load_vector_market(const std::string& path);
 void write_vector_market(const std::string& path, const double* v, int n);
 
 }  // namespace mscg::host
+
+namespace mscg {
+struct Ctx;
+// partition_saddle (Interleaved, partitioned_matrix.cpp:71-203) on the
+// device (csrc/device/partition.cu) — attached lists, enriched graph, nested
+// dissection, the second-block assignment, C' = P C P^T — and optionally
+// the SURVEY 8(d) interface anchoring: identical to host::partition_saddle
+// (+ host::anchor_interface).
+host::Partitioned partition_saddle_device(Ctx* ctx, const host::Csr& c, int p, int target_blocks,
+                                          bool anchored);
+}  // namespace mscg
