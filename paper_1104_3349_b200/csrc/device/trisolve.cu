@@ -421,8 +421,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   constexpr int kFirstWorker = kProducer ? 2 : 1;
   constexpr int kWorkers = kWarps - kFirstWorker;
   constexpr bool kCl = kCluster > 1;
-  // workers of the whole cluster: the home CTA's, then every warp of the others
-  constexpr int kAllWorkers = kWorkers + (kCluster - 1) * kWarps;
+  // workers of the whole cluster: the home CTA's, then warps 1.. of the
+  // others (warp 0 of a remote CTA pulls the solution, see below)
+  constexpr int kAllWorkers = kWorkers + (kCluster - 1) * (kWarps - 1);
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                        // kRing slots: tile | meta | rhs slice
   double* part = ring + kRing * kSlotElems; // far sums, one slot per work item
@@ -446,8 +447,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // Cluster: every CTA keeps its own copy of the solution and pass counters
-  // (the home solver pushes each solved tile and counter to the others over
-  // DSMEM, so workers gather locally); far sums go to the home CTA's slots.
+  // (warp 0 of a remote CTA pulls each solved tile from the home CTA over
+  // DSMEM, so workers gather locally and the solver's chain does no extra
+  // work); far sums go to the home CTA's slots.
   double* const zh = z;
   double* const xh = x;
   double* parth = kCl && !home ? map_rank(part, 0) : part;
@@ -551,19 +553,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       double zj = valid ? tile_inverse_dot<true>(T, rbuf, j) : 0.0;
       __syncwarp();  // rbuf is rewritten by the next tile
-      if (valid) {
-        *reinterpret_cast<volatile double*>(z + i) = zj;
-        if constexpr (kCl)
-          for (unsigned r = 1; r < kCluster; ++r)
-            *reinterpret_cast<volatile double*>(map_rank(z + i, r)) = zj;
-      }
+      if (valid) *reinterpret_cast<volatile double*>(z + i) = zj;
       __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
         *reinterpret_cast<volatile int*>(&done_l) = t + 1;
-        if constexpr (kCl)
-          for (unsigned r = 1; r < kCluster; ++r)
-            *reinterpret_cast<volatile int*>(map_rank(&done_l, r)) = t + 1;
         if (tr) tr[4 * t + 2] = clock64();
         if (!kProducer && t + kRing < 2 * nt) issue(t + kRing, next_bytes(t));
       }
@@ -572,10 +566,38 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     }
   } else if (kProducer && home && warp == 1) {
     produce(kRing, min(nt + kRing, 2 * nt));
+  } else if (kCl && !home && warp == 0) {
+    // puller: copy each tile the home solver publishes into this CTA's copy
+    // (readiness is the value itself: spin on the sentinel), then publish the
+    // tile count locally
+    const volatile int* hd = map_rank(&done_l, 0);
+    const double* hz = map_rank(z, 0);
+    int pl = 0;
+    for (unsigned sl = a.sleep_ns; pl < nt;) {
+      const int hv = *hd;
+      if (hv <= pl) {
+        __nanosleep(sl);
+        sl = min(2 * sl, a.sleep_max);
+        continue;
+      }
+      sl = a.sleep_ns;
+      for (int t = pl; t < hv; ++t) {
+        const int i = t * kTile + lane;
+        if (i < n) {
+          const volatile double* src = hz + i;
+          double v = *src;
+          while (is_pending(v)) v = *src;
+          *reinterpret_cast<volatile double*>(z + i) = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) *reinterpret_cast<volatile int*>(&done_l) = hv;
+      pl = hv;
+    }
   } else {
     // workers: far items of L rows, rows ascending
-    const int lw = home ? warp - kFirstWorker : warp;  // scratch slot in this CTA
-    const int w = home ? lw : kWorkers + static_cast<int>(crank - 1) * kWarps + warp;
+    const int lw = home ? warp - kFirstWorker : warp - 1;  // scratch slot in this CTA
+    const int w = home ? lw : kWorkers + static_cast<int>(crank - 1) * (kWarps - 1) + lw;
     const double* fv = a.lval + a.loff[b];
     const uint16_t* fc = a.lcol + a.loff[b];
     const int4* items = a.litems + a.lioff[b];
@@ -651,24 +673,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       double xj = valid ? tile_inverse_dot<false>(T, rbuf, j) : 0.0;
       __syncwarp();
-      if (valid) {
-        *reinterpret_cast<volatile double*>(x + i) = xj;
-        if constexpr (kCl)
-          for (unsigned r = 1; r < kCluster; ++r)
-            *reinterpret_cast<volatile double*>(map_rank(x + i, r)) = xj;
-      }
+      if (valid) *reinterpret_cast<volatile double*>(x + i) = xj;
       __syncwarp();
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
         if (kInPlace) {
           if constexpr (kCl) {
-            // one cluster-scope fence orders the tile's pushes before every
-            // CTA's counter (its workers acquire before reading x)
-            asm volatile("fence.acq_rel.cluster;" ::: "memory");
-            for (unsigned r = 0; r < kCluster; ++r) {
-              int* c = r ? map_rank(&done_u, r) : &done_u;
-              asm volatile("st.relaxed.cluster.b32 [%0], %1;" ::"l"(c), "r"(tt + 1) : "memory");
-            }
+            // cluster scope: the remote pullers acquire it before copying x
+            st_release_cluster(&done_u, tt + 1);
           } else {
             st_release(&done_u, tt + 1);
           }
@@ -683,10 +695,32 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     }
   } else if (kProducer && home && warp == 1) {
     produce(nt + kRing, 2 * nt);
+  } else if (kCl && !home && warp == 0) {
+    // puller, U pass: x overwrites z in place, so readiness is the home's
+    // counter (cluster-scope acquire), republished locally with a release
+    const int* hd = map_rank(&done_u, 0);
+    const double* hx = map_rank(x, 0);
+    int pu = 0;
+    for (unsigned sl = a.sleep_ns; pu < nt;) {
+      const int hv = ld_acquire_cluster(hd);
+      if (hv <= pu) {
+        __nanosleep(sl);
+        sl = min(2 * sl, a.sleep_max);
+        continue;
+      }
+      sl = a.sleep_ns;
+      for (int tt = pu; tt < hv; ++tt) {
+        const int i = (nt - 1 - tt) * kTile + lane;
+        if (i < n) *reinterpret_cast<volatile double*>(x + i) = hx[i];
+      }
+      __syncwarp();
+      if (lane == 0) st_release(&done_u, hv);
+      pu = hv;
+    }
   } else {
     // workers: far items of U rows, rows descending
-    const int lw = home ? warp - kFirstWorker : warp;
-    const int w = home ? lw : kWorkers + static_cast<int>(crank - 1) * kWarps + warp;
+    const int lw = home ? warp - kFirstWorker : warp - 1;
+    const int w = home ? lw : kWorkers + static_cast<int>(crank - 1) * (kWarps - 1) + lw;
     const double* fv = a.uval + a.uoff[b];
     const uint16_t* fc = a.ucol + a.uoff[b];
     const int4* items = a.uitems + a.uioff[b];
@@ -714,13 +748,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int span = (k & 0x7f) + 1;
         const int my = lane < span ? a.uslot[r0 + i + lane] : 0;
         bool has;
-        const double acc = group_dot<kGroupEntries / 32, kInPlace, kCl>(
+        const double acc = group_dot<kGroupEntries / 32, kInPlace>(
             fv, fc, d.z, d.w, rp, i, span, xh, scr, lane, a.sleep_ns, done_uh, d.y >> 8,
             a.sleep_max, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, kInPlace, kCl>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
+        const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
                                                            done_uh, d.y >> 8, a.sleep_max);
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
@@ -872,46 +906,47 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const char* e = getenv("MSCG_TRI_CLUSTER");
     return e ? atoi(e) : -1;
   }();
-  int ccl = 1;
-  if (variant == 0 && d > 1024 && cl_env != 0) {
-    const int fit = sms / std::max(1, npos);
-    // measured at cfg2 (16 blocks): 4 CTAs per block 0.305 ms, 8: 0.487 ms
-    // (pushes to more CTAs lengthen the chain), 1: 0.420 ms
-    for (int c : {6, 4, 3, 2})
-      if ((cl_env < 0 ? c <= std::min(fit, 4) : c == cl_env)) {
-        ccl = c;
-        break;
-      }
-  }
-  if (ccl > 1) {
-    const size_t smc = smem_bytes<true>(d, 32, ns);  // remote CTAs: 32 worker scratches
+  if (variant == 0 && d > 1024 && cl_env != 0 && npos * 2 <= sms) {
+    const size_t smc = smem_bytes<true>(d, 31, ns);
     check_smem(smc);
-    auto go = [&](auto kern) {
-      ensure_smem(reinterpret_cast<const void*>(kern), smc);
+    auto config = [&](int c) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(npos * ccl);
+      cfg.gridDim = dim3(npos * c);
       cfg.blockDim = dim3(32 * 32);
       cfg.dynamicSmemBytes = smc;
       cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = ccl;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
+      return cfg;
+    };
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    // the largest cluster whose clusters all fit at once (a cluster must sit
+    // in one GPC: 16 clusters of 8 full SMs need not fit even when 128 SMs
+    // are free; cfg2 16 blocks: 6 CTAs 0.288 ms, 4: 0.297, 1: 0.420)
+    auto try_size = [&](int c, auto kern) {
+      if (cl_env > 0 ? c != cl_env : npos * c > sms) return false;
+      ensure_smem(reinterpret_cast<const void*>(kern), smc);
+      cudaLaunchConfig_t cfg = config(c);
+      at[0].val.clusterDim.x = c;
       cfg.attrs = at;
       cfg.numAttrs = 1;
+      int active = 0;
+      if (cl_env <= 0 &&
+          (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) != cudaSuccess || active < npos)) {
+        cudaGetLastError();
+        return false;
+      }
       MSCG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, rhs, out, sub));
+      MSCG_CUDA(cudaGetLastError());
+      return true;
     };
-    if (ccl == 6)
-      go(trisolve_kernel<32, 4, 1, true, false, 6>);
-    else if (ccl == 4)
-      go(trisolve_kernel<32, 4, 1, true, false, 4>);
-    else if (ccl == 3)
-      go(trisolve_kernel<32, 4, 1, true, false, 3>);
-    else
-      go(trisolve_kernel<32, 4, 1, true, false, 2>);
-    MSCG_CUDA(cudaGetLastError());
-    return;
+    if (try_size(8, trisolve_kernel<32, 4, 1, true, false, 8>) ||
+        try_size(6, trisolve_kernel<32, 4, 1, true, false, 6>) ||
+        try_size(4, trisolve_kernel<32, 4, 1, true, false, 4>) ||
+        try_size(3, trisolve_kernel<32, 4, 1, true, false, 3>) ||
+        try_size(2, trisolve_kernel<32, 4, 1, true, false, 2>))
+      return;
   }
   if (variant == 0 && npos <= sms && d > 1024) {
     launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
