@@ -696,13 +696,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   } else if (kProducer && home && warp == 1) {
     produce(nt + kRing, 2 * nt);
   } else if (kCl && !home && warp == 0) {
-    // puller, U pass: x overwrites z in place, so readiness is the home's
-    // counter (cluster-scope acquire), republished locally with a release
+    // puller, U pass.  Separate x (the cluster kernels): readiness is the
+    // value itself, as in the L pass, so the solver publishes its counter
+    // without a cluster-scope fence.  In place: the home's counter with
+    // cluster-scope acquire, republished locally with a release.
     const int* hd = map_rank(&done_u, 0);
     const double* hx = map_rank(x, 0);
     int pu = 0;
     for (unsigned sl = a.sleep_ns; pu < nt;) {
-      const int hv = ld_acquire_cluster(hd);
+      const int hv = kInPlace ? ld_acquire_cluster(hd) : *reinterpret_cast<const volatile int*>(hd);
       if (hv <= pu) {
         __nanosleep(sl);
         sl = min(2 * sl, a.sleep_max);
@@ -711,10 +713,20 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       sl = a.sleep_ns;
       for (int tt = pu; tt < hv; ++tt) {
         const int i = (nt - 1 - tt) * kTile + lane;
-        if (i < n) *reinterpret_cast<volatile double*>(x + i) = hx[i];
+        if (i < n) {
+          const volatile double* src = hx + i;
+          double v = *src;
+          while (!kInPlace && is_pending(v)) v = *src;
+          *reinterpret_cast<volatile double*>(x + i) = v;
+        }
       }
       __syncwarp();
-      if (lane == 0) st_release(&done_u, hv);
+      if (lane == 0) {
+        if (kInPlace)
+          st_release(&done_u, hv);
+        else
+          *reinterpret_cast<volatile int*>(&done_u) = hv;
+      }
       pu = hv;
     }
   } else {
@@ -907,7 +919,8 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? atoi(e) : -1;
   }();
   if (variant == 0 && d > 1024 && cl_env != 0 && npos * 2 <= sms) {
-    const size_t smc = smem_bytes<true>(d, 31, ns);
+    // separate z and x (not in place): the U pass needs no cluster fence
+    const size_t smc = smem_bytes<false>(d, 31, ns);
     check_smem(smc);
     auto config = [&](int c) {
       cudaLaunchConfig_t cfg = {};
@@ -941,11 +954,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       MSCG_CUDA(cudaGetLastError());
       return true;
     };
-    if (try_size(8, trisolve_kernel<32, 4, 1, true, false, 8>) ||
-        try_size(6, trisolve_kernel<32, 4, 1, true, false, 6>) ||
-        try_size(4, trisolve_kernel<32, 4, 1, true, false, 4>) ||
-        try_size(3, trisolve_kernel<32, 4, 1, true, false, 3>) ||
-        try_size(2, trisolve_kernel<32, 4, 1, true, false, 2>))
+    if (try_size(8, trisolve_kernel<32, 4, 1, false, false, 8>) ||
+        try_size(6, trisolve_kernel<32, 4, 1, false, false, 6>) ||
+        try_size(4, trisolve_kernel<32, 4, 1, false, false, 4>) ||
+        try_size(3, trisolve_kernel<32, 4, 1, false, false, 3>) ||
+        try_size(2, trisolve_kernel<32, 4, 1, false, false, 2>))
       return;
   }
   if (variant == 0 && npos <= sms && d > 1024) {
