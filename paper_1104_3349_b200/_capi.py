@@ -6,7 +6,8 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libmscg.so")
+# MSCG_LIB: an alternate in-tree build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("MSCG_LIB") or os.path.join(PKG, "libmscg.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "mscg.h")
 
 MSCG_OK = 0

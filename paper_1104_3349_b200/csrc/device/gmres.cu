@@ -61,28 +61,21 @@ __device__ __forceinline__ bool last_block(Reducer red) {
 }
 
 // out[i] (i < nvec) = sum over CTAs of partials[i][cta]; scale: out = f(sum).
+// One warp per output: lane l adds the CTAs l, l + 32, ... in order
+// (coalesced loads), then a fixed butterfly — deterministic, and a few
+// latencies instead of one dependent L2 load per CTA.
 __device__ void finish(Reducer red, int nvec, double* out, int mode) {
   __threadfence();
-  if (nvec == 1 && red.nblk <= 1024) {
-    // one sum (norms): stage the partials in shared memory with one coalesced
-    // round trip, then add them in CTA order (same order as below)
-    __shared__ double stage[1024];
-    for (int c = threadIdx.x; c < red.nblk; c += blockDim.x) stage[c] = __ldcg(red.partials + c);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int c = 0; c < red.nblk; ++c) s += stage[c];
-      out[0] = mode == 1 ? sqrt(s) : s;
-      *red.counter = 0u;
-    }
-    return;
-  }
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i < nvec; i += nw) {
+    const double* pr = red.partials + static_cast<size_t>(i) * red.nblk;
     double s = 0.0;
-    for (int c = 0; c < red.nblk; ++c) s += red.partials[static_cast<size_t>(i) * red.nblk + c];
-    out[i] = mode == 1 ? sqrt(s) : s;
+    for (int c = lane; c < red.nblk; c += 32) s += __ldcg(pr + c);
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) out[i] = mode == 1 ? sqrt(s) : s;
   }
   if (threadIdx.x == 0) *red.counter = 0u;
+  __syncthreads();  // every output written before the caller's epilogue reads it
 }
 
 // ||x||_2 -> *out
