@@ -808,6 +808,25 @@ def test_nested_dissection_device_matches_reference(msc, ctx, ref, seed):
         assert np.array_equal(p, p_ref) and np.array_equal(r, r_ref), (A.nrows, target)
 
 
+def test_nested_dissection_device_many_pieces(msc, ctx, ref):
+    """More than 8191 pieces at the last levels: the device dissection falls
+    back from the cooperative search to the per-round kernels (global piece
+    prefix); still the reference's permutation and ranges."""
+    import scipy.sparse as sp
+    m = 300
+    e = np.ones(m)
+    T = sp.diags([e[:-1], e[:-1]], [-1, 1], shape=(m, m))
+    G = (sp.kron(sp.eye(m), T) + sp.kron(T, sp.eye(m)) + sp.eye(m * m)).tocsr()
+    G.sort_indices()
+    A = msc.SparseMatrix(m * m, m * m, G.indptr.astype(np.int32), G.indices.astype(np.int32),
+                         G.data.astype(np.float64))
+    target = 16384
+    p_ref, r_ref = ref.nested_dissection(A.row_offsets, A.col_indices, target)
+    p, r = msc.nested_dissection(A, target, ctx=ctx)
+    assert len(r_ref) > 8192
+    assert np.array_equal(p, p_ref) and np.array_equal(r, r_ref)
+
+
 def test_device_partition_cfg4_digest(msc, ctx):
     """cfg4 (1024^2, 1024 blocks, anchored) through the device problem path
     (device assembly + device nested dissection): C and the permutation
