@@ -339,7 +339,9 @@ def run_sharded(args, cfg, ws, rank, local, pg, ctx):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)  # library work and NCCL in one stream order
-    pb, setup = build_problem(cfg, threads=max(1, (os.cpu_count() or 8) // ws))
+    # every rank builds the problem on its own GPU (device assembly,
+    # partition and build_msc, bit-identical across ranks)
+    pb, setup = build_problem(cfg, threads=max(1, (os.cpu_count() or 8) // ws), ctx=ctx)
     dr = pb.d_ranges()
     b0, b1 = pdist.shard_blocks(dr[:, 1] - dr[:, 0], ws)[rank]
     t0 = time.perf_counter()
