@@ -36,6 +36,12 @@
 //    lanes poll the same word): a divergent spin sends the next shuffles to
 //    their slow collective path.  The result leaves in one coalesced
 //    epilogue.
+// When the blocks are too few to fill the GPU (cfg2: 16, cfg3: 64), a
+// thread-block cluster of 2-8 CTAs solves each block (kCluster): the home CTA
+// is the kernel above; in the others warp 0 pulls every solved tile into the
+// CTA's own copy of the solution over distributed shared memory and the
+// remaining warps are workers that publish their partial sums straight into
+// the home CTA's slots (see trisolve_kernel and block_trisolve).
 // Rounding differs from the reference's sequential row sums by ~1e-16
 // relative, far inside the 1e-10 apply bar.
 #include <algorithm>
@@ -407,12 +413,13 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
 // ~400 cycles of its chain per tile) and warps 2.. are the workers.
 // kCluster > 1: a cluster of kCluster CTAs solves one block.  CTA 0 (home)
 // is the single-CTA kernel (solver + workers, solution and far-sum slots in
-// its shared memory); CTAs 1.. are all workers: they read the solution from
-// the home CTA's shared memory and publish their partial sums into its slots
-// through distributed shared memory (generic addresses from mapa), and poll
-// its pass counters with cluster-scope acquire.  Used when the blocks are
-// too few to fill the GPU (cfg1 / cfg2): a block's far entries then stream
-// through kCluster SMs instead of one.
+// its shared memory).  In CTAs 1.. warp 0 pulls each solved tile from the
+// home CTA into the CTA's own copy of the solution (generic addresses from
+// mapa; a value is its own readiness when x is kept apart from z, which the
+// cluster launches do) and warps 1.. are workers that gather locally and
+// store their partial sums into the home CTA's slots.  Used when the blocks
+// are too few to fill the GPU (cfg2 / cfg3): a block's far entries then
+// stream through kCluster SMs instead of one.
 template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer,
           int kCluster = 1>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
