@@ -13,6 +13,8 @@
 // CTA order by the last CTA).  The host reads one 32-byte status record per
 // iteration (the reference's convergence test needs it); no other host
 // synchronisation happens inside a cycle.
+#include <cooperative_groups.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -572,9 +574,8 @@ __device__ void dcgs2_fix(const Small& s, const Dcgs& d, int j, bool finalize_on
 // the cycle's finalize-only sweep (no w).  The inner loop is branch-free so
 // that every load of a row pair is in flight at once.
 template <int kG, bool kW>
-__global__ void __launch_bounds__(kThreads, 1) dcgs2_dot_kernel(int n, int j, const double* __restrict__ V,
-                                                             size_t ld, const double* __restrict__ w,
-                                                             Reducer red, Small s, Dcgs d, int local) {
+__device__ __forceinline__ void dot_sweep(int n, int j, const double* __restrict__ V, size_t ld,
+                                          const double* __restrict__ w, Reducer red) {
   __shared__ double sh[kThreads / 32][2 * kG + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nq = j;
@@ -667,8 +668,15 @@ __global__ void __launch_bounds__(kThreads, 1) dcgs2_dot_kernel(int n, int j, co
     }
     __syncthreads();
   }
+}
+
+template <int kG, bool kW>
+__global__ void __launch_bounds__(kThreads, 1) dcgs2_dot_kernel(int n, int j, const double* __restrict__ V,
+                                                             size_t ld, const double* __restrict__ w,
+                                                             Reducer red, Small s, Dcgs d, int local) {
+  dot_sweep<kG, kW>(n, j, V, ld, w, red);
   if (last_block(red)) {
-    finish(red, 2 * nq + 2, d.dots, 0);
+    finish(red, 2 * j + 2, d.dots, 0);
     if (local) return;  // distributed: the sums are all-reduced first (dcgs2_fix_kernel)
     __syncthreads();
     dcgs2_fix(s, d, j, !kW);
@@ -716,15 +724,16 @@ __global__ void __launch_bounds__(kThreads) dcgs2_prelim_kernel(Small s, Dcgs d,
 // last CTA forms the preliminary rotation of column j and the status.
 // n_dot <= n: rows counted in the norm (a distributed rank's own rows);
 // local: leave the sum of squares in nu[j+1] for the all-reduce.
-__global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, double* V, size_t ld,
-                                                              const double* __restrict__ w, Small s,
-                                                              Dcgs d, Reducer red, double denom,
-                                                              int n_dot, int local) {
-  // the coefficients and (last CTA, after the sweep) the Givens stage share
-  // one shared-memory buffer: more CTAs per SM for the sweep
-  constexpr int kCoef = 2 * (kMaxRestart + 12);
-  constexpr int kStage = (sizeof(GivensStage) + sizeof(double) - 1) / sizeof(double);
-  __shared__ __align__(16) double sbuf[kCoef > kStage ? kCoef : kStage];
+// the coefficients and (last CTA, after the sweep) the Givens stage share
+// one shared-memory buffer: more CTAs per SM for the sweep
+constexpr int kCoefElems = 2 * (kMaxRestart + 12);
+constexpr int kStageElems = (sizeof(GivensStage) + sizeof(double) - 1) / sizeof(double);
+constexpr int kSbufElems = kCoefElems > kStageElems ? kCoefElems : kStageElems;
+
+// the sweep of dcgs2_axpy_kernel; this CTA's sum of squares -> partials[cta]
+__device__ __forceinline__ void axpy_sweep(int n, int j, double* V, size_t ld,
+                                           const double* __restrict__ w, const Small& s,
+                                           const Dcgs& d, Reducer red, int n_dot, double* sbuf) {
   double* sS = sbuf;
   double* sT = sbuf + kMaxRestart + 12;
   __shared__ double sh[kThreads / 32];
@@ -778,6 +787,14 @@ __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, doub
   }
   const double bs = block_sum(acc, sh);
   if (threadIdx.x == 0) red.partials[blockIdx.x] = bs;
+}
+
+__global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, double* V, size_t ld,
+                                                              const double* __restrict__ w, Small s,
+                                                              Dcgs d, Reducer red, double denom,
+                                                              int n_dot, int local) {
+  __shared__ __align__(16) double sbuf[kSbufElems];
+  axpy_sweep(n, j, V, ld, w, s, d, red, n_dot, sbuf);
   if (last_block(red)) {
     if (local) {
       finish(red, 1, d.nu + j + 1, 0);
@@ -785,6 +802,52 @@ __global__ void __launch_bounds__(kThreads) dcgs2_axpy_kernel(int n, int j, doub
     }
     finish(red, 1, d.nu + j + 1, 1);
     GivensStage& gs = *reinterpret_cast<GivensStage*>(sbuf);  // coefficients no longer read
+    dcgs2_prelim(s, d, j, denom, gs);
+  }
+}
+
+// ---- one cooperative kernel per DCGS2 step, for short vectors (cfg1 /
+// cfg2), where the two sweeps are latency-bound: grid-wide barriers replace
+// the last-CTA hand-offs, and every CTA helps reduce the per-CTA partials,
+// so only the Givens work stays on one CTA.
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ void grid_finish(Reducer red, int nvec, double* out, int mode) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
+  for (int i = gw; i < nvec; i += nw) {
+    const double* pr = red.partials + static_cast<size_t>(i) * red.nblk;
+    double v = 0.0;
+    for (int c = lane; c < red.nblk; c += 32) v += __ldcg(pr + c);
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) out[i] = mode == 1 ? sqrt(v) : v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) dcgs2_step_coop_kernel(int n, int j, double* V, size_t ld,
+                                                                   const double* __restrict__ w,
+                                                                   Reducer red, Small s, Dcgs d,
+                                                                   double denom) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ __align__(16) double sbuf[kSbufElems];
+  dot_sweep<8, true>(n, j, V, ld, w, red);
+  grid.sync();
+  grid_finish(red, 2 * j + 2, d.dots, 0);
+  grid.sync();
+  if (blockIdx.x == 0) dcgs2_fix(s, d, j, false);
+  grid.sync();
+  axpy_sweep(n, j, V, ld, w, s, d, red, n, sbuf);
+  grid.sync();
+  if (blockIdx.x == 0) {
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+      double v = 0.0;
+      for (int c = lane; c < red.nblk; c += 32) v += __ldcg(red.partials + c);
+      for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) d.nu[j + 1] = sqrt(v);
+    }
+    __syncthreads();
+    GivensStage& gs = *reinterpret_cast<GivensStage*>(sbuf);
     dcgs2_prelim(s, d, j, denom, gs);
   }
 }
@@ -889,6 +952,19 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
   // MSCG_CGS2_FUSED=0: the four-sweep CGS2 (two multi-dot + multi-axpy pairs)
   const char* fused_env = std::getenv("MSCG_CGS2_FUSED");
   const bool cgs2_fused = !(fused_env && fused_env[0] == '0');
+  // Short vectors (n < 2^18: cfg1 / cfg2): one cooperative kernel per DCGS2
+  // step (MSCG_DCGS2_COOP=0|1 forces it off / on), as many CTAs as fit at
+  // once and as the partials buffer holds
+  int coop_grid = 0;
+  if (dcgs2) {
+    const char* ce = std::getenv("MSCG_DCGS2_COOP");
+    const bool want = ce ? ce[0] == '1' : n < (1 << 18);
+    int coop = 0, per_sm = 0, dev = 0;
+    MSCG_CUDA(cudaGetDevice(&dev));
+    MSCG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    MSCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dcgs2_step_coop_kernel, kThreads, 0));
+    if (want && coop && per_sm > 0) coop_grid = std::max(1, std::min(per_sm * ctx->sm_count, G));
+  }
   // MSCG_DOT16=0|1 forces the group size (tests: both give bit-identical sums)
   const char* dot16_env = std::getenv("MSCG_DOT16");
   const bool dot16 = dot16_env ? dot16_env[0] == '1' : G >= 4 * ctx->sm_count;
@@ -987,11 +1063,25 @@ GmresResult gmres(Ctx* ctx, const DevCsr& a, Precond* pc, const double* b, doubl
       apply_op(vj, wp);
       double* Hc = st.H + static_cast<size_t>(j) * (m + 1);
       if (dcgs2) {
-        // two basis sweeps; the status comes from sweep 2's last CTA
-        (dot16 ? dcgs2_dot_kernel<16, true> : dcgs2_dot_kernel<8, true>)<<<G, kThreads, 0, s>>>(
-            n, j, vbase, ld, wp, ws.red, st, dc, 0);
-        dcgs2_axpy_kernel<<<G, kThreads, 0, s>>>(n, j, vbase, ld, wp, st, dc, ws.red, denom, n, 0);
-        ctx->launches += 2;
+        // two basis sweeps; the status comes from sweep 2's last CTA (or the
+        // cooperative step kernel for short vectors)
+        if (coop_grid > 0) {
+          Reducer rc = ws.red;
+          rc.nblk = coop_grid;
+          int jj = j;
+          double dn = denom;
+          int nn = n;
+          size_t lld = ld;
+          void* args[] = {&nn, &jj, &vbase, &lld, &wp, &rc, &st, &dc, &dn};
+          MSCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dcgs2_step_coop_kernel),
+                                                coop_grid, kThreads, args, 0, s));
+          ctx->launches += 1;
+        } else {
+          (dot16 ? dcgs2_dot_kernel<16, true> : dcgs2_dot_kernel<8, true>)<<<G, kThreads, 0, s>>>(
+              n, j, vbase, ld, wp, ws.red, st, dc, 0);
+          dcgs2_axpy_kernel<<<G, kThreads, 0, s>>>(n, j, vbase, ld, wp, st, dc, ws.red, denom, n, 0);
+          ctx->launches += 2;
+        }
         MSCG_CUDA(cudaMemcpyAsync(hstat + 4 * (j & 1), st.status, 3 * sizeof(double),
                                   cudaMemcpyDeviceToHost, s));
         MSCG_CUDA(cudaEventRecord(hev[j & 1], s));

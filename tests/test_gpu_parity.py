@@ -203,6 +203,23 @@ def test_gmres_dcgs2_matches_cgs2(msc, ctx, n, restart, monkeypatch):
     assert np.linalg.norm(b - ax) / np.linalg.norm(b) <= 1e-10
 
 
+@pytest.mark.parametrize("n,restart", [(3001, 30), (48896, 50)])
+def test_gmres_dcgs2_cooperative_step_matches(msc, ctx, n, restart, monkeypatch):
+    """Short vectors run each DCGS2 step as one cooperative kernel
+    (MSCG_DCGS2_COOP): the same arithmetic per row, the reductions over a
+    different CTA grid — iterations equal, histories to 1e-10."""
+    S, A, b = _banded_system(msc, ctx, n, 11)
+    cfg = msc.SolverConfig(restart=restart, max_iters=300, rel_tol=1e-10, orth="dcgs2")
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("MSCG_DCGS2_COOP", mode)
+        out[mode] = msc.gmres(A, None, b, cfg)
+    (x0, r0), (x1, r1) = out["0"], out["1"]
+    assert r0.converged and r1.converged and r0.iterations == r1.iterations
+    assert np.allclose(r1.residual_history, r0.residual_history, rtol=1e-10, atol=1e-15)
+    assert rel_err(x1, x0) < 1e-10
+
+
 @pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
 def test_gmres_dot_groups_bit_identical(msc, ctx, orth, monkeypatch):
     """Basis dots in groups of 8 or 16 vectors (MSCG_DOT16) keep every
