@@ -21,7 +21,9 @@
 // Layout: per block, W_b column-major (column k = dim_b consecutive fp64),
 // blocks back to back; cols_b ascending interface columns (int32).  A work
 // item is (block, 512-row slice; 256 or 128 when there are too few blocks to
-// fill the GPU); a CTA of 256 threads owns one item, stages
+// fill the GPU; 64 rows split four ways over k — correct_split_kernel —
+// when even 128 leaves fewer than 4 items per SM, cfg2 22 -> 16 us); a CTA
+// of 256 threads owns one item, stages
 // z2[cols_b] in shared memory and each thread accumulates rows i and i+256
 // over k in ascending order (one fma per entry, deterministic).  Roofline:
 // HBM, 8 B per W entry (read once per apply, streaming loads so W does not
@@ -103,6 +105,55 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(
     corr_rows<false>(wa, wb, d, kb, zs, a0, a1);
   if (ia < de) out[r0 + ia] = __dsub_rn(z1[r0 + ia], a0);
   if (ib < de) out[r0 + ib] = __dsub_rn(z1[r0 + ib], a1);
+}
+
+// Few rows (cfg1 / cfg2): one row per kSplit threads, each summing a
+// contiguous quarter of the columns (ascending), the quarters then added in
+// order — deterministic; kSplit times the loads in flight of the one-thread
+// rows, whose k_b-long chains left the GPU latency-bound (cfg2 22 us).
+constexpr int kSplit = 4;
+constexpr int kSplitRows = kCorrThreads / kSplit;  // rows per CTA
+
+__global__ void __launch_bounds__(kCorrThreads) correct_split_kernel(
+    const int2* __restrict__ items, int item0, const int* __restrict__ row0,
+    const int* __restrict__ dim, const long long* __restrict__ woff,
+    const int* __restrict__ wcoff, const int* __restrict__ wcols,
+    const double* __restrict__ W, const double* __restrict__ x2,
+    const double* __restrict__ z1, double* __restrict__ out) {
+  extern __shared__ double zs[];
+  __shared__ double part[kSplit][kSplitRows];
+  const int2 it = items[item0 + blockIdx.x];
+  const int b = it.x, i0 = it.y;
+  const int c0 = wcoff[b], kb = wcoff[b + 1] - c0;
+  for (int k = threadIdx.x; k < kb; k += kCorrThreads) zs[k] = __ldg(x2 + __ldg(wcols + c0 + k));
+  __syncthreads();
+  const int d = dim[b];
+  const int r = threadIdx.x % kSplitRows, q = threadIdx.x / kSplitRows;  // row, quarter
+  const int i = i0 + r;
+  const int k0 = kb * q / kSplit, k1 = kb * (q + 1) / kSplit;
+  const double* wr = W + woff[b] + min(i, d - 1);
+  double a = 0.0, a2 = 0.0;
+  int k = k0;
+  for (; k + 8 <= k1; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldcs(wr + static_cast<size_t>(k + j) * d);
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      a = fma(v[j], zs[k + j], a);
+      a2 = fma(v[j + 1], zs[k + j + 1], a2);
+    }
+  }
+  for (; k < k1; ++k) a = fma(__ldcs(wr + static_cast<size_t>(k) * d), zs[k], a);
+  part[q][r] = a + a2;
+  __syncthreads();
+  if (q == 0 && i < d && i < i0 + kSplitRows) {
+    double t = part[0][r];
+#pragma unroll
+    for (int qq = 1; qq < kSplit; ++qq) t += part[qq][r];
+    const int r0 = row0[b];
+    out[r0 + i] = __dsub_rn(z1[r0 + i], t);
+  }
 }
 
 // Setup: r[row0_b + rows of column k of E_b] = values (or 0 when clearing).
@@ -235,6 +286,12 @@ std::unique_ptr<Correction> build_correction(Ctx* ctx, const FactorSet& D, const
   MSCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   c->slice = kCorrSlice;
   while (c->slice > 128 && static_cast<int64_t>(D.total_rows) / c->slice < 4 * sms) c->slice /= 2;
+  // still too few items for the GPU: rows of kSplit threads (MSCG_CORR_SPLIT=0|1)
+  {
+    const char* e = getenv("MSCG_CORR_SPLIT");
+    c->split = e ? e[0] == '1' : static_cast<int64_t>(D.total_rows) / c->slice < 4 * sms;
+    if (c->split) c->slice = kSplitRows;
+  }
   std::vector<int2> items;
   c->h_item_chunk.assign(kSolveChunks + 1, 0);
   for (int ch = 0; ch < kSolveChunks; ++ch) {
@@ -281,10 +338,17 @@ void apply_correction(const Correction& c, const double* x2, const double* z1, d
   const int i1 = chunk < 0 ? c.h_item_chunk[kSolveChunks] : c.h_item_chunk[chunk + 1];
   if (i1 <= i0) return;
   const size_t smem = sizeof(double) * std::max(1, c.kmax);
-  ensure_smem(reinterpret_cast<const void*>(correct_kernel), smem);
-  correct_kernel<<<i1 - i0, kCorrThreads, smem, s>>>(
-      c.items.as<int2>(), i0, c.row0, c.dim, c.woff.as<long long>(), c.wcoff.as<int>(),
-      c.wcols.as<int>(), c.wval.as<double>(), x2, z1, out, c.slice);
+  if (c.split) {
+    ensure_smem(reinterpret_cast<const void*>(correct_split_kernel), smem);
+    correct_split_kernel<<<i1 - i0, kCorrThreads, smem, s>>>(
+        c.items.as<int2>(), i0, c.row0, c.dim, c.woff.as<long long>(), c.wcoff.as<int>(),
+        c.wcols.as<int>(), c.wval.as<double>(), x2, z1, out);
+  } else {
+    ensure_smem(reinterpret_cast<const void*>(correct_kernel), smem);
+    correct_kernel<<<i1 - i0, kCorrThreads, smem, s>>>(
+        c.items.as<int2>(), i0, c.row0, c.dim, c.woff.as<long long>(), c.wcoff.as<int>(),
+        c.wcols.as<int>(), c.wval.as<double>(), x2, z1, out, c.slice);
+  }
   MSCG_CUDA(cudaGetLastError());
 }
 

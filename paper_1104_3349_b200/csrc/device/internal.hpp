@@ -253,6 +253,7 @@ struct Correction {
   DevBuf wval;                 // fp64 panels
   DevBuf items;                // int2 {block, first row} (slices of `slice` rows)
   int slice = 512;
+  bool split = false;          // correct_split_kernel (few rows)
   std::vector<int> h_item_chunk;  // item range of block chunk c
   double build_s = 0;
 };
