@@ -177,6 +177,31 @@ template <bool kAcquire, bool kRemote = false>
 __device__ __forceinline__ int poll(const int* p) {
   return kAcquire ? (kRemote ? ld_acquire_cluster(p) : ld_acquire(p)) : vload(p);
 }
+// How a worker learns that `need` tiles of the pass are solved:
+//   kWaitValue   relaxed counter as a hint, the solution slots' sentinels as
+//                the guarantee (x kept apart from z, and every L pass);
+//   kWaitAcquire the counter read with acquire (x overwrites z in place: a
+//                value's presence cannot mark readiness);
+//   kWaitTile    in place, one mbarrier per tile: the solver's arrive releases
+//                the tile's stores, try_wait acquires them and suspends the
+//                warp in hardware instead of a sleep loop.
+constexpr int kWaitValue = 0, kWaitAcquire = 1, kWaitTile = 2;
+template <int kWait, bool kRemote>
+__device__ __forceinline__ void wait_tiles(const int* done, int need, unsigned ns,
+                                           unsigned ns_max) {
+  if constexpr (kWait == kWaitTile) {
+    if (need > 0)
+      mbar_wait(reinterpret_cast<uint64_t*>(const_cast<int*>(done)) + (need - 1), 0);
+  } else {
+    // every lane polls the same word: the loop exit is warp-uniform, so the
+    // warp stays converged (divergent spins cost the shuffles afterwards
+    // their fast path).  Exponential back-off: the solver finishes a tile
+    // every few microseconds and short polls would steal its issue slots.
+    for (unsigned sl = ns; poll<kWait == kWaitAcquire, kRemote>(done) < need;
+         sl = min(2 * sl, ns_max))
+      __nanosleep(sl);
+  }
+}
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -214,11 +239,12 @@ __device__ __forceinline__ Slice aligned_slice(const double* p, int len) {
 // instead of per-lane loop bounds) so the final reduction runs converged.
 // The first round's loads are issued before the readiness wait (one poll
 // per warp on the tile counter).
-template <int kUnroll, bool kInPlace, bool kRemote = false>
+template <int kUnroll, int kWait, bool kRemote = false>
 __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
                                           const int* done, int need, unsigned ns_max) {
+  constexpr bool kInPlace = kWait != kWaitValue;
   double acc = 0.0, acc2 = 0.0;
   for (int base = s; base < e; base += 32 * kUnroll) {
     double v[kUnroll];
@@ -234,14 +260,7 @@ __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
         c[u] = -1;
       }
     }
-    if (base == s) {
-      // every lane polls the same word: the loop exit is warp-uniform, so
-      // the warp stays converged (divergent spins cost the shuffles below
-      // their fast path)
-      // exponential back-off: the solver finishes a tile every few
-      // microseconds and short polls would steal its issue slots
-      for (unsigned s = ns; poll<kInPlace, kRemote>(done) < need; s = min(2 * s, ns_max)) __nanosleep(s);
-    }
+    if (base == s) wait_tiles<kWait, kRemote>(done, need, ns, ns_max);
     // Gather operands (independent shared loads); poll only if one is still
     // pending (the counter is a hint, the sentinel is the guarantee).
     const volatile double* vs = sol;
@@ -274,13 +293,14 @@ __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
 // (at most 32 * kUnroll).  One round of loads for all rows; each product goes
 // to the warp's shared scratch and lane r sums row r's run in entry order.
 // Returns lane r's row sum (and whether row r has entries).
-template <int kUnroll, bool kInPlace, bool kRemote = false>
+template <int kUnroll, int kWait, bool kRemote = false>
 __device__ __noinline__ double group_dot(const double* __restrict__ vals,
                                             const uint16_t* __restrict__ cols, int s, int e,
                                             const int* rp, int row0, int span,
                                             const double* sol, double* scratch, int lane,
                                             unsigned ns, const int* done, int need,
                                             unsigned ns_max, bool& has) {
+  constexpr bool kInPlace = kWait != kWaitValue;
   double v[kUnroll];
   int c[kUnroll];
 #pragma unroll
@@ -292,7 +312,7 @@ __device__ __noinline__ double group_dot(const double* __restrict__ vals,
   const bool mine = lane < span;
   const int rb = mine ? __ldg(rp + row0 + lane) : 0;
   const int re = mine ? __ldg(rp + row0 + lane + 1) : 0;
-  for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max)) __nanosleep(sl);
+  wait_tiles<kWait, kRemote>(done, need, ns, ns_max);
   const volatile double* vs = sol;
   double xv[kUnroll];
   bool pending = false;
@@ -420,14 +440,18 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
 // store their partial sums into the home CTA's slots.  Used when the blocks
 // are too few to fill the GPU (cfg2 / cfg3): a block's far entries then
 // stream through kCluster SMs instead of one.
+// kTileBars (in place, single CTA): U readiness through one mbarrier per tile
+// (kWaitTile) instead of the release/acquire counter.
 template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer,
-          int kCluster = 1>
+          int kCluster = 1, bool kTileBars = false>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
   constexpr int kFirstWorker = kProducer ? 2 : 1;
   constexpr int kWorkers = kWarps - kFirstWorker;
   constexpr bool kCl = kCluster > 1;
+  static_assert(!kTileBars || (kInPlace && !kCl), "tile barriers: in-place single-CTA solve");
+  constexpr int kWaitU = !kInPlace ? kWaitValue : (kTileBars ? kWaitTile : kWaitAcquire);
   // workers of the whole cluster: the home CTA's, then warps 1.. of the
   // others (warp 0 of a remote CTA pulls the solution, see below)
   constexpr int kAllWorkers = kWorkers + (kCluster - 1) * (kWarps - 1);
@@ -439,6 +463,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
   double* rbuf = scratch + kWorkers * kGroupEntries;  // solver: the tile's residuals
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(rbuf + kTile);  // U tile solved (kTileBars)
   __shared__ __align__(8) uint64_t bars[kRing];   // near item landed (TMA)
   __shared__ __align__(8) uint64_t empty[kRing];  // near item consumed (producer variant)
   __shared__ int done_l, done_u;
@@ -468,6 +493,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (!kInPlace) x[i] = i < n ? pend : 0.0;
   }
   for (int i = threadIdx.x; i < a.max_slots; i += blockDim.x) part[i] = pend;
+  if constexpr (kTileBars)
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) mbar_init(&tbar[t], 1);
   if (threadIdx.x == 0) {
     done_l = 0;
     done_u = 0;
@@ -632,13 +659,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int my = lane < span ? a.lslot[r0 + i + lane] : 0;
         bool has;
         const double acc =
-            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, span, zh, scr, lane,
+            group_dot<kGroupEntries / 32, kWaitValue>(fv, fc, d.z, d.w, rp, i, span, zh, scr, lane,
                                                  a.sleep_ns, done_lh, d.y >> 8, a.sleep_max, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
-                                                   done_lh, d.y >> 8, a.sleep_max);
+        const double acc = seg_dot<kUnroll, kWaitValue>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
+                                                        done_lh, d.y >> 8, a.sleep_max);
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
@@ -684,7 +711,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
-        if (kInPlace) {
+        if constexpr (kTileBars) {
+          mbar_arrive(&tbar[tt]);  // release: the tile's x is visible to whoever acquires it
+        } else if (kInPlace) {
           if constexpr (kCl) {
             // cluster scope: the remote pullers acquire it before copying x
             st_release_cluster(&done_u, tt + 1);
@@ -747,6 +776,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const long long lit = a.lnum[b];
     const int* rp = a.urp + r0 + b;
     double* scr = scratch + lw * kGroupEntries;
+    const int* wait_u = kTileBars ? reinterpret_cast<const int*>(tbar) : done_uh;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_u && w + kAllWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kAllWorkers * lane];
@@ -767,14 +797,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int span = (k & 0x7f) + 1;
         const int my = lane < span ? a.uslot[r0 + i + lane] : 0;
         bool has;
-        const double acc = group_dot<kGroupEntries / 32, kInPlace>(
-            fv, fc, d.z, d.w, rp, i, span, xh, scr, lane, a.sleep_ns, done_uh, d.y >> 8,
+        const double acc = group_dot<kGroupEntries / 32, kWaitU>(
+            fv, fc, d.z, d.w, rp, i, span, xh, scr, lane, a.sleep_ns, wait_u, d.y >> 8,
             a.sleep_max, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
-                                                           done_uh, d.y >> 8, a.sleep_max);
+        const double acc = seg_dot<kUnroll, kWaitU>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
+                                                         wait_u, d.y >> 8, a.sleep_max);
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
@@ -799,7 +829,8 @@ size_t smem_bytes(int dim_max, int workers, int slots) {
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
                            ((static_cast<size_t>(slots) + 1) & ~static_cast<size_t>(1)) +
                            (kInPlace ? 1 : 2) * dpad +
-                           static_cast<size_t>(workers) * kGroupEntries + kTile);
+                           static_cast<size_t>(workers) * kGroupEntries + kTile +
+                           dpad / kTile);  // + one mbarrier per tile (kTileBars)
 }
 
 }  // namespace
@@ -892,6 +923,12 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const char* e = getenv("MSCG_TRI_VARIANT");
     return e ? atoi(e) : 0;
   }();
+  // U readiness in the in-place kernels: per-tile mbarriers (1) or the
+  // release/acquire counter (0)
+  static const bool tile_bars = [] {
+    const char* e = getenv("MSCG_TRI_TILEBARS");
+    return e ? atoi(e) != 0 : false;
+  }();
   auto check_smem = [&](size_t smem) {
     if (smem > 227 * 1024)
       throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
@@ -969,7 +1006,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       return;
   }
   if (variant == 0 && npos <= sms && d > 1024) {
-    launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
+    if (tile_bars)
+      launch(trisolve_kernel<32, 4, 1, true, false, 1, true>, 32, smem_bytes<true>(d, 31, ns));
+    else
+      launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
     MSCG_CUDA(cudaGetLastError());
     return;
   }
@@ -992,7 +1032,8 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const int head = npos - tail;
     check_smem(smem_bytes<true>(d, 31, ns));
     {
-      auto k16 = trisolve_kernel<16, 4, 2, true, false>;
+      auto k16 = tile_bars ? trisolve_kernel<16, 4, 2, true, false, 1, true>
+                           : trisolve_kernel<16, 4, 2, true, false>;
       const size_t sm16 = smem_bytes<true>(d, 15, ns);
       ensure_smem(reinterpret_cast<const void*>(k16), sm16);
       k16<<<head, 16 * 32, sm16, s>>>(a, rhs, out, sub);
@@ -1001,7 +1042,8 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     {
       TriArgs at = a;
       at.pos0 = pos0 + head;
-      auto k32 = trisolve_kernel<32, 4, 1, true, false>;
+      auto k32 = tile_bars ? trisolve_kernel<32, 4, 1, true, false, 1, true>
+                           : trisolve_kernel<32, 4, 1, true, false>;
       const size_t sm32 = smem_bytes<true>(d, 31, ns);
       ensure_smem(reinterpret_cast<const void*>(k32), sm32);
       k32<<<tail, 32 * 32, sm32, fs.tail_stream>>>(at, rhs, out, sub);
@@ -1028,7 +1070,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       launch(trisolve_kernel<16, 4, 2, false, false>, 16, smem_bytes<false>(d, 15, ns));
       break;
     default:  // 2 CTAs/SM (64 registers), x overwrites z in place
-      launch(trisolve_kernel<16, 4, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
+      if (tile_bars)
+        launch(trisolve_kernel<16, 4, 2, true, false, 1, true>, 16, smem_bytes<true>(d, 15, ns));
+      else
+        launch(trisolve_kernel<16, 4, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
       break;
   }
   MSCG_CUDA(cudaGetLastError());
