@@ -661,7 +661,8 @@ __global__ void __launch_bounds__(256) count_far_kernel(
     const int* __restrict__ set_row0, const int* __restrict__ blk_dim, PoolView pool,
     int* __restrict__ lcnt, int* __restrict__ ucnt, int* __restrict__ lnb,
     int* __restrict__ unb, long long* __restrict__ far_l, long long* __restrict__ far_u,
-    long long* __restrict__ items_l, long long* __restrict__ items_u) {
+    long long* __restrict__ items_l, long long* __restrict__ items_u, int pieces_l,
+    int pieces_u) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -699,8 +700,8 @@ __global__ void __launch_bounds__(256) count_far_kernel(
       unb[r0 + i] = nu;
       tl += cl;
       tu += cu;
-      jl += far_segments(cl);
-      ju += far_segments(cu);
+      jl += far_pieces(cl, pieces_l);  // upper bounds (the pack may choose fewer)
+      ju += far_pieces(cu, pieces_u);
     }
   }
   if (lane == 0) {
@@ -731,32 +732,84 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
     int* __restrict__ lnum, int* __restrict__ unum, const int* __restrict__ lnb,
     const int* __restrict__ unb, int* __restrict__ lwidth, int* __restrict__ uwidth,
     int* __restrict__ lslot, int* __restrict__ uslot, int* __restrict__ nslots,
-    int4* __restrict__ ltmp, int4* __restrict__ utmp) {
+    int4* __restrict__ ltmp, int4* __restrict__ utmp, int pieces_l, int pieces_u, int slack_l,
+    int slack_u) {
   const int b = blockIdx.x;
   const int r0 = set_row0[b], n = blk_dim[b];
+  const int ntb = (n + kTile - 1) / kTile;
   int* lr = lrp + r0 + b;
   int* ur = urp + r0 + b;
+  // pieces per long row chosen for this block (<= pieces_l / pieces_u)
+  __shared__ int s_pl, s_pu;
   if (threadIdx.x == 0) {
+    // Long rows are cut into pieces by readiness (see `cuts` below); more
+    // pieces let a row's early columns stream while the chain is still far
+    // from the row.  Every piece owns a far-sum slot in shared memory, so a
+    // pass takes more pieces only while its slots stay within what the block
+    // needs anyway (the larger of the two passes with the default cut).
+    auto slots = [&](const int* cnt, int pieces) {
+      int q = 0;
+      for (int i = 0; i < n; ++i) q += far_pieces(cnt[r0 + i], pieces);
+      return q;
+    };
+    const int budget = max(slots(lcnt, 1), slots(ucnt, 1));
+    int pl = pieces_l, pu = pieces_u;
+    while (pl > 1 && slots(lcnt, pl) > budget) --pl;
+    while (pu > 1 && slots(ucnt, pu) > budget) --pu;
+    s_pl = pl;
+    s_pu = pu;
     int sl = 0, su = 0, ql = 0, qu = 0;
     for (int i = 0; i < n; ++i) {
       lr[i] = sl;
       ur[i] = su;
       sl += lcnt[r0 + i];
       su += ucnt[r0 + i];
-      // far-sum slots of the row's work items (one per segment)
+      // far-sum slots of the row's work items (one per piece)
       lslot[r0 + i] = ql;
       uslot[r0 + i] = qu;
-      ql += far_segments(lcnt[r0 + i]);
-      qu += far_segments(ucnt[r0 + i]);
+      ql += far_pieces(lcnt[r0 + i], pl);
+      qu += far_pieces(ucnt[r0 + i], pu);
     }
     lr[n] = sl;
     ur[n] = su;
     nslots[b] = max(ql, qu);
+    // Piece boundaries of a long row, as offsets e[0..ns] into the row's far
+    // entries taken in the order they become computable (L: columns
+    // ascending; U: descending).  One piece per kSeg entries by count when
+    // the block keeps the default; otherwise by readiness: piece q ends where
+    // the readiness coordinate passes (q/ns)^2 of the row's range, so the
+    // early pieces are small and available early, and no piece is empty.
+    auto cuts = [&](int i, int cnt, int pieces, bool lower, int* e) {
+      const int ns = far_pieces(cnt, pieces);
+      e[0] = 0;
+      e[ns] = cnt;
+      if (pieces <= 1) {
+        for (int q = 1; q < ns; ++q) e[q] = q * kSeg;
+        return ns;
+      }
+      const uint16_t* col = lower ? pool.lcol + pool.lstart[r0 + i]
+                                  : pool.ucol + pool.ustart[r0 + i] + pool.ulen[r0 + i] - cnt;
+      auto rho = [&](int k) {  // readiness coordinate of the k-th entry in readiness order
+        return lower ? static_cast<int>(col[k]) : ntb * kTile - 1 - static_cast<int>(col[cnt - 1 - k]);
+      };
+      const long long span = rho(cnt - 1) + 1;
+      for (int q = 1; q < ns; ++q) {
+        const int thr = static_cast<int>(span * q * q / (ns * ns));
+        int lo = 0, hi = cnt;  // first k with rho(k) >= thr
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (rho(mid) >= thr) hi = mid; else lo = mid + 1;
+        }
+        e[q] = min(max(lo, e[q - 1] + 1), cnt - (ns - q));
+      }
+      return ns;
+    };
     // Work items in solve order (entry offsets within the block).  Long rows:
     // {row, segment, begin, end}, kSeg entries per segment.  Runs of short
     // rows of one tile: one multi-row item (see kShortRow).
     // x = row | first far-sum slot << 16.
-    auto build = [&](int4* out, const int* rp, const int* cnt, const int* slot, bool asc) {
+    auto build = [&](int4* out, const int* rp, const int* cnt, const int* slot, bool asc,
+                     int pieces) {
       int4* o = out;
       int g0 = -1, g1 = -1, gent = 0;  // open group: rows [g0, g1], entries
       auto close = [&]() {
@@ -787,18 +840,20 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
           continue;
         }
         close();
-        const int ns = far_segments(c);
+        int e[kMaxSeg + 1];
+        const int ns = cuts(i, c, pieces, asc, e);
         for (int q = 0; q < ns; ++q) {
-          const int b0 = rp[i] + q * kSeg;
-          *o++ = make_int4(i | ((slot[r0 + i] + q) << 16), q, b0,
-                           q == ns - 1 ? rp[i] + c : b0 + kSeg);
+          // U: readiness order runs from the row's last entry backwards
+          const int b0 = asc ? rp[i] + e[q] : rp[i] + c - e[q + 1];
+          const int b1 = asc ? rp[i] + e[q + 1] : rp[i] + c - e[q];
+          *o++ = make_int4(i | ((slot[r0 + i] + q) << 16), q, b0, b1);
         }
       }
       close();
       return static_cast<int>(o - out);
     };
-    lnum[b] = build(litems + lioff[b], lr, lcnt, lslot, true);
-    unum[b] = build(uitems + uioff[b], ur, ucnt, uslot, false);
+    lnum[b] = build(litems + lioff[b], lr, lcnt, lslot, true, pl);
+    unum[b] = build(uitems + uioff[b], ur, ucnt, uslot, false, pu);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -840,10 +895,10 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
       urdiag[r0 + i] = rd;
       // tile metadata for the solver (see kMetaDiag / kMetaSeg)
       utt[kMetaDiag + j] = rd;
-      ltt[kMetaSeg + j] =
-          __longlong_as_double(far_segments(lcnt[r0 + i]) | (static_cast<long long>(lslot[r0 + i]) << 8));
-      utt[kMetaSeg + j] =
-          __longlong_as_double(far_segments(ucnt[r0 + i]) | (static_cast<long long>(uslot[r0 + i]) << 8));
+      ltt[kMetaSeg + j] = __longlong_as_double(far_pieces(lcnt[r0 + i], s_pl) |
+                                               (static_cast<long long>(lslot[r0 + i]) << 8));
+      utt[kMetaSeg + j] = __longlong_as_double(far_pieces(ucnt[r0 + i], s_pu) |
+                                               (static_cast<long long>(uslot[r0 + i]) << 8));
     }
     // window padding: every ELL slot past the row's entries reads a solved slot
     if (wl != kDenseNbr)
@@ -1000,24 +1055,36 @@ __global__ void __launch_bounds__(256) pack_tiled_kernel(
   // the far entries of late rows stream while the chain is still early.
   // Each item writes its own far-sum slot, so the sums stay deterministic.
   __syncthreads();
+  // With a slack (tiles) the key is max(need, deadline - slack), deadline =
+  // the tiles solved before the item's own: an item computable early but due
+  // late (U: velocity rows against pressure columns) no longer queues ahead
+  // of the items the chain is about to wait for.  need <= key <= deadline - 2,
+  // so an item is still computable when the workers reach it in key order
+  // whenever the chain has passed its key.
   __shared__ int hist[2][kMaxNeed + 2];
-  auto sort_items = [&](int4* items, int4* tmp, int cnt, int* h) {
+  auto sort_items = [&](int4* items, int4* tmp, int cnt, int* h, bool lower, int slack) {
+    auto key = [&](const int4& d) {
+      const int need = d.y >> 8;
+      if (slack <= 0) return need;
+      const int t = (d.x & 0xffff) >> 5;
+      return max(need, (lower ? t : nt - 1 - t) - slack);
+    };
     for (int k = threadIdx.x; k < kMaxNeed + 2; k += blockDim.x) h[k] = 0;
     __syncthreads();
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
       tmp[q] = items[q];
-      atomicAdd(&h[(items[q].y >> 8) + 1], 1);
+      atomicAdd(&h[key(items[q]) + 1], 1);
     }
     __syncthreads();
     if (threadIdx.x == 0)
       for (int k = 1; k < kMaxNeed + 2; ++k) h[k] += h[k - 1];
     __syncthreads();
     if (threadIdx.x == 0)  // stable scatter
-      for (int q = 0; q < cnt; ++q) items[h[tmp[q].y >> 8]++] = tmp[q];
+      for (int q = 0; q < cnt; ++q) items[h[key(tmp[q])]++] = tmp[q];
     __syncthreads();
   };
-  sort_items(litems + lioff[b], ltmp + lioff[b], lnum[b], hist[0]);
-  sort_items(uitems + uioff[b], utmp + uioff[b], unum[b], hist[1]);
+  sort_items(litems + lioff[b], ltmp + lioff[b], lnum[b], hist[0], true, slack_l);
+  sort_items(uitems + uioff[b], utmp + uioff[b], unum[b], hist[1], false, slack_u);
 }
 
 template <class T>
@@ -1229,10 +1296,21 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
   DevBuf lnb(sizeof(int) * total), unb(sizeof(int) * total);
   DevBuf farl(sizeof(long long) * nb), faru(sizeof(long long) * nb);
   DevBuf itl(sizeof(long long) * nb), itu(sizeof(long long) * nb);
+  // Work-item policy of the pack (see pack_tiled_kernel): pieces per long row
+  // and the ordering slack, per pass.
+  auto env_int = [](const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+  };
+  const int pieces_l = std::min(kMaxSeg, std::max(1, env_int("MSCG_PACK_PIECES_L", 1)));
+  const int pieces_u = std::min(kMaxSeg, std::max(1, env_int("MSCG_PACK_PIECES_U", 1)));
+  const int slack_l = env_int("MSCG_PACK_SLACK_L", 0);
+  const int slack_u = env_int("MSCG_PACK_SLACK_U", 8);
   count_far_kernel<<<nb, 256, 0, s>>>(fs->row0.as<int>(), fs->dim.as<int>(), pv, lcnt.as<int>(),
                                       ucnt.as<int>(), lnb.as<int>(), unb.as<int>(),
                                       farl.as<long long>(), faru.as<long long>(),
-                                      itl.as<long long>(), itu.as<long long>());
+                                      itl.as<long long>(), itu.as<long long>(), pieces_l,
+                                      pieces_u);
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
   std::vector<long long> hl(nb), hu(nb), hil(nb), hiu(nb);
@@ -1290,7 +1368,7 @@ std::unique_ptr<FactorSet> factor_blocks(Ctx* ctx, const int* a_rp, const int* a
       fs->uioff.as<long long>(), fs->litems.as<int4>(), fs->uitems.as<int4>(),
       fs->lnum.as<int>(), fs->unum.as<int>(), lnb.as<int>(), unb.as<int>(),
       fs->lwidth.as<int>(), fs->uwidth.as<int>(), fs->lslot.as<int>(), fs->uslot.as<int>(),
-      nslots.as<int>(), ltmp.as<int4>(), utmp.as<int4>());
+      nslots.as<int>(), ltmp.as<int4>(), utmp.as<int4>(), pieces_l, pieces_u, slack_l, slack_u);
   MSCG_CUDA(cudaGetLastError());
   ctx->launches++;
   {

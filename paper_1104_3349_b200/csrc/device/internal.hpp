@@ -157,6 +157,13 @@ __host__ __device__ inline int far_segments(int nfar) {
   const int s = (nfar + kSeg - 1) / kSeg;
   return s < kMaxSeg ? s : kMaxSeg;
 }
+// Pieces of a long row (more than kShortRow far entries) when the pack cuts
+// rows by readiness (pack_tiled_kernel): at least `pieces`, at most kMaxSeg.
+__host__ __device__ inline int far_pieces(int nfar, int pieces) {
+  int s = far_segments(nfar);
+  if (nfar > kShortRow && s < pieces) s = pieces;
+  return s < kMaxSeg ? s : kMaxSeg;
+}
 struct FactorSet {
   int nblocks = 0;
   int total_rows = 0;

@@ -177,31 +177,6 @@ template <bool kAcquire, bool kRemote = false>
 __device__ __forceinline__ int poll(const int* p) {
   return kAcquire ? (kRemote ? ld_acquire_cluster(p) : ld_acquire(p)) : vload(p);
 }
-// How a worker learns that `need` tiles of the pass are solved:
-//   kWaitValue   relaxed counter as a hint, the solution slots' sentinels as
-//                the guarantee (x kept apart from z, and every L pass);
-//   kWaitAcquire the counter read with acquire (x overwrites z in place: a
-//                value's presence cannot mark readiness);
-//   kWaitTile    in place, one mbarrier per tile: the solver's arrive releases
-//                the tile's stores, try_wait acquires them and suspends the
-//                warp in hardware instead of a sleep loop.
-constexpr int kWaitValue = 0, kWaitAcquire = 1, kWaitTile = 2;
-template <int kWait, bool kRemote>
-__device__ __forceinline__ void wait_tiles(const int* done, int need, unsigned ns,
-                                           unsigned ns_max) {
-  if constexpr (kWait == kWaitTile) {
-    if (need > 0)
-      mbar_wait(reinterpret_cast<uint64_t*>(const_cast<int*>(done)) + (need - 1), 0);
-  } else {
-    // every lane polls the same word: the loop exit is warp-uniform, so the
-    // warp stays converged (divergent spins cost the shuffles afterwards
-    // their fast path).  Exponential back-off: the solver finishes a tile
-    // every few microseconds and short polls would steal its issue slots.
-    for (unsigned sl = ns; poll<kWait == kWaitAcquire, kRemote>(done) < need;
-         sl = min(2 * sl, ns_max))
-      __nanosleep(sl);
-  }
-}
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -239,14 +214,68 @@ __device__ __forceinline__ Slice aligned_slice(const double* p, int len) {
 // instead of per-lane loop bounds) so the final reduction runs converged.
 // The first round's loads are issued before the readiness wait (one poll
 // per warp on the tile counter).
-template <int kUnroll, int kWait, bool kRemote = false>
-__device__ __noinline__ double seg_dot(const double* __restrict__ vals,
+template <int kUnroll, bool kInPlace, bool kRemote = false>
+__device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
                                           const int* done, int need, unsigned ns_max) {
-  constexpr bool kInPlace = kWait != kWaitValue;
   double acc = 0.0, acc2 = 0.0;
-  for (int base = s; base < e; base += 32 * kUnroll) {
+  const volatile double* vs = sol;
+  bool waited = false;
+  // every lane polls the same word: the loop exit is warp-uniform, so the
+  // warp stays converged (divergent spins cost the shuffles below their fast
+  // path).  Exponential back-off: the solver finishes a tile every few
+  // microseconds and short polls would steal its issue slots.
+  auto wait = [&]() {
+    for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max))
+      __nanosleep(sl);
+    waited = true;
+  };
+  // Gather operands (independent shared loads); poll only if one is still
+  // pending (the counter is a hint, the sentinel is the guarantee).
+  auto settle = [&](double (&xv)[kUnroll], const int (&c)[kUnroll]) {
+    if (kInPlace) return;
+    bool pending = false;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) pending |= is_pending(xv[u]);
+    while (__any_sync(0xffffffffu, pending)) {
+      __nanosleep(ns);
+      pending = false;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (c[u] >= 0 && is_pending(xv[u])) xv[u] = vs[c[u]];
+        pending |= is_pending(xv[u]);
+      }
+    }
+  };
+  int base = s;
+  // Full rounds: no bounds predicates.  The streaming phases of the solve are
+  // issue-bound (16 warps per scheduler pair), and a predicated load costs
+  // its own descriptor moves on top of the compare.
+  const double* pv = vals + s + lane;
+  const uint16_t* pc = cols + s + lane;
+  for (; base + 32 * kUnroll <= e; base += 32 * kUnroll) {
+    double v[kUnroll];
+    int c[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      v[u] = __ldg(pv + 32 * u);
+      c[u] = __ldg(pc + 32 * u);
+    }
+    pv += 32 * kUnroll;
+    pc += 32 * kUnroll;
+    if (!waited) wait();
+    double xv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) xv[u] = vs[c[u]];
+    settle(xv, c);
+#pragma unroll
+    for (int u = 0; u < kUnroll; u += 2) {
+      acc = fma(v[u], xv[u], acc);
+      acc2 = fma(v[u + 1], xv[u + 1], acc2);
+    }
+  }
+  if (base < e) {  // the last, partial round
     double v[kUnroll];
     int c[kUnroll];
 #pragma unroll
@@ -260,26 +289,11 @@ __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
         c[u] = -1;
       }
     }
-    if (base == s) wait_tiles<kWait, kRemote>(done, need, ns, ns_max);
-    // Gather operands (independent shared loads); poll only if one is still
-    // pending (the counter is a hint, the sentinel is the guarantee).
-    const volatile double* vs = sol;
+    if (!waited) wait();
     double xv[kUnroll];
-    bool pending = false;
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
-      pending |= is_pending(xv[u]);
-    }
-    while (!kInPlace && __any_sync(0xffffffffu, pending)) {
-      __nanosleep(ns);
-      pending = false;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        if (c[u] >= 0 && is_pending(xv[u])) xv[u] = vs[c[u]];
-        pending |= is_pending(xv[u]);
-      }
-    }
+    for (int u = 0; u < kUnroll; ++u) xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
+    settle(xv, c);
 #pragma unroll
     for (int u = 0; u < kUnroll; u += 2) {
       acc = fma(v[u], xv[u], acc);
@@ -289,18 +303,81 @@ __device__ __noinline__ double seg_dot(const double* __restrict__ vals,
   return warp_sum(acc + acc2);
 }
 
+// The same with each lane loading adjacent entry pairs: one 16-byte value load
+// and one 4-byte column load per pair, so kPairs pairs per lane and round keep
+// 64 * kPairs entries in flight per warp for 5 registers a pair (twice the
+// entries of the scalar form for 8 more registers), and an item of kSeg
+// entries takes two exposed load round trips instead of four.  Pairs start at
+// an even absolute entry index; the odd neighbours of s and e are loaded and
+// masked (the far arrays are padded by two entries).
+template <int kPairs, bool kInPlace, bool kRemote = false>
+__device__ __noinline__ double seg_dot_pairs(const double* __restrict__ vals,
+                                                const uint16_t* __restrict__ cols, int s, int e,
+                                                const double* sol, int lane, unsigned ns,
+                                                const int* done, int need, unsigned ns_max) {
+  double acc = 0.0, acc2 = 0.0;
+  const int odd = static_cast<int>((reinterpret_cast<unsigned long long>(vals + s) >> 3) & 1);
+  for (int base = s - odd; base < e; base += 64 * kPairs) {
+    double2 v[kPairs];
+    unsigned c[kPairs];
+#pragma unroll
+    for (int u = 0; u < kPairs; ++u) {
+      const int k = base + 2 * (lane + 32 * u);
+      if (k < e) {
+        v[u] = __ldg(reinterpret_cast<const double2*>(vals + k));
+        c[u] = __ldg(reinterpret_cast<const unsigned*>(cols + k));
+      } else {
+        v[u] = make_double2(0.0, 0.0);
+        c[u] = 0;
+      }
+    }
+    if (base == s - odd) {
+      for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max))
+        __nanosleep(sl);
+    }
+    const volatile double* vs = sol;
+    double x0[kPairs], x1[kPairs];
+    bool pending = false;
+#pragma unroll
+    for (int u = 0; u < kPairs; ++u) {
+      const int k = base + 2 * (lane + 32 * u);
+      const bool in0 = k >= s && k < e, in1 = k + 1 < e;  // k + 1 >= s always
+      if (!in0) v[u].x = 0.0;
+      if (!in1) v[u].y = 0.0;
+      x0[u] = in0 ? vs[c[u] & 0xffffu] : 0.0;
+      x1[u] = in1 ? vs[c[u] >> 16] : 0.0;
+      pending |= is_pending(x0[u]) | is_pending(x1[u]);
+    }
+    while (!kInPlace && __any_sync(0xffffffffu, pending)) {
+      __nanosleep(ns);
+      pending = false;
+#pragma unroll
+      for (int u = 0; u < kPairs; ++u) {
+        if (is_pending(x0[u])) x0[u] = vs[c[u] & 0xffffu];
+        if (is_pending(x1[u])) x1[u] = vs[c[u] >> 16];
+        pending |= is_pending(x0[u]) | is_pending(x1[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kPairs; ++u) {
+      acc = fma(v[u].x, x0[u], acc);
+      acc2 = fma(v[u].y, x1[u], acc2);
+    }
+  }
+  return warp_sum(acc + acc2);
+}
+
 // A multi-row item: rows [row0, row0 + span) of one tile, entries [s, e)
 // (at most 32 * kUnroll).  One round of loads for all rows; each product goes
 // to the warp's shared scratch and lane r sums row r's run in entry order.
 // Returns lane r's row sum (and whether row r has entries).
-template <int kUnroll, int kWait, bool kRemote = false>
+template <int kUnroll, bool kInPlace, bool kRemote = false>
 __device__ __noinline__ double group_dot(const double* __restrict__ vals,
                                             const uint16_t* __restrict__ cols, int s, int e,
                                             const int* rp, int row0, int span,
                                             const double* sol, double* scratch, int lane,
                                             unsigned ns, const int* done, int need,
                                             unsigned ns_max, bool& has) {
-  constexpr bool kInPlace = kWait != kWaitValue;
   double v[kUnroll];
   int c[kUnroll];
 #pragma unroll
@@ -312,7 +389,7 @@ __device__ __noinline__ double group_dot(const double* __restrict__ vals,
   const bool mine = lane < span;
   const int rb = mine ? __ldg(rp + row0 + lane) : 0;
   const int re = mine ? __ldg(rp + row0 + lane + 1) : 0;
-  wait_tiles<kWait, kRemote>(done, need, ns, ns_max);
+  for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max)) __nanosleep(sl);
   const volatile double* vs = sol;
   double xv[kUnroll];
   bool pending = false;
@@ -440,18 +517,14 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
 // store their partial sums into the home CTA's slots.  Used when the blocks
 // are too few to fill the GPU (cfg2 / cfg3): a block's far entries then
 // stream through kCluster SMs instead of one.
-// kTileBars (in place, single CTA): U readiness through one mbarrier per tile
-// (kWaitTile) instead of the release/acquire counter.
 template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer,
-          int kCluster = 1, bool kTileBars = false>
+          int kCluster = 1>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
   constexpr int kFirstWorker = kProducer ? 2 : 1;
   constexpr int kWorkers = kWarps - kFirstWorker;
   constexpr bool kCl = kCluster > 1;
-  static_assert(!kTileBars || (kInPlace && !kCl), "tile barriers: in-place single-CTA solve");
-  constexpr int kWaitU = !kInPlace ? kWaitValue : (kTileBars ? kWaitTile : kWaitAcquire);
   // workers of the whole cluster: the home CTA's, then warps 1.. of the
   // others (warp 0 of a remote CTA pulls the solution, see below)
   constexpr int kAllWorkers = kWorkers + (kCluster - 1) * (kWarps - 1);
@@ -463,7 +536,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
   double* rbuf = scratch + kWorkers * kGroupEntries;  // solver: the tile's residuals
-  uint64_t* tbar = reinterpret_cast<uint64_t*>(rbuf + kTile);  // U tile solved (kTileBars)
   __shared__ __align__(8) uint64_t bars[kRing];   // near item landed (TMA)
   __shared__ __align__(8) uint64_t empty[kRing];  // near item consumed (producer variant)
   __shared__ int done_l, done_u;
@@ -493,8 +565,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (!kInPlace) x[i] = i < n ? pend : 0.0;
   }
   for (int i = threadIdx.x; i < a.max_slots; i += blockDim.x) part[i] = pend;
-  if constexpr (kTileBars)
-    for (int t = threadIdx.x; t < nt; t += blockDim.x) mbar_init(&tbar[t], 1);
   if (threadIdx.x == 0) {
     done_l = 0;
     done_u = 0;
@@ -659,13 +729,18 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int my = lane < span ? a.lslot[r0 + i + lane] : 0;
         bool has;
         const double acc =
-            group_dot<kGroupEntries / 32, kWaitValue>(fv, fc, d.z, d.w, rp, i, span, zh, scr, lane,
+            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, span, zh, scr, lane,
                                                  a.sleep_ns, done_lh, d.y >> 8, a.sleep_max, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, kWaitValue>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
-                                                        done_lh, d.y >> 8, a.sleep_max);
+#ifdef MSCG_PAIRS
+        const double acc = seg_dot_pairs<kUnroll, false>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
+                                                         done_lh, d.y >> 8, a.sleep_max);
+#else
+        const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
+                                                   done_lh, d.y >> 8, a.sleep_max);
+#endif
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
@@ -711,9 +786,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
-        if constexpr (kTileBars) {
-          mbar_arrive(&tbar[tt]);  // release: the tile's x is visible to whoever acquires it
-        } else if (kInPlace) {
+        if (kInPlace) {
           if constexpr (kCl) {
             // cluster scope: the remote pullers acquire it before copying x
             st_release_cluster(&done_u, tt + 1);
@@ -776,7 +849,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const long long lit = a.lnum[b];
     const int* rp = a.urp + r0 + b;
     double* scr = scratch + lw * kGroupEntries;
-    const int* wait_u = kTileBars ? reinterpret_cast<const int*>(tbar) : done_uh;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_u && w + kAllWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kAllWorkers * lane];
@@ -797,14 +869,19 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int span = (k & 0x7f) + 1;
         const int my = lane < span ? a.uslot[r0 + i + lane] : 0;
         bool has;
-        const double acc = group_dot<kGroupEntries / 32, kWaitU>(
-            fv, fc, d.z, d.w, rp, i, span, xh, scr, lane, a.sleep_ns, wait_u, d.y >> 8,
+        const double acc = group_dot<kGroupEntries / 32, kInPlace>(
+            fv, fc, d.z, d.w, rp, i, span, xh, scr, lane, a.sleep_ns, done_uh, d.y >> 8,
             a.sleep_max, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, kWaitU>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
-                                                         wait_u, d.y >> 8, a.sleep_max);
+#ifdef MSCG_PAIRS
+        const double acc = seg_dot_pairs<kUnroll, kInPlace>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
+                                                            done_uh, d.y >> 8, a.sleep_max);
+#else
+        const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
+                                                      done_uh, d.y >> 8, a.sleep_max);
+#endif
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
@@ -829,8 +906,7 @@ size_t smem_bytes(int dim_max, int workers, int slots) {
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
                            ((static_cast<size_t>(slots) + 1) & ~static_cast<size_t>(1)) +
                            (kInPlace ? 1 : 2) * dpad +
-                           static_cast<size_t>(workers) * kGroupEntries + kTile +
-                           dpad / kTile);  // + one mbarrier per tile (kTileBars)
+                           static_cast<size_t>(workers) * kGroupEntries + kTile);
 }
 
 }  // namespace
@@ -923,12 +999,6 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const char* e = getenv("MSCG_TRI_VARIANT");
     return e ? atoi(e) : 0;
   }();
-  // U readiness in the in-place kernels: per-tile mbarriers (1) or the
-  // release/acquire counter (0)
-  static const bool tile_bars = [] {
-    const char* e = getenv("MSCG_TRI_TILEBARS");
-    return e ? atoi(e) != 0 : false;
-  }();
   auto check_smem = [&](size_t smem) {
     if (smem > 227 * 1024)
       throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
@@ -1006,10 +1076,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       return;
   }
   if (variant == 0 && npos <= sms && d > 1024) {
-    if (tile_bars)
-      launch(trisolve_kernel<32, 4, 1, true, false, 1, true>, 32, smem_bytes<true>(d, 31, ns));
-    else
-      launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
+    launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
     MSCG_CUDA(cudaGetLastError());
     return;
   }
@@ -1032,8 +1099,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const int head = npos - tail;
     check_smem(smem_bytes<true>(d, 31, ns));
     {
-      auto k16 = tile_bars ? trisolve_kernel<16, 4, 2, true, false, 1, true>
-                           : trisolve_kernel<16, 4, 2, true, false>;
+      auto k16 = trisolve_kernel<16, 4, 2, true, false>;
       const size_t sm16 = smem_bytes<true>(d, 15, ns);
       ensure_smem(reinterpret_cast<const void*>(k16), sm16);
       k16<<<head, 16 * 32, sm16, s>>>(a, rhs, out, sub);
@@ -1042,8 +1108,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     {
       TriArgs at = a;
       at.pos0 = pos0 + head;
-      auto k32 = tile_bars ? trisolve_kernel<32, 4, 1, true, false, 1, true>
-                           : trisolve_kernel<32, 4, 1, true, false>;
+      auto k32 = trisolve_kernel<32, 4, 1, true, false>;
       const size_t sm32 = smem_bytes<true>(d, 31, ns);
       ensure_smem(reinterpret_cast<const void*>(k32), sm32);
       k32<<<tail, 32 * 32, sm32, fs.tail_stream>>>(at, rhs, out, sub);
@@ -1070,10 +1135,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       launch(trisolve_kernel<16, 4, 2, false, false>, 16, smem_bytes<false>(d, 15, ns));
       break;
     default:  // 2 CTAs/SM (64 registers), x overwrites z in place
-      if (tile_bars)
-        launch(trisolve_kernel<16, 4, 2, true, false, 1, true>, 16, smem_bytes<true>(d, 15, ns));
-      else
-        launch(trisolve_kernel<16, 4, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
+      launch(trisolve_kernel<16, 4, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
       break;
   }
   MSCG_CUDA(cudaGetLastError());
