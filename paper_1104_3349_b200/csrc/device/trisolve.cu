@@ -303,81 +303,20 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
   return warp_sum(acc + acc2);
 }
 
-// The same with each lane loading adjacent entry pairs: one 16-byte value load
-// and one 4-byte column load per pair, so kPairs pairs per lane and round keep
-// 64 * kPairs entries in flight per warp for 5 registers a pair (twice the
-// entries of the scalar form for 8 more registers), and an item of kSeg
-// entries takes two exposed load round trips instead of four.  Pairs start at
-// an even absolute entry index; the odd neighbours of s and e are loaded and
-// masked (the far arrays are padded by two entries).
-template <int kPairs, bool kInPlace, bool kRemote = false>
-__device__ __noinline__ double seg_dot_pairs(const double* __restrict__ vals,
-                                                const uint16_t* __restrict__ cols, int s, int e,
-                                                const double* sol, int lane, unsigned ns,
-                                                const int* done, int need, unsigned ns_max) {
-  double acc = 0.0, acc2 = 0.0;
-  const int odd = static_cast<int>((reinterpret_cast<unsigned long long>(vals + s) >> 3) & 1);
-  for (int base = s - odd; base < e; base += 64 * kPairs) {
-    double2 v[kPairs];
-    unsigned c[kPairs];
-#pragma unroll
-    for (int u = 0; u < kPairs; ++u) {
-      const int k = base + 2 * (lane + 32 * u);
-      if (k < e) {
-        v[u] = __ldg(reinterpret_cast<const double2*>(vals + k));
-        c[u] = __ldg(reinterpret_cast<const unsigned*>(cols + k));
-      } else {
-        v[u] = make_double2(0.0, 0.0);
-        c[u] = 0;
-      }
-    }
-    if (base == s - odd) {
-      for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max))
-        __nanosleep(sl);
-    }
-    const volatile double* vs = sol;
-    double x0[kPairs], x1[kPairs];
-    bool pending = false;
-#pragma unroll
-    for (int u = 0; u < kPairs; ++u) {
-      const int k = base + 2 * (lane + 32 * u);
-      const bool in0 = k >= s && k < e, in1 = k + 1 < e;  // k + 1 >= s always
-      if (!in0) v[u].x = 0.0;
-      if (!in1) v[u].y = 0.0;
-      x0[u] = in0 ? vs[c[u] & 0xffffu] : 0.0;
-      x1[u] = in1 ? vs[c[u] >> 16] : 0.0;
-      pending |= is_pending(x0[u]) | is_pending(x1[u]);
-    }
-    while (!kInPlace && __any_sync(0xffffffffu, pending)) {
-      __nanosleep(ns);
-      pending = false;
-#pragma unroll
-      for (int u = 0; u < kPairs; ++u) {
-        if (is_pending(x0[u])) x0[u] = vs[c[u] & 0xffffu];
-        if (is_pending(x1[u])) x1[u] = vs[c[u] >> 16];
-        pending |= is_pending(x0[u]) | is_pending(x1[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kPairs; ++u) {
-      acc = fma(v[u].x, x0[u], acc);
-      acc2 = fma(v[u].y, x1[u], acc2);
-    }
-  }
-  return warp_sum(acc + acc2);
-}
-
 // A multi-row item: rows [row0, row0 + span) of one tile, entries [s, e)
 // (at most 32 * kUnroll).  One round of loads for all rows; each product goes
-// to the warp's shared scratch and lane r sums row r's run in entry order.
-// Returns lane r's row sum (and whether row r has entries).
+// to the warp's shared scratch.  Row r is summed by the P = 32 / span (rounded
+// down to a power of two) lanes r * P .. r * P + P - 1: lane `sub` of the row
+// adds every P-th product of the row's run and the P partial sums meet in a
+// fixed butterfly (deterministic).  The first lane of each row returns the row
+// sum, with the row's far-sum slot in `my` (has = the row has entries).
 template <int kUnroll, bool kInPlace, bool kRemote = false>
-__device__ __noinline__ double group_dot(const double* __restrict__ vals,
-                                            const uint16_t* __restrict__ cols, int s, int e,
-                                            const int* rp, int row0, int span,
-                                            const double* sol, double* scratch, int lane,
-                                            unsigned ns, const int* done, int need,
-                                            unsigned ns_max, bool& has) {
+__device__ __forceinline__ double group_dot(const double* __restrict__ vals,
+                                             const uint16_t* __restrict__ cols, int s, int e,
+                                             const int* rp, const int* slots, int row0, int span,
+                                             const double* sol, double* scratch, int lane,
+                                             unsigned ns, const int* done, int need,
+                                             unsigned ns_max, int& my, bool& has) {
   double v[kUnroll];
   int c[kUnroll];
 #pragma unroll
@@ -386,9 +325,12 @@ __device__ __noinline__ double group_dot(const double* __restrict__ vals,
     v[u] = k < e ? __ldg(vals + k) : 0.0;
     c[u] = k < e ? __ldg(cols + k) : -1;
   }
-  const bool mine = lane < span;
-  const int rb = mine ? __ldg(rp + row0 + lane) : 0;
-  const int re = mine ? __ldg(rp + row0 + lane + 1) : 0;
+  const int lg = 31 - __clz(32 / span);  // log2 of the lanes per row
+  const int r = lane >> lg, sub = lane & ((1 << lg) - 1);
+  const bool mine = r < span;
+  const int rb = mine ? __ldg(rp + row0 + r) : 0;
+  const int re = mine ? __ldg(rp + row0 + r + 1) : 0;
+  my = mine && sub == 0 ? __ldg(slots + row0 + r) : 0;
   for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max)) __nanosleep(sl);
   const volatile double* vs = sol;
   double xv[kUnroll];
@@ -411,9 +353,10 @@ __device__ __noinline__ double group_dot(const double* __restrict__ vals,
   for (int u = 0; u < kUnroll; ++u) scratch[lane + 32 * u] = v[u] * xv[u];
   __syncwarp();
   double acc = 0.0;
-  for (int k = rb; k < re; ++k) acc += scratch[k - s];
-  __syncwarp();  // scratch is reused by the warp's next item
-  has = re > rb;
+  for (int k = rb + sub; k < re; k += 1 << lg) acc += scratch[k - s];
+  __syncwarp();  // converged again; scratch is reused by the warp's next item
+  for (int off = (1 << lg) >> 1; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  has = re > rb && sub == 0;
   return acc;
 }
 
@@ -726,21 +669,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (rt) rt[0] = clock64();
       if (k & kMultiFlag) {
         const int span = (k & 0x7f) + 1;
-        const int my = lane < span ? a.lslot[r0 + i + lane] : 0;
+        int my;
         bool has;
-        const double acc =
-            group_dot<kGroupEntries / 32, false>(fv, fc, d.z, d.w, rp, i, span, zh, scr, lane,
-                                                 a.sleep_ns, done_lh, d.y >> 8, a.sleep_max, has);
+        const double acc = group_dot<kGroupEntries / 32, false>(
+            fv, fc, d.z, d.w, rp, a.lslot + r0, i, span, zh, scr, lane, a.sleep_ns, done_lh,
+            d.y >> 8, a.sleep_max, my, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-#ifdef MSCG_PAIRS
-        const double acc = seg_dot_pairs<kUnroll, false>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
-                                                         done_lh, d.y >> 8, a.sleep_max);
-#else
         const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
                                                    done_lh, d.y >> 8, a.sleep_max);
-#endif
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
@@ -867,21 +805,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (rt) rt[0] = clock64();
       if (k & kMultiFlag) {
         const int span = (k & 0x7f) + 1;
-        const int my = lane < span ? a.uslot[r0 + i + lane] : 0;
+        int my;
         bool has;
         const double acc = group_dot<kGroupEntries / 32, kInPlace>(
-            fv, fc, d.z, d.w, rp, i, span, xh, scr, lane, a.sleep_ns, done_uh, d.y >> 8,
-            a.sleep_max, has);
+            fv, fc, d.z, d.w, rp, a.uslot + r0, i, span, xh, scr, lane, a.sleep_ns, done_uh,
+            d.y >> 8, a.sleep_max, my, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-#ifdef MSCG_PAIRS
-        const double acc = seg_dot_pairs<kUnroll, kInPlace>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
-                                                            done_uh, d.y >> 8, a.sleep_max);
-#else
         const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
                                                       done_uh, d.y >> 8, a.sleep_max);
-#endif
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
