@@ -177,6 +177,33 @@ template <bool kAcquire, bool kRemote = false>
 __device__ __forceinline__ int poll(const int* p) {
   return kAcquire ? (kRemote ? ld_acquire_cluster(p) : ld_acquire(p)) : vload(p);
 }
+// How a worker learns that `need` tiles of the pass are solved:
+//   kWaitValue   relaxed counter as a hint, the solution slots' sentinels as
+//                the guarantee (cluster solves: x kept apart from z, values
+//                pulled over DSMEM);
+//   kWaitAcquire the counter read with acquire (x overwrites z in place: a
+//                value's presence cannot mark readiness);
+//   kWaitTile    one mbarrier per tile and pass: the solver's arrive releases
+//                the tile's stores, try_wait acquires them and suspends the
+//                warp in hardware; no sentinel tests in the dot loops (the
+//                streaming phases are issue-bound).
+constexpr int kWaitValue = 0, kWaitAcquire = 1, kWaitTile = 2;
+template <int kWait, bool kRemote>
+__device__ __forceinline__ void wait_tiles(const int* done, int need, unsigned ns,
+                                           unsigned ns_max, unsigned parity) {
+  if constexpr (kWait == kWaitTile) {
+    if (need > 0)
+      mbar_wait(reinterpret_cast<uint64_t*>(const_cast<int*>(done)) + (need - 1), parity);
+  } else {
+    // every lane polls the same word: the loop exit is warp-uniform, so the
+    // warp stays converged (divergent spins cost the shuffles afterwards
+    // their fast path).  Exponential back-off: the solver finishes a tile
+    // every few microseconds and short polls would steal its issue slots.
+    for (unsigned sl = ns; poll<kWait == kWaitAcquire, kRemote>(done) < need;
+         sl = min(2 * sl, ns_max))
+      __nanosleep(sl);
+  }
+}
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -214,21 +241,18 @@ __device__ __forceinline__ Slice aligned_slice(const double* p, int len) {
 // instead of per-lane loop bounds) so the final reduction runs converged.
 // The first round's loads are issued before the readiness wait (one poll
 // per warp on the tile counter).
-template <int kUnroll, bool kInPlace, bool kRemote = false>
+template <int kUnroll, int kWait, bool kRemote = false>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const uint16_t* __restrict__ cols, int s, int e,
                                           const double* sol, int lane, unsigned ns,
-                                          const int* done, int need, unsigned ns_max) {
+                                          const int* done, int need, unsigned ns_max,
+                                          unsigned parity) {
+  constexpr bool kInPlace = kWait != kWaitValue;  // no sentinel tests
   double acc = 0.0, acc2 = 0.0;
   const volatile double* vs = sol;
   bool waited = false;
-  // every lane polls the same word: the loop exit is warp-uniform, so the
-  // warp stays converged (divergent spins cost the shuffles below their fast
-  // path).  Exponential back-off: the solver finishes a tile every few
-  // microseconds and short polls would steal its issue slots.
   auto wait = [&]() {
-    for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max))
-      __nanosleep(sl);
+    wait_tiles<kWait, kRemote>(done, need, ns, ns_max, parity);
     waited = true;
   };
   // Gather operands (independent shared loads); poll only if one is still
@@ -310,13 +334,15 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
 // adds every P-th product of the row's run and the P partial sums meet in a
 // fixed butterfly (deterministic).  The first lane of each row returns the row
 // sum, with the row's far-sum slot in `my` (has = the row has entries).
-template <int kUnroll, bool kInPlace, bool kRemote = false>
+template <int kUnroll, int kWait, bool kRemote = false>
 __device__ __forceinline__ double group_dot(const double* __restrict__ vals,
                                              const uint16_t* __restrict__ cols, int s, int e,
                                              const int* rp, const int* slots, int row0, int span,
                                              const double* sol, double* scratch, int lane,
                                              unsigned ns, const int* done, int need,
-                                             unsigned ns_max, int& my, bool& has) {
+                                             unsigned ns_max, unsigned parity, int& my,
+                                             bool& has) {
+  constexpr bool kInPlace = kWait != kWaitValue;
   double v[kUnroll];
   int c[kUnroll];
 #pragma unroll
@@ -331,7 +357,7 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ vals,
   const int rb = mine ? __ldg(rp + row0 + r) : 0;
   const int re = mine ? __ldg(rp + row0 + r + 1) : 0;
   my = mine && sub == 0 ? __ldg(slots + row0 + r) : 0;
-  for (unsigned sl = ns; poll<kInPlace, kRemote>(done) < need; sl = min(2 * sl, ns_max)) __nanosleep(sl);
+  wait_tiles<kWait, kRemote>(done, need, ns, ns_max, parity);
   const volatile double* vs = sol;
   double xv[kUnroll];
   bool pending = false;
@@ -460,14 +486,26 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
 // store their partial sums into the home CTA's slots.  Used when the blocks
 // are too few to fill the GPU (cfg2 / cfg3): a block's far entries then
 // stream through kCluster SMs instead of one.
+// kTileBars (in-place single-CTA solves): readiness of both passes through
+// one mbarrier per tile (kWaitTile; phase 0 = the L pass, phase 1 = the U
+// pass) instead of the release/acquire counters: cfg5 D-solve 6.86 -> 6.78 ms.
+// Costs 8 bytes of shared memory per tile, so the launcher falls back to the
+// counters when that would cost the second CTA per SM.
 template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer,
-          int kCluster = 1>
+          int kCluster = 1, bool kTileBars = false>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
   constexpr int kFirstWorker = kProducer ? 2 : 1;
   constexpr int kWorkers = kWarps - kFirstWorker;
   constexpr bool kCl = kCluster > 1;
+  static_assert(!kTileBars || (kInPlace && !kCl), "tile barriers: in-place single-CTA solve");
+  // in-place single-CTA solves publish the L pass like the U pass
+  // (release/acquire counter): no sentinel tests in the workers' dot loops,
+  // which are issue-bound (cfg5 D-solve 7.05 -> 6.86 ms)
+  constexpr bool kAcqL = kInPlace && !kCl && !kTileBars;
+  constexpr int kWaitL = kTileBars ? kWaitTile : (kAcqL ? kWaitAcquire : kWaitValue);
+  constexpr int kWaitU = !kInPlace ? kWaitValue : (kTileBars ? kWaitTile : kWaitAcquire);
   // workers of the whole cluster: the home CTA's, then warps 1.. of the
   // others (warp 0 of a remote CTA pulls the solution, see below)
   constexpr int kAllWorkers = kWorkers + (kCluster - 1) * (kWarps - 1);
@@ -479,6 +517,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
   double* rbuf = scratch + kWorkers * kGroupEntries;  // solver: the tile's residuals
+  // kTileBars: tbar[t] completes phase 0 with L tile t, phase 1 with the
+  // t-th tile of the U pass
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(rbuf + kTile);
   __shared__ __align__(8) uint64_t bars[kRing];   // near item landed (TMA)
   __shared__ __align__(8) uint64_t empty[kRing];  // near item consumed (producer variant)
   __shared__ int done_l, done_u;
@@ -508,6 +549,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (!kInPlace) x[i] = i < n ? pend : 0.0;
   }
   for (int i = threadIdx.x; i < a.max_slots; i += blockDim.x) part[i] = pend;
+  if constexpr (kTileBars)
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) mbar_init(&tbar[t], 1);
   if (threadIdx.x == 0) {
     done_l = 0;
     done_u = 0;
@@ -604,7 +647,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();  // every lane is done with the slot
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
-        *reinterpret_cast<volatile int*>(&done_l) = t + 1;
+        if constexpr (kTileBars)
+          mbar_arrive(&tbar[t]);  // release: the tile's z is visible to whoever acquires it
+        else if constexpr (kAcqL)
+          st_release(&done_l, t + 1);
+        else
+          *reinterpret_cast<volatile int*>(&done_l) = t + 1;
         if (tr) tr[4 * t + 2] = clock64();
         if (!kProducer && t + kRing < 2 * nt) issue(t + kRing, next_bytes(t));
       }
@@ -651,6 +699,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const int nitems = a.lnum[b];
     const int* rp = a.lrp + r0 + b;
     double* scr = scratch + lw * kGroupEntries;
+    const int* wait_l = kTileBars ? reinterpret_cast<const int*>(tbar) : done_lh;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_items && w + kAllWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kAllWorkers * lane];
@@ -663,6 +712,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int4 f = items[it + kAllWorkers * a.pf_items];
         prefetch_far(fv, fc, f.z, f.w);
       }
+
       const int i = d.x & 0xffff, k = d.y & 0xff;
       const int slot = static_cast<int>(static_cast<unsigned>(d.x) >> 16);
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * it : nullptr;
@@ -671,14 +721,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int span = (k & 0x7f) + 1;
         int my;
         bool has;
-        const double acc = group_dot<kGroupEntries / 32, false>(
-            fv, fc, d.z, d.w, rp, a.lslot + r0, i, span, zh, scr, lane, a.sleep_ns, done_lh,
-            d.y >> 8, a.sleep_max, my, has);
+        const double acc = group_dot<kGroupEntries / 32, kWaitL>(
+            fv, fc, d.z, d.w, rp, a.lslot + r0, i, span, zh, scr, lane, a.sleep_ns, wait_l,
+            d.y >> 8, a.sleep_max, 0u, my, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, false>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
-                                                   done_lh, d.y >> 8, a.sleep_max);
+        const double acc = seg_dot<kUnroll, kWaitL>(fv, fc, d.z, d.w, zh, lane, a.sleep_ns,
+                                                    wait_l, d.y >> 8, a.sleep_max, 0u);
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
@@ -724,7 +774,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
       if (lane == 0) {
         if (kProducer) mbar_arrive(&empty[slot]);
-        if (kInPlace) {
+        if constexpr (kTileBars) {
+          mbar_arrive(&tbar[tt]);
+        } else if (kInPlace) {
           if constexpr (kCl) {
             // cluster scope: the remote pullers acquire it before copying x
             st_release_cluster(&done_u, tt + 1);
@@ -787,6 +839,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const long long lit = a.lnum[b];
     const int* rp = a.urp + r0 + b;
     double* scr = scratch + lw * kGroupEntries;
+    const int* wait_u = kTileBars ? reinterpret_cast<const int*>(tbar) : done_uh;
     int4 nxt = w < nitems ? items[w] : make_int4(0, 0, 0, 0);
     if (lane < a.pf_u && w + kAllWorkers * lane < nitems) {  // warm the first items
       const int4 d = items[w + kAllWorkers * lane];
@@ -799,6 +852,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int4 f = items[it + kAllWorkers * a.pf_u];
         prefetch_far(fv, fc, f.z, f.w);
       }
+
       const int i = d.x & 0xffff, k = d.y & 0xff;
       const int slot = static_cast<int>(static_cast<unsigned>(d.x) >> 16);
       long long* rt = (tr && lane == 0) ? tr + 8LL * nt + 4LL * (lit + it) : nullptr;
@@ -807,14 +861,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const int span = (k & 0x7f) + 1;
         int my;
         bool has;
-        const double acc = group_dot<kGroupEntries / 32, kInPlace>(
-            fv, fc, d.z, d.w, rp, a.uslot + r0, i, span, xh, scr, lane, a.sleep_ns, done_uh,
-            d.y >> 8, a.sleep_max, my, has);
+        const double acc = group_dot<kGroupEntries / 32, kWaitU>(
+            fv, fc, d.z, d.w, rp, a.uslot + r0, i, span, xh, scr, lane, a.sleep_ns, wait_u,
+            d.y >> 8, a.sleep_max, 1u, my, has);
         if (rt) rt[1] = clock64();
         if (has) *reinterpret_cast<volatile double*>(parth + my) = acc;
       } else {
-        const double acc = seg_dot<kUnroll, kInPlace>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
-                                                      done_uh, d.y >> 8, a.sleep_max);
+        const double acc = seg_dot<kUnroll, kWaitU>(fv, fc, d.z, d.w, xh, lane, a.sleep_ns,
+                                                    wait_u, d.y >> 8, a.sleep_max, 1u);
         if (rt) rt[1] = clock64();
         if (lane == 0) *reinterpret_cast<volatile double*>(parth + slot) = acc;
       }
@@ -834,12 +888,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 }
 
 template <bool kInPlace>
-size_t smem_bytes(int dim_max, int workers, int slots) {
+size_t smem_bytes(int dim_max, int workers, int slots, bool tile_bars = false) {
   const size_t dpad = (static_cast<size_t>(dim_max) + kTile - 1) & ~static_cast<size_t>(kTile - 1);
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
                            ((static_cast<size_t>(slots) + 1) & ~static_cast<size_t>(1)) +
                            (kInPlace ? 1 : 2) * dpad +
-                           static_cast<size_t>(workers) * kGroupEntries + kTile);
+                           static_cast<size_t>(workers) * kGroupEntries + kTile +
+                           (tile_bars ? dpad / kTile : 0));  // one mbarrier per tile
 }
 
 }  // namespace
@@ -932,6 +987,14 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const char* e = getenv("MSCG_TRI_VARIANT");
     return e ? atoi(e) : 0;
   }();
+  // Readiness through per-tile mbarriers (MSCG_TRI_TILEBARS=0: the
+  // release/acquire counters).  With two CTAs per SM the barriers must not
+  // cost the second CTA: 228 KB per SM, 1 KB reserved per CTA.
+  static const bool tb_env = [] {
+    const char* e = getenv("MSCG_TRI_TILEBARS");
+    return e ? atoi(e) != 0 : true;
+  }();
+  constexpr size_t kTwoPerSm = (228 * 1024 - 2 * 1024) / 2 - 128;  // less the static part
   auto check_smem = [&](size_t smem) {
     if (smem > 227 * 1024)
       throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
@@ -1009,7 +1072,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       return;
   }
   if (variant == 0 && npos <= sms && d > 1024) {
-    launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
+    if (tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024)
+      launch(trisolve_kernel<32, 4, 1, true, false, 1, true>, 32, smem_bytes<true>(d, 31, ns, true));
+    else
+      launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
     MSCG_CUDA(cudaGetLastError());
     return;
   }
@@ -1032,8 +1098,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const int head = npos - tail;
     check_smem(smem_bytes<true>(d, 31, ns));
     {
-      auto k16 = trisolve_kernel<16, 4, 2, true, false>;
-      const size_t sm16 = smem_bytes<true>(d, 15, ns);
+      const bool tb = tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm;
+      auto k16 = tb ? trisolve_kernel<16, 4, 2, true, false, 1, true>
+                    : trisolve_kernel<16, 4, 2, true, false>;
+      const size_t sm16 = smem_bytes<true>(d, 15, ns, tb);
       ensure_smem(reinterpret_cast<const void*>(k16), sm16);
       k16<<<head, 16 * 32, sm16, s>>>(a, rhs, out, sub);
       MSCG_CUDA(cudaGetLastError());
@@ -1041,8 +1109,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     {
       TriArgs at = a;
       at.pos0 = pos0 + head;
-      auto k32 = trisolve_kernel<32, 4, 1, true, false>;
-      const size_t sm32 = smem_bytes<true>(d, 31, ns);
+      const bool tb = tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024;
+      auto k32 = tb ? trisolve_kernel<32, 4, 1, true, false, 1, true>
+                    : trisolve_kernel<32, 4, 1, true, false>;
+      const size_t sm32 = smem_bytes<true>(d, 31, ns, tb);
       ensure_smem(reinterpret_cast<const void*>(k32), sm32);
       k32<<<tail, 32 * 32, sm32, fs.tail_stream>>>(at, rhs, out, sub);
       MSCG_CUDA(cudaGetLastError());
@@ -1068,7 +1138,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       launch(trisolve_kernel<16, 4, 2, false, false>, 16, smem_bytes<false>(d, 15, ns));
       break;
     default:  // 2 CTAs/SM (64 registers), x overwrites z in place
-      launch(trisolve_kernel<16, 4, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
+      if (tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
+        launch(trisolve_kernel<16, 4, 2, true, false, 1, true>, 16,
+               smem_bytes<true>(d, 15, ns, true));
+      else
+        launch(trisolve_kernel<16, 4, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
       break;
   }
   MSCG_CUDA(cudaGetLastError());
