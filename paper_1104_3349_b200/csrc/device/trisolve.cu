@@ -135,15 +135,25 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// L2 prefetch of far entries [s, e) (values + columns), widened to 16 B.
+// L2 prefetch of far entries [s, e) (values + columns), widened to 16 B
+// (32-bit arithmetic on entry offsets: this runs once per work item in loops
+// that are issue-bound).
 __device__ __forceinline__ void prefetch_far(const double* v, const uint16_t* c, int s, int e) {
   if (e <= s) return;
-  const unsigned long long v0 = reinterpret_cast<unsigned long long>(v + s) & ~15ull;
-  const unsigned long long v1 = (reinterpret_cast<unsigned long long>(v + e) + 15) & ~15ull;
-  const unsigned long long c0 = reinterpret_cast<unsigned long long>(c + s) & ~15ull;
-  const unsigned long long c1 = (reinterpret_cast<unsigned long long>(c + e) + 15) & ~15ull;
-  l2_prefetch(reinterpret_cast<const void*>(v0), static_cast<unsigned>(v1 - v0));
-  l2_prefetch(reinterpret_cast<const void*>(c0), static_cast<unsigned>(c1 - c0));
+  const int mv = static_cast<int>(reinterpret_cast<unsigned long long>(v) >> 3) & 1;
+  const int mc = static_cast<int>(reinterpret_cast<unsigned long long>(c) >> 1) & 7;
+  const int sv = s - ((s + mv) & 1), ev = e + ((e + mv) & 1);
+  const int sc = s - ((s + mc) & 7), ec = e + ((-(e + mc)) & 7);
+  l2_prefetch(v + sv, 8u * static_cast<unsigned>(ev - sv));
+  l2_prefetch(c + sc, 2u * static_cast<unsigned>(ec - sc));
+}
+
+// Entry c of the solution vector at shared-window address `base` (32-bit
+// shared addressing: one address instruction per gather in the dot loops).
+__device__ __forceinline__ double sol_at(uint32_t base, int c) {
+  double x;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(x) : "r"(base + 8u * static_cast<uint32_t>(c)) : "memory");
+  return x;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -249,7 +259,7 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           unsigned parity) {
   constexpr bool kInPlace = kWait != kWaitValue;  // no sentinel tests
   double acc = 0.0, acc2 = 0.0;
-  const volatile double* vs = sol;
+  const uint32_t vs = smem_addr(sol);
   bool waited = false;
   auto wait = [&]() {
     wait_tiles<kWait, kRemote>(done, need, ns, ns_max, parity);
@@ -267,7 +277,7 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
       pending = false;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        if (c[u] >= 0 && is_pending(xv[u])) xv[u] = vs[c[u]];
+        if (c[u] >= 0 && is_pending(xv[u])) xv[u] = sol_at(vs, c[u]);
         pending |= is_pending(xv[u]);
       }
     }
@@ -291,7 +301,7 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
     if (!waited) wait();
     double xv[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) xv[u] = vs[c[u]];
+    for (int u = 0; u < kUnroll; ++u) xv[u] = sol_at(vs, c[u]);
     settle(xv, c);
 #pragma unroll
     for (int u = 0; u < kUnroll; u += 2) {
@@ -316,7 +326,7 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
     if (!waited) wait();
     double xv[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
+    for (int u = 0; u < kUnroll; ++u) xv[u] = c[u] >= 0 ? sol_at(vs, c[u]) : 0.0;
     settle(xv, c);
 #pragma unroll
     for (int u = 0; u < kUnroll; u += 2) {
@@ -358,12 +368,12 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ vals,
   const int re = mine ? __ldg(rp + row0 + r + 1) : 0;
   my = mine && sub == 0 ? __ldg(slots + row0 + r) : 0;
   wait_tiles<kWait, kRemote>(done, need, ns, ns_max, parity);
-  const volatile double* vs = sol;
+  const uint32_t vs = smem_addr(sol);
   double xv[kUnroll];
   bool pending = false;
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
-    xv[u] = c[u] >= 0 ? vs[c[u]] : 0.0;
+    xv[u] = c[u] >= 0 ? sol_at(vs, c[u]) : 0.0;
     pending |= is_pending(xv[u]);
   }
   while (!kInPlace && __any_sync(0xffffffffu, pending)) {
@@ -371,7 +381,7 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ vals,
     pending = false;
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      if (c[u] >= 0 && is_pending(xv[u])) xv[u] = vs[c[u]];
+      if (c[u] >= 0 && is_pending(xv[u])) xv[u] = sol_at(vs, c[u]);
       pending |= is_pending(xv[u]);
     }
   }
@@ -709,8 +719,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int4 d = nxt;
       if (it + kAllWorkers < nitems) nxt = items[it + kAllWorkers];
       if (lane == 0 && a.pf_items && it + kAllWorkers * a.pf_items < nitems) {
-        const int4 f = items[it + kAllWorkers * a.pf_items];
-        prefetch_far(fv, fc, f.z, f.w);
+        if (a.pf_items == 1) {  // the descriptor just loaded
+          prefetch_far(fv, fc, nxt.z, nxt.w);
+        } else {
+          const int4 f = items[it + kAllWorkers * a.pf_items];
+          prefetch_far(fv, fc, f.z, f.w);
+        }
       }
 
       const int i = d.x & 0xffff, k = d.y & 0xff;
@@ -849,8 +863,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int4 d = nxt;
       if (it + kAllWorkers < nitems) nxt = items[it + kAllWorkers];
       if (lane == 0 && a.pf_u && it + kAllWorkers * a.pf_u < nitems) {
-        const int4 f = items[it + kAllWorkers * a.pf_u];
-        prefetch_far(fv, fc, f.z, f.w);
+        if (a.pf_u == 1) {  // the descriptor just loaded
+          prefetch_far(fv, fc, nxt.z, nxt.w);
+        } else {
+          const int4 f = items[it + kAllWorkers * a.pf_u];
+          prefetch_far(fv, fc, f.z, f.w);
+        }
       }
 
       const int i = d.x & 0xffff, k = d.y & 0xff;
