@@ -501,8 +501,10 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
 // pass) instead of the release/acquire counters: cfg5 D-solve 6.86 -> 6.78 ms.
 // Costs 8 bytes of shared memory per tile, so the launcher falls back to the
 // counters when that would cost the second CTA per SM.
+// kTrace: clock stamps of block 0 (tools/trace_dsolve.py); a separate
+// instantiation, so the production kernels carry no trace tests.
 template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer,
-          int kCluster = 1, bool kTileBars = false>
+          int kCluster = 1, bool kTileBars = false, bool kTrace = false>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       __syncwarp();
     }
   };
-  long long* tr = (a.trace && b == 0 && home) ? a.trace : nullptr;
+  long long* tr = (kTrace && a.trace && b == 0 && home) ? a.trace : nullptr;
   const int j = lane;
 
   // ================================================================ L pass
@@ -1046,7 +1048,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     const char* e = getenv("MSCG_TRI_CLUSTER");
     return e ? atoi(e) : -1;
   }();
-  if (variant == 0 && d > 1024 && cl_env != 0 && npos * 2 <= sms) {
+  // (a traced solve always takes the default kernel: only it is instantiated
+  // with kTrace)
+  if (variant == 0 && d > 1024 && cl_env != 0 && npos * 2 <= sms && !trace) {
     // separate z and x (not in place): the U pass needs no cluster fence
     const size_t smc = smem_bytes<false>(d, 31, ns);
     check_smem(smc);
@@ -1089,7 +1093,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
         try_size(2, trisolve_kernel<32, 4, 1, false, false, 2>))
       return;
   }
-  if (variant == 0 && npos <= sms && d > 1024) {
+  if (variant == 0 && npos <= sms && d > 1024 && !trace) {
     if (tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024)
       launch(trisolve_kernel<32, 4, 1, true, false, 1, true>, 32, smem_bytes<true>(d, 31, ns, true));
     else
@@ -1103,7 +1107,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   // as SMs drain, instead of half-empty SMs at the end of one launch.
   const int tail = npos % (2 * sms);
   static const bool split_tail = getenv("MSCG_TRI_NO_TAIL") == nullptr;
-  if (split_tail && variant == 0 && chunk < 0 && d > 1024 && npos > 2 * sms && tail > 0 &&
+  if (split_tail && !trace && variant == 0 && chunk < 0 && d > 1024 && npos > 2 * sms && tail > 0 &&
       tail <= sms) {
     std::lock_guard<std::mutex> lk(fs.tail_mu);
     if (!fs.tail_stream) {
@@ -1156,7 +1160,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       launch(trisolve_kernel<16, 4, 2, false, false>, 16, smem_bytes<false>(d, 15, ns));
       break;
     default:  // 2 CTAs/SM (64 registers), x overwrites z in place
-      if (tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
+      if (trace && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
+        launch(trisolve_kernel<16, 4, 2, true, false, 1, true, true>, 16,
+               smem_bytes<true>(d, 15, ns, true));
+      else if (tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
         launch(trisolve_kernel<16, 4, 2, true, false, 1, true>, 16,
                smem_bytes<true>(d, 15, ns, true));
       else
