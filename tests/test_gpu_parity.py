@@ -334,6 +334,36 @@ def test_cfg2_ilut_and_apply(msc, ctx, rs, ref):
     assert rel_err(pc.apply(y), M.apply(y)) <= APPLY_TOL
 
 
+@pytest.mark.parametrize("env", [
+    {"MSCG_PACK_SLACK_U": "0"},                                # items by readiness alone
+    {"MSCG_PACK_SLACK_U": "3", "MSCG_PACK_SLACK_L": "5"},      # deadline-aware, both passes
+    {"MSCG_PACK_PIECES_L": "4", "MSCG_PACK_PIECES_U": "4"},    # long rows cut by readiness
+    {"MSCG_PACK_PIECES_L": "3", "MSCG_PACK_SLACK_U": "16"},
+])
+def test_work_item_policies_same_operator(msc, ctx, rs, ref, env, monkeypatch):
+    """The pack's work-item policy (how long far rows are cut, in which order
+    the workers take the items: factor.cu pack_tiled_kernel) only schedules
+    the interior solve: the stored factors stay the reference's bit for bit
+    and the apply stays within the bar (sums regrouped, nothing else)."""
+    pb = msc.oseen_problem(128, 0.01, 16)  # cfg2: ~3000-row blocks, long pressure rows
+    pb.build_msc("lum")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    pc = msc.build_preconditioner(pb, tolA=1e-4, sA=0, ctx=ctx)
+    M = oracle_msc(rs, pb, 1e-4, 0)
+    for b in (0, pb.nblocks - 1):
+        f, o = pc.d_factors(b), M.dfac[b]
+        assert np.array_equal(f.lower.row_offsets, o.lrp)
+        assert np.array_equal(f.lower.col_indices, o.lci)
+        assert same_bits(f.lower.values, o.lv) and same_bits(f.upper.values, o.uv)
+    for seed in (0, 1):
+        y = ref.random_vector(pb.n, seed)
+        assert rel_err(pc.apply(y), M.apply(y)) <= APPLY_TOL
+    # deterministic: the same launch twice gives the same bits
+    y = ref.random_vector(pb.n, 2)
+    assert same_bits(pc.apply(y), pc.apply(y))
+
+
 @pytest.mark.parametrize("nshards", [2, 3])
 def test_sharded_apply_and_spmv_match_full(msc, ctx, ref, nshards):
     """the interior blocks split over ranks, one n_g all-reduce
