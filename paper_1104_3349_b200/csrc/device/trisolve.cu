@@ -503,12 +503,21 @@ __device__ __forceinline__ int meta_int(const double* T, int idx) {
 // counters when that would cost the second CTA per SM.
 // kTrace: clock stamps of block 0 (tools/trace_dsolve.py); a separate
 // instantiation, so the production kernels carry no trace tests.
+// kSolvers = 2: warps 0 and 1 solve alternate tiles (item q belongs to warp
+// q & 1, which also owns ring slot q & 1 and refills it).  A tile's
+// prologue — waiting for its copy, metadata, collecting the far sums — and
+// its epilogue — the refill — need nothing from the previous tile, so they
+// run while the other warp is on the chain; only the neighbour window, the
+// tile-inverse dot and the publication stay on it.  The hand-off is the
+// tile's own publication (mbarrier phase or release/acquire counter).
 template <int kWarps, int kUnroll, int kMinBlocks, bool kInPlace, bool kProducer,
-          int kCluster = 1, bool kTileBars = false, bool kTrace = false>
+          int kCluster = 1, bool kTileBars = false, bool kTrace = false, int kSolvers = 1>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
-  constexpr int kFirstWorker = kProducer ? 2 : 1;
+  static_assert(kSolvers == 1 || (kSolvers == 2 && kRing == 2 && !kProducer),
+                "two solvers: one per ring slot");
+  constexpr int kFirstWorker = kProducer ? 2 : kSolvers;
   constexpr int kWorkers = kWarps - kFirstWorker;
   constexpr bool kCl = kCluster > 1;
   static_assert(!kTileBars || (kInPlace && !kCl), "tile barriers: in-place single-CTA solve");
@@ -528,10 +537,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int dpad = (a.dim_max + kTile - 1) & ~(kTile - 1);
   double* x = kInPlace ? z : z + dpad;      // U output
   double* scratch = x + dpad;               // [workers][kGroupEntries]
-  double* rbuf = scratch + kWorkers * kGroupEntries;  // solver: the tile's residuals
+  // (a remote CTA of a cluster has kWarps - 1 workers)
+  constexpr int kScratchSlots = kCl ? kWarps - 1 : kWorkers;
+  // solver: the tile's residuals (one buffer per solver warp)
+  double* rbuf = scratch + kScratchSlots * kGroupEntries +
+                 (threadIdx.x >> 5 < kSolvers ? (threadIdx.x >> 5) * kTile : 0);
   // kTileBars: tbar[t] completes phase 0 with L tile t, phase 1 with the
   // t-th tile of the U pass
-  uint64_t* tbar = reinterpret_cast<uint64_t*>(rbuf + kTile);
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(scratch + kScratchSlots * kGroupEntries + kSolvers * kTile);
   __shared__ __align__(8) uint64_t bars[kRing];   // near item landed (TMA)
   __shared__ __align__(8) uint64_t empty[kRing];  // near item consumed (producer variant)
   __shared__ int done_l, done_u;
@@ -616,8 +629,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const int j = lane;
 
   // ================================================================ L pass
-  if (home && warp == 0) {
-    if (lane == 0) {
+  if (home && warp < kSolvers) {
+    if (warp == 0 && lane == 0) {
       for (int q = 0; q < kRing && q < 2 * nt; ++q) issue(q, first_bytes(q));
       // the block's work-item lists go to L2 once
       l2_prefetch(reinterpret_cast<const void*>(reinterpret_cast<unsigned long long>(
@@ -625,7 +638,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
                   16u * static_cast<unsigned>(a.lioff[b + 1] - a.lioff[b]) + 16);
     }
     __syncwarp();
-    for (int t = 0; t < nt; ++t) {
+    for (int t = warp; t < nt; t += kSolvers) {
       const int i = t * kTile + j;
       const bool valid = i < n;
       const int slot = t % kRing;
@@ -639,6 +652,26 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double bi = valid ? (pm ? bperm : T[kTileElems + off + j]) : 0.0;
       const int fm = valid ? meta_int(T, kMetaSeg + j) : 0;  // items | first slot << 8
       const int wn = meta_int(T, kHdr);
+      double far = 0.0;
+      if constexpr (kSolvers > 1) {
+        // off the chain: the far sums, then wait for the other warp's tile
+        far = take_far(part + (fm >> 8), fm & 0xff, pend);
+        __syncwarp();
+        if (t > 0) {
+          if constexpr (kTileBars) {
+            mbar_wait(&tbar[t - 1], 0);
+          } else if constexpr (kWaitL == kWaitValue) {
+            // the previous tile's values are their own readiness (lane j
+            // watches row j; the warp leaves the spin together)
+            const volatile double* pz = z + (t - 1) * kTile + lane;
+            while (__any_sync(0xffffffffu, is_pending(*pz))) {
+            }
+          } else {
+            while (ld_acquire(&done_l) < t) {
+            }
+          }
+        }
+      }
       double nb = 0.0;
       if (wn == kDenseNbr) {
         if (t > 1) nb += neighbour(T + kNbrOff, 0, j, z + (t - 2) * kTile);
@@ -646,7 +679,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       } else {
         nb = ell_neighbours(T, wn, j, z + (t - 2) * kTile);
       }
-      const double far = take_far(part + (fm >> 8), fm & 0xff, pend);
+      if constexpr (kSolvers == 1) far = take_far(part + (fm >> 8), fm & 0xff, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 1] = clock64();
       // z_t = L_tt^-1 r with r = b - (known sums): one dot product per row
@@ -758,8 +791,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   if constexpr (kCl) cluster_sync_all();
 
   // ================================================================ U pass
-  if (home && warp == 0) {
-    for (int tt = 0; tt < nt; ++tt) {
+  if (home && warp < kSolvers) {
+    // item q = nt + tt belongs to warp q & 1 (its ring slot)
+    for (int tt = kSolvers > 1 ? ((warp - nt) & 1) : 0; tt < nt; tt += kSolvers) {
       const int t = nt - 1 - tt;
       const int q = nt + tt;
       const int i = t * kTile + j;
@@ -771,6 +805,23 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const double* T = ring + slot * kSlotElems;
       const int fm = valid ? meta_int(T, kMetaSeg + j) : 0;
       const int wn = meta_int(T, kHdr);
+      double far = 0.0;
+      if constexpr (kSolvers > 1) {
+        far = take_far(part + (fm >> 8), fm & 0xff, pend);
+        __syncwarp();
+        if (tt > 0) {
+          if constexpr (kTileBars) {
+            mbar_wait(&tbar[tt - 1], 1);
+          } else if constexpr (kWaitU == kWaitValue) {
+            const volatile double* px = x + (t + 1) * kTile + lane;
+            while (__any_sync(0xffffffffu, is_pending(*px))) {
+            }
+          } else {
+            while (ld_acquire(&done_u) < tt) {
+            }
+          }
+        }
+      }
       double nb = 0.0;
       if (wn == kDenseNbr) {
         if (tt > 0) nb += neighbour(T + kNbrOff, 0, j, x + (t + 1) * kTile);
@@ -778,7 +829,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       } else {
         nb = ell_neighbours(T, wn, j, x + (t + 1) * kTile);
       }
-      const double far = take_far(part + (fm >> 8), fm & 0xff, pend);
+      if constexpr (kSolvers == 1) far = take_far(part + (fm >> 8), fm & 0xff, pend);
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 1] = clock64();
       // x_t = U_tt^-1 r with r = z - (known sums)
@@ -913,7 +964,7 @@ size_t smem_bytes(int dim_max, int workers, int slots, bool tile_bars = false) {
   return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
                            ((static_cast<size_t>(slots) + 1) & ~static_cast<size_t>(1)) +
                            (kInPlace ? 1 : 2) * dpad +
-                           static_cast<size_t>(workers) * kGroupEntries + kTile +
+                           static_cast<size_t>(workers) * kGroupEntries + 2 * kTile +
                            (tile_bars ? dpad / kTile : 0));  // one mbarrier per tile
 }
 
@@ -1015,6 +1066,14 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return e ? atoi(e) != 0 : true;
   }();
   constexpr size_t kTwoPerSm = (228 * 1024 - 2 * 1024) / 2 - 128;  // less the static part
+  // Solver warps per block (MSCG_TRI_SOLVERS=1|2; see trisolve_kernel): two
+  // where the chain is the bound (few blocks: clusters and 32-warp CTAs)
+  static const int solvers_env = [] {
+    const char* e = getenv("MSCG_TRI_SOLVERS");
+    return e ? atoi(e) : 0;
+  }();
+  const bool two_wide = solvers_env ? solvers_env == 2 : true;    // 32-warp kernels
+  const bool two_k16 = solvers_env ? solvers_env == 2 : false;    // 16-warp kernels
   auto check_smem = [&](size_t smem) {
     if (smem > 227 * 1024)
       throw Error(1, "block_trisolve: block of " + std::to_string(fs.max_dim) +
@@ -1052,7 +1111,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   // with kTrace)
   if (variant == 0 && d > 1024 && cl_env != 0 && npos * 2 <= sms && !trace) {
     // separate z and x (not in place): the U pass needs no cluster fence
-    const size_t smc = smem_bytes<false>(d, 31, ns);
+    const size_t smc = smem_bytes<false>(d, 31, ns);  // 31 workers in the remote CTAs
     check_smem(smc);
     auto config = [&](int c) {
       cudaLaunchConfig_t cfg = {};
@@ -1086,18 +1145,30 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       MSCG_CUDA(cudaGetLastError());
       return true;
     };
-    if (try_size(8, trisolve_kernel<32, 4, 1, false, false, 8>) ||
-        try_size(6, trisolve_kernel<32, 4, 1, false, false, 6>) ||
-        try_size(4, trisolve_kernel<32, 4, 1, false, false, 4>) ||
-        try_size(3, trisolve_kernel<32, 4, 1, false, false, 3>) ||
-        try_size(2, trisolve_kernel<32, 4, 1, false, false, 2>))
+    if (two_wide
+            ? (try_size(8, trisolve_kernel<32, 4, 1, false, false, 8, false, false, 2>) ||
+               try_size(6, trisolve_kernel<32, 4, 1, false, false, 6, false, false, 2>) ||
+               try_size(4, trisolve_kernel<32, 4, 1, false, false, 4, false, false, 2>) ||
+               try_size(3, trisolve_kernel<32, 4, 1, false, false, 3, false, false, 2>) ||
+               try_size(2, trisolve_kernel<32, 4, 1, false, false, 2, false, false, 2>))
+            : (try_size(8, trisolve_kernel<32, 4, 1, false, false, 8>) ||
+               try_size(6, trisolve_kernel<32, 4, 1, false, false, 6>) ||
+               try_size(4, trisolve_kernel<32, 4, 1, false, false, 4>) ||
+               try_size(3, trisolve_kernel<32, 4, 1, false, false, 3>) ||
+               try_size(2, trisolve_kernel<32, 4, 1, false, false, 2>)))
       return;
   }
   if (variant == 0 && npos <= sms && d > 1024 && !trace) {
-    if (tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024)
-      launch(trisolve_kernel<32, 4, 1, true, false, 1, true>, 32, smem_bytes<true>(d, 31, ns, true));
-    else
+    if (tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024) {
+      if (two_wide)
+        launch(trisolve_kernel<32, 4, 1, true, false, 1, true, false, 2>, 32,
+               smem_bytes<true>(d, 30, ns, true));
+      else
+        launch(trisolve_kernel<32, 4, 1, true, false, 1, true>, 32,
+               smem_bytes<true>(d, 31, ns, true));
+    } else {
       launch(trisolve_kernel<32, 4, 1, true, false>, 32, smem_bytes<true>(d, 31, ns));
+    }
     MSCG_CUDA(cudaGetLastError());
     return;
   }
@@ -1121,9 +1192,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     check_smem(smem_bytes<true>(d, 31, ns));
     {
       const bool tb = tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm;
-      auto k16 = tb ? trisolve_kernel<16, 4, 2, true, false, 1, true>
+      auto k16 = tb ? (two_k16 ? trisolve_kernel<16, 4, 2, true, false, 1, true, false, 2>
+                               : trisolve_kernel<16, 4, 2, true, false, 1, true>)
                     : trisolve_kernel<16, 4, 2, true, false>;
-      const size_t sm16 = smem_bytes<true>(d, 15, ns, tb);
+      const size_t sm16 = smem_bytes<true>(d, tb && two_k16 ? 14 : 15, ns, tb);
       ensure_smem(reinterpret_cast<const void*>(k16), sm16);
       k16<<<head, 16 * 32, sm16, s>>>(a, rhs, out, sub);
       MSCG_CUDA(cudaGetLastError());
@@ -1132,9 +1204,10 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       TriArgs at = a;
       at.pos0 = pos0 + head;
       const bool tb = tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024;
-      auto k32 = tb ? trisolve_kernel<32, 4, 1, true, false, 1, true>
+      auto k32 = tb ? (two_wide ? trisolve_kernel<32, 4, 1, true, false, 1, true, false, 2>
+                                : trisolve_kernel<32, 4, 1, true, false, 1, true>)
                     : trisolve_kernel<32, 4, 1, true, false>;
-      const size_t sm32 = smem_bytes<true>(d, 31, ns, tb);
+      const size_t sm32 = smem_bytes<true>(d, tb && two_wide ? 30 : 31, ns, tb);
       ensure_smem(reinterpret_cast<const void*>(k32), sm32);
       k32<<<tail, 32 * 32, sm32, fs.tail_stream>>>(at, rhs, out, sub);
       MSCG_CUDA(cudaGetLastError());
@@ -1144,17 +1217,8 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     return;
   }
   switch (variant) {
-    case 1:  // 3 CTAs/SM: 12 warps
-      launch(trisolve_kernel<12, 4, 3, true, false>, 12, smem_bytes<true>(d, 11, ns));
-      break;
     case 2:  // producer warp issues the near tiles, 14 workers
       launch(trisolve_kernel<16, 4, 2, true, true>, 16, smem_bytes<true>(d, 14, ns));
-      break;
-    case 4:  // 8 far entries in flight per lane
-      launch(trisolve_kernel<16, 8, 2, true, false>, 16, smem_bytes<true>(d, 15, ns));
-      break;
-    case 6:  // 14 warps (72 registers): 13 workers, 6 far entries in flight per lane (~1 % either way)
-      launch(trisolve_kernel<14, 6, 2, true, false>, 14, smem_bytes<true>(d, 13, ns));
       break;
     case 3:  // separate z and x vectors
       launch(trisolve_kernel<16, 4, 2, false, false>, 16, smem_bytes<false>(d, 15, ns));
@@ -1163,6 +1227,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       if (trace && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
         launch(trisolve_kernel<16, 4, 2, true, false, 1, true, true>, 16,
                smem_bytes<true>(d, 15, ns, true));
+      else if (tb_env && two_k16 && smem_bytes<true>(d, 14, ns, true) <= kTwoPerSm)
+        launch(trisolve_kernel<16, 4, 2, true, false, 1, true, false, 2>, 16,
+               smem_bytes<true>(d, 14, ns, true));
       else if (tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
         launch(trisolve_kernel<16, 4, 2, true, false, 1, true>, 16,
                smem_bytes<true>(d, 15, ns, true));
