@@ -1,16 +1,17 @@
-"""Worker-time breakdown of a trace written by tools/trace_dsolve.py.
+"""Worker-side view of a trace written by tools/trace_dsolve.py (block 0).
 
-Per pass, sums over the 15 worker warps of block 0:
-  need  - waiting for the item's input tiles (solver progress),
-  dot   - loading + multiplying the item's far entries,
-  pub   - waiting for a free slot in the partial-sum ring,
-and the bytes each pass streamed, against the pass duration.
+Per pass: items, their busy time (from the later of start and readiness to
+the end of the dot), the workers' busy fraction per twentieth of the pass and
+the distribution of `need`.  The U items are those started after the L pass
+ended.
+
+    python tools/trace_workers.py gpurun_out/trace_cfg5.npz [workers=15]
 """
 import sys
 
 import numpy as np
 
-KW = 15
+KW = int(sys.argv[2]) if len(sys.argv) > 2 else 15
 z = np.load(sys.argv[1])
 buf = z["trace"].astype(np.int64)
 n = len(z["unnz"])
@@ -18,42 +19,31 @@ nt = (n + 31) // 32
 t = buf[: 8 * nt].reshape(-1, 4)
 base = t[0, 0]
 t = t - base
-if "nitems" in z:
-    last = int(z["nitems"])
-    items = buf[8 * nt: 8 * nt + 4 * last].reshape(-1, 4)
-else:
-    items = buf[8 * nt:].reshape(-1, 4)
-    valid = items[:, 0] != 0
-    last = np.nonzero(valid)[0].max() + 1
-    items = items[:last]
-meta = items[:, 3]
+items = buf[8 * nt:].reshape(-1, 4)
+valid = np.nonzero(items[:, 0] != 0)[0]
+it = items[: valid.max() + 1]
+meta = it[:, 3]
 need = meta >> 32
-row = (meta & 0xffffffff) >> 3
-st, de, pe = items[:, 0] - base, items[:, 1] - base, items[:, 2] - base
-# split L / U lists: the U list starts where rows stop ascending from the tail
-lrows = np.diff(row)
-cut = np.nonzero(lrows < -40)[0]
-nl = int(cut[0]) + 1 if len(cut) else last
-for name, sl, q0 in (("L", slice(0, nl), 0), ("U", slice(nl, last), nt)):
-    s, d, p, nd = st[sl], de[sl], pe[sl], need[sl]
+st, de = it[:, 0] - base, it[:, 1] - base
+l_end = t[nt - 1, 2]
+nl = int(np.nonzero(st >= l_end - 1000)[0][0])
+print(f"L pass {l_end} cycles, U pass {t[2 * nt - 1, 2] - l_end}; items L {nl} U {len(it) - nl}")
+for name, sl, q0 in (("L", slice(0, nl), 0), ("U", slice(nl, len(it)), nt)):
+    s, d, nd = st[sl], de[sl], need[sl]
     if len(s) == 0:
         continue
     ready = np.where(nd > 0, t[np.clip(q0 + nd - 1, 0, 2 * nt - 1), 2], 0)
-    wait_need = np.clip(ready - s, 0, None)
-    dot = d - np.maximum(s, ready)
-    pub = p - d
-    p0 = 0 if name == "L" else t[nt - 1, 2]
-    p1 = t[nt - 1, 2] if name == "L" else t[2 * nt - 1, 2]
-    dur = p1 - p0
-    busy = KW * dur
-    print(f"{name}: pass {dur} cyc, {len(s)} items; worker time share: need "
-          f"{wait_need.sum() / busy:.2f} dot {dot.sum() / busy:.2f} pub {pub.sum() / busy:.2f}"
-          f" idle {1 - (wait_need.sum() + dot.sum() + pub.sum()) / busy:.2f}; median dot "
-          f"{np.median(dot):.0f} cyc")
-    # coarse timeline: fraction of workers computing per 1/10 of the pass
-    edges = np.linspace(p0, p1, 11)
+    busy = d - np.maximum(ready, s)
+    print(f"{name}: {len(s)} items, busy median {np.median(busy):.0f} mean {busy.mean():.0f} cycles, "
+          f"sum/{KW} workers {busy.sum() / KW:.0f}; started after ready by median "
+          f"{np.median(s - ready):.0f} cycles")
+    p0 = 0 if name == "L" else l_end
+    p1 = l_end if name == "L" else t[2 * nt - 1, 2]
+    edges = np.linspace(p0, p1, 21)
     occ = []
     for a, b in zip(edges[:-1], edges[1:]):
         lo, hi = np.maximum(np.maximum(s, ready), a), np.minimum(d, b)
         occ.append(np.clip(hi - lo, 0, None).sum() / (KW * (b - a)))
-    print("   computing fraction per tenth:", " ".join(f"{o:.2f}" for o in occ))
+    print("   busy fraction per 1/20:", " ".join(f"{o:.2f}" for o in occ))
+    print("   need quantiles (0,10,25,50,75,90,100 %):",
+          np.percentile(nd, [0, 10, 25, 50, 75, 90, 100]).astype(int).tolist())
