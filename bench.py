@@ -629,12 +629,12 @@ def main():
                              _capi.MEM_HOST, C.byref(st))
             msc.msc._check(rc, st)
 
-        for _ in range(2):
+        for _ in range(3):
             e2e_step()
         if pg:
             pg.barrier()
         te0 = time.perf_counter()
-        ke = max(3, min(args.steps, 10))
+        ke = max(3, min(args.steps, 20))
         for _ in range(ke):
             e2e_step()
         te = time.perf_counter() - te0

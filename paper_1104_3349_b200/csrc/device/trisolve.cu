@@ -516,7 +516,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     trisolve_kernel(TriArgs a, const double* __restrict__ rhs, double* __restrict__ out,
                     const double* __restrict__ sub) {
   static_assert(kSolvers == 1 || (kSolvers == 2 && kRing == 2 && !kProducer),
-                "two solvers: one per ring slot");
+                "two solvers: items alternate between them");
+  // Ring slots.  One solver: kRing (the next-but-one tile is in flight while
+  // a tile is solved).  Two solvers (one CTA per SM, shared memory to spare):
+  // two slots per warp — with one, a warp's refill, issued when its tile
+  // ends, had a full DRAM round trip before the warp's next tile and was the
+  // bound of the chain.  Copy sizes then come from the width tables (the
+  // tile headers only carry the size of the item kRing ahead).
+  constexpr int kDepth = kSolvers == 2 ? 4 : kRing;
   constexpr int kFirstWorker = kProducer ? 2 : kSolvers;
   constexpr int kWorkers = kWarps - kFirstWorker;
   constexpr bool kCl = kCluster > 1;
@@ -531,8 +538,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   // others (warp 0 of a remote CTA pulls the solution, see below)
   constexpr int kAllWorkers = kWorkers + (kCluster - 1) * (kWarps - 1);
   extern __shared__ __align__(128) double sm[];
-  double* ring = sm;                        // kRing slots: tile | meta | rhs slice
-  double* part = ring + kRing * kSlotElems; // far sums, one slot per work item
+  double* ring = sm;                        // kDepth slots: tile | meta | rhs slice
+  double* part = ring + kDepth * kSlotElems; // far sums, one slot per work item
   double* z = part + ((a.max_slots + 1) & ~1);  // L output
   const int dpad = (a.dim_max + kTile - 1) & ~(kTile - 1);
   double* x = kInPlace ? z : z + dpad;      // U output
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   // kTileBars: tbar[t] completes phase 0 with L tile t, phase 1 with the
   // t-th tile of the U pass
   uint64_t* tbar = reinterpret_cast<uint64_t*>(scratch + kScratchSlots * kGroupEntries + kSolvers * kTile);
-  __shared__ __align__(8) uint64_t bars[kRing];   // near item landed (TMA)
+  __shared__ __align__(8) uint64_t bars[kDepth];  // near item landed (TMA)
   __shared__ __align__(8) uint64_t empty[kRing];  // near item consumed (producer variant)
   __shared__ int done_l, done_u;
 
@@ -579,22 +586,20 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   if (threadIdx.x == 0) {
     done_l = 0;
     done_u = 0;
-    for (int r = 0; r < kRing; ++r) {
-      mbar_init(&bars[r], 1);
-      mbar_init(&empty[r], 1);
-    }
+    for (int r = 0; r < kDepth; ++r) mbar_init(&bars[r], 1);
+    for (int r = 0; r < kRing; ++r) mbar_init(&empty[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if constexpr (kCl) cluster_sync_all();  // the home's sentinels are in place
 
   // Near item q: q < nt -> L tile q (+ rhs slice), else U tile 2nt-1-q.
-  // Item q lives in slot q % kRing, phase (q / kRing) & 1.
+  // Item q lives in slot q % kDepth, phase (q / kDepth) & 1.
   const int* pm = a.perm ? a.perm + r0 : nullptr;
   // `bytes`: the item's used prefix (its predecessor kRing items earlier
   // carries it in its header; the first kRing come from the width tables).
   auto issue = [&](int q, unsigned bytes) {  // solver lane 0
-    const int slot = q % kRing;
+    const int slot = q % kDepth;
     double* dst = ring + slot * kSlotElems;
     const bool lpass = q < nt;
     const int t = lpass ? q : 2 * nt - 1 - q;
@@ -631,7 +636,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   // ================================================================ L pass
   if (home && warp < kSolvers) {
     if (warp == 0 && lane == 0) {
-      for (int q = 0; q < kRing && q < 2 * nt; ++q) issue(q, first_bytes(q));
+      for (int q = 0; q < kDepth && q < 2 * nt; ++q) issue(q, first_bytes(q));
       // the block's work-item lists go to L2 once
       l2_prefetch(reinterpret_cast<const void*>(reinterpret_cast<unsigned long long>(
                       a.litems + a.lioff[b]) & ~15ull),
@@ -641,11 +646,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     for (int t = warp; t < nt; t += kSolvers) {
       const int i = t * kTile + j;
       const bool valid = i < n;
-      const int slot = t % kRing;
+      const int slot = t % kDepth;
       // Schur blocks (row_perm): gather the right-hand side directly.
       double bperm = 0.0;
       if (pm && valid) bperm = rhs[r0 + pm[i]];
-      mbar_wait(&bars[slot], (t / kRing) & 1);
+      // deep ring: the refill's size, loaded now, used when the tile ends
+      unsigned nbytes = 0;
+      if (kDepth != kRing && t + kDepth < 2 * nt) nbytes = first_bytes(t + kDepth);
+      mbar_wait(&bars[slot], (t / kDepth) & 1);
       if (tr && lane == 0) tr[4 * t + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
       const int off = static_cast<int>((reinterpret_cast<unsigned long long>(rhs + r0 + t * kTile) & 15) >> 3);
@@ -699,7 +707,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         else
           *reinterpret_cast<volatile int*>(&done_l) = t + 1;
         if (tr) tr[4 * t + 2] = clock64();
-        if (!kProducer && t + kRing < 2 * nt) issue(t + kRing, next_bytes(t));
+        if (!kProducer && t + kDepth < 2 * nt)
+          issue(t + kDepth, kDepth != kRing ? nbytes : next_bytes(t));
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * t + 3] = clock64();
@@ -798,9 +807,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       const int q = nt + tt;
       const int i = t * kTile + j;
       const bool valid = i < n;
-      const int slot = q % kRing;
+      const int slot = q % kDepth;
       const double zi = valid ? z[i] : 0.0;
-      mbar_wait(&bars[slot], (q / kRing) & 1);
+      unsigned nbytes = 0;
+      if (kDepth != kRing && q + kDepth < 2 * nt) nbytes = first_bytes(q + kDepth);
+      mbar_wait(&bars[slot], (q / kDepth) & 1);
       if (tr && lane == 0) tr[4 * q + 0] = clock64();
       const double* T = ring + slot * kSlotElems;
       const int fm = valid ? meta_int(T, kMetaSeg + j) : 0;
@@ -854,7 +865,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
           *reinterpret_cast<volatile int*>(&done_u) = tt + 1;
         }
         if (tr) tr[4 * q + 2] = clock64();
-        if (!kProducer && q + kRing < 2 * nt) issue(q + kRing, next_bytes(q));
+        if (!kProducer && q + kDepth < 2 * nt)
+          issue(q + kDepth, kDepth != kRing ? nbytes : next_bytes(q));
       }
       __syncwarp();
       if (tr && lane == 0) tr[4 * q + 3] = clock64();
@@ -959,9 +971,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 }
 
 template <bool kInPlace>
-size_t smem_bytes(int dim_max, int workers, int slots, bool tile_bars = false) {
+size_t smem_bytes(int dim_max, int workers, int slots, bool tile_bars = false, int depth = kRing) {
   const size_t dpad = (static_cast<size_t>(dim_max) + kTile - 1) & ~static_cast<size_t>(kTile - 1);
-  return sizeof(double) * (static_cast<size_t>(kRing) * kSlotElems +
+  return sizeof(double) * (static_cast<size_t>(depth) * kSlotElems +
                            ((static_cast<size_t>(slots) + 1) & ~static_cast<size_t>(1)) +
                            (kInPlace ? 1 : 2) * dpad +
                            static_cast<size_t>(workers) * kGroupEntries + 2 * kTile +
@@ -1041,7 +1053,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   a.sleep_ns = sleep_ns;
   static const unsigned sleep_max = [] {
     const char* e = getenv("MSCG_TRI_SLEEP_MAX");
-    return e ? static_cast<unsigned>(atoi(e)) : 512u;
+    return e ? static_cast<unsigned>(atoi(e)) : 256u;
   }();
   a.sleep_max = sleep_max < sleep_ns ? sleep_ns : sleep_max;
   static const int pf_items = [] {
@@ -1111,7 +1123,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   // with kTrace)
   if (variant == 0 && d > 1024 && cl_env != 0 && npos * 2 <= sms && !trace) {
     // separate z and x (not in place): the U pass needs no cluster fence
-    const size_t smc = smem_bytes<false>(d, 31, ns);  // 31 workers in the remote CTAs
+    // (31 workers in the remote CTAs; two solvers need the four-slot ring)
+    const bool two_cl = two_wide && smem_bytes<false>(d, 31, ns, false, 4) <= 227 * 1024;
+    const size_t smc = smem_bytes<false>(d, 31, ns, false, two_cl ? 4 : kRing);
     check_smem(smc);
     auto config = [&](int c) {
       cudaLaunchConfig_t cfg = {};
@@ -1145,7 +1159,7 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       MSCG_CUDA(cudaGetLastError());
       return true;
     };
-    if (two_wide
+    if (two_cl
             ? (try_size(8, trisolve_kernel<32, 4, 1, false, false, 8, false, false, 2>) ||
                try_size(6, trisolve_kernel<32, 4, 1, false, false, 6, false, false, 2>) ||
                try_size(4, trisolve_kernel<32, 4, 1, false, false, 4, false, false, 2>) ||
@@ -1160,9 +1174,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
   }
   if (variant == 0 && npos <= sms && d > 1024 && !trace) {
     if (tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024) {
-      if (two_wide)
+      if (two_wide && smem_bytes<true>(d, 30, ns, true, 4) <= 227 * 1024)
         launch(trisolve_kernel<32, 4, 1, true, false, 1, true, false, 2>, 32,
-               smem_bytes<true>(d, 30, ns, true));
+               smem_bytes<true>(d, 30, ns, true, 4));
       else
         launch(trisolve_kernel<32, 4, 1, true, false, 1, true>, 32,
                smem_bytes<true>(d, 31, ns, true));
@@ -1192,10 +1206,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
     check_smem(smem_bytes<true>(d, 31, ns));
     {
       const bool tb = tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm;
-      auto k16 = tb ? (two_k16 ? trisolve_kernel<16, 4, 2, true, false, 1, true, false, 2>
-                               : trisolve_kernel<16, 4, 2, true, false, 1, true>)
+      const bool two16 = tb && two_k16 && smem_bytes<true>(d, 14, ns, true, 4) <= 227 * 1024;
+      auto k16 = tb ? (two16 ? trisolve_kernel<16, 4, 2, true, false, 1, true, false, 2>
+                             : trisolve_kernel<16, 4, 2, true, false, 1, true>)
                     : trisolve_kernel<16, 4, 2, true, false>;
-      const size_t sm16 = smem_bytes<true>(d, tb && two_k16 ? 14 : 15, ns, tb);
+      const size_t sm16 = two16 ? smem_bytes<true>(d, 14, ns, true, 4) : smem_bytes<true>(d, 15, ns, tb);
       ensure_smem(reinterpret_cast<const void*>(k16), sm16);
       k16<<<head, 16 * 32, sm16, s>>>(a, rhs, out, sub);
       MSCG_CUDA(cudaGetLastError());
@@ -1204,10 +1219,11 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       TriArgs at = a;
       at.pos0 = pos0 + head;
       const bool tb = tb_env && smem_bytes<true>(d, 31, ns, true) <= 227 * 1024;
-      auto k32 = tb ? (two_wide ? trisolve_kernel<32, 4, 1, true, false, 1, true, false, 2>
-                                : trisolve_kernel<32, 4, 1, true, false, 1, true>)
+      const bool two = tb && two_wide && smem_bytes<true>(d, 30, ns, true, 4) <= 227 * 1024;
+      auto k32 = tb ? (two ? trisolve_kernel<32, 4, 1, true, false, 1, true, false, 2>
+                           : trisolve_kernel<32, 4, 1, true, false, 1, true>)
                     : trisolve_kernel<32, 4, 1, true, false>;
-      const size_t sm32 = smem_bytes<true>(d, tb && two_wide ? 30 : 31, ns, tb);
+      const size_t sm32 = two ? smem_bytes<true>(d, 30, ns, true, 4) : smem_bytes<true>(d, 31, ns, tb);
       ensure_smem(reinterpret_cast<const void*>(k32), sm32);
       k32<<<tail, 32 * 32, sm32, fs.tail_stream>>>(at, rhs, out, sub);
       MSCG_CUDA(cudaGetLastError());
@@ -1227,9 +1243,9 @@ void block_trisolve(const FactorSet& fs, const double* rhs, double* out, const d
       if (trace && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
         launch(trisolve_kernel<16, 4, 2, true, false, 1, true, true>, 16,
                smem_bytes<true>(d, 15, ns, true));
-      else if (tb_env && two_k16 && smem_bytes<true>(d, 14, ns, true) <= kTwoPerSm)
+      else if (tb_env && two_k16 && smem_bytes<true>(d, 14, ns, true, 4) <= 227 * 1024)
         launch(trisolve_kernel<16, 4, 2, true, false, 1, true, false, 2>, 16,
-               smem_bytes<true>(d, 14, ns, true));
+               smem_bytes<true>(d, 14, ns, true, 4));
       else if (tb_env && smem_bytes<true>(d, 15, ns, true) <= kTwoPerSm)
         launch(trisolve_kernel<16, 4, 2, true, false, 1, true>, 16,
                smem_bytes<true>(d, 15, ns, true));

@@ -28,6 +28,16 @@ import numpy as np
 from . import _capi as api
 
 
+
+def _destroy(name, h):
+    """Handle release for __del__: at interpreter shutdown the module globals
+    may already be gone, and a destructor must not raise."""
+    try:
+        getattr(api.lib(), name)(h)
+    except Exception:  # noqa: BLE001
+        pass
+
+
 class MscError(RuntimeError):
     pass
 
@@ -147,7 +157,7 @@ class Context:
 
     def __del__(self):
         if getattr(self, "h", None):
-            api.lib().mscg_ctx_destroy(self.h)
+            _destroy("mscg_ctx_destroy", self.h)
             self.h = None
 
 
@@ -199,7 +209,7 @@ class DeviceMatrix:
 
     def __del__(self):
         if getattr(self, "_owned", False) and getattr(self, "h", None):
-            api.lib().mscg_csr_destroy(self.h)
+            _destroy("mscg_csr_destroy", self.h)
             self.h = None
 
 
@@ -271,7 +281,7 @@ class DeviceFactors(TriangularFactors):
 
     def __del__(self):
         if getattr(self, "h", None):
-            api.lib().mscg_factors_destroy(self.h)
+            _destroy("mscg_factors_destroy", self.h)
             self.h = None
 
 
@@ -396,7 +406,7 @@ class MscPreconditioner:
 
     def __del__(self):
         if getattr(self, "h", None):
-            api.lib().mscg_precond_destroy(self.h)
+            _destroy("mscg_precond_destroy", self.h)
             self.h = None
 
 
@@ -484,7 +494,7 @@ class Problem:
 
     def __del__(self):
         if getattr(self, "h", None):
-            api.lib().mscg_problem_destroy(self.h)
+            _destroy("mscg_problem_destroy", self.h)
             self.h = None
 
 
@@ -641,7 +651,7 @@ class PreconditionerShard:
 
     def __del__(self):
         if getattr(self, "h", None):
-            api.lib().mscg_precond_destroy(self.h)
+            _destroy("mscg_precond_destroy", self.h)
             self.h = None
 
 
